@@ -1,0 +1,191 @@
+/*
+ * scorepic_b200.h — C ABI of the B200-native (sm_100a) scorepic hot path.
+ *
+ * Every pointer is a DEVICE pointer unless stated otherwise; every op takes the caller's
+ * cudaStream_t as `void* stream`, never allocates (scratch is passed in, sized by the
+ * matching *_scratch_bytes query), never synchronizes, and returns 0 or a negative
+ * SPIC_ERR_* status. Data-dependent error conditions (non-finite state, isolated blob
+ * particles, training divergence) are reported through a device int32 flag array
+ * `flags[SPIC_NFLAGS]` that the host reads once per step.
+ *
+ * Particle layout on device ("pid order" = the reference's particle index order):
+ *   x  float[n]                       positions
+ *   v  float[dv][ldv]                 velocity planes (SoA), plane k at v + k*ldv
+ *   w  float[n]                       weights
+ * Cell-sorted working copies ("sorted order", produced by spic_bin):
+ *   xv float4[n] = (x', v0, v1, v2)   x' = x, or x - L for the % M quirk particle
+ *   sw float4[n] = (s0, s1, s2, w)    scores written by the estimator, weight by spic_bin
+ *   perm int32[n]                     sorted position -> pid
+ * For dv == 2 the unused lanes are zero.
+ *
+ * Each entry point names the reference function(s) it replaces
+ * (/root/reference/pkg/src/scorepic/<file>:<line>).
+ */
+#ifndef SCOREPIC_B200_H
+#define SCOREPIC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SPIC_OK = 0,
+  SPIC_ERR_ARG = -1,          /* invalid argument (size, dv, M, H out of range) */
+  SPIC_ERR_SCRATCH = -2,      /* scratch buffer too small */
+  SPIC_ERR_UNSUPPORTED = -3,  /* valid in the reference, not supported by this build */
+  SPIC_ERR_CUDA = -1000       /* -1000 - cudaError_t */
+};
+
+/* device flag indices (int32 each; nonzero = condition seen) */
+enum {
+  SPIC_FLAG_NONFINITE_X = 0,   /* ValueError("non-finite position"), state.py:23-24 */
+  SPIC_FLAG_NONFINITE_V = 1,   /* ValueError("non-finite particle state"), state.py:47-49 */
+  SPIC_FLAG_BAD_SCORE = 2,     /* ValueError("invalid score input"), collision.py:95-96 */
+  SPIC_FLAG_ISOLATED = 3,      /* ValueError("isolated particle ..."), score.py:518-521 */
+  SPIC_FLAG_TRAIN_FATAL = 4,   /* RuntimeError("training divergence"), score.py:584-585 */
+  SPIC_FLAG_LR_HALVINGS = 5,   /* count of restore-and-halve events, score.py:579-583 */
+  SPIC_FLAG_NON_NEUTRAL = 6,   /* ValueError("non-neutral plasma"), pic.py:126-127 */
+  SPIC_FLAG_NONFINITE_FIELD = 7, /* ValueError("non-finite field state"), state.py:75-78 */
+  SPIC_NFLAGS = 8
+};
+
+/* ---- version / build ------------------------------------------------------------------ */
+int spic_version(void);
+/* number of SMs the launch heuristics assume (148 on B200) */
+int spic_num_sms(void);
+
+/* ---- binning (replaces Grid.cell_of pic.py:27-30, build_cell_index collision.py:39-46) -- */
+/* cell[i] = min(floor(x_i/eta) mod M, M-1), float64 arithmetic on the float32 input. */
+int spic_cell_of(const float* x, int64_t n, double eta, int32_t M, int32_t* cell, void* stream);
+
+size_t spic_bin_scratch_bytes(int64_t n, int32_t M, int32_t S);
+/* Stable counting sort by key = (cell, sub) where sub = floor(frac(x/eta)*S).
+ * S == 1 gives exactly np.argsort(cell_of(x), kind="stable") (the reference CellIndex).
+ * Outputs: perm[n] (sorted position -> pid), cell_start[M+1], sub_start[M*S+1] (nullable).
+ * Optional fused gather (all nullable): xv[n], sw[n] (w lane only) in sorted order. */
+int spic_bin(const float* x, const float* v, int64_t ldv, const float* w, int64_t n, int32_t dv,
+             double eta, int32_t M, int32_t S, int32_t* perm, int32_t* cell_start,
+             int32_t* sub_start, float* xv, float* sw, void* scratch, size_t scratch_bytes,
+             void* stream);
+/* Gather pid-order scores s[dv][lds] into the sorted records sw (lanes 0..dv-1). */
+int spic_gather_scores(const float* s, int64_t lds, const int32_t* perm, int64_t n, int32_t dv,
+                       float* sw, int32_t* flags, void* stream);
+
+/* ---- Landau collision (replaces _collision_cell collision.py:49-89, collision_force
+ *      collision.py:92-110, collision_push collision.py:113-116) --------------------------- */
+size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nsplit);
+/* U (sorted order, float[dv][n]) for all targets against their 3-cell stencil.
+ * gamma must be -3 (dv=3) or -2 (dv=2) or any value (generic pow path).
+ * uniform_w > 0: all weights equal uniform_w (sw.w ignored). nsplit: j-window split
+ * factor (0 = automatic). */
+int spic_landau(const float* xv, const float* sw, int64_t n, int32_t dv, const int32_t* cell_start,
+                const int32_t* sub_start, int32_t M, int32_t S, double eta, double gamma,
+                float uniform_w, int32_t nsplit, float* U_sorted, void* scratch,
+                size_t scratch_bytes, void* stream);
+/* Sum nsplit partial U planes [nsplit][dv][n] into U_sorted in a fixed order. */
+int spic_landau_fold(const float* U_part, int32_t nsplit, int32_t dv, int64_t n, float* U_sorted,
+                     void* stream);
+/* Epilogue: U_pid[:, perm[k]] = U_sorted[:, k] (nullable), v[:, perm[k]] -= nu_dt*U (if
+ * nu_dt != 0), and diagnostics partial sums; red_out (float64, nullable) receives
+ * [H_dot = sum w s.U, E_K = 1/2 sum w |v|^2 (post-push), P_0..P_{dv-1}]. */
+int spic_collision_epilogue(const float* U_sorted, const float* sw, const int32_t* perm,
+                            int64_t n, int32_t dv, float nu_dt, float* v, int64_t ldv,
+                            float* U_pid, int64_t ldu, double* red_out, int32_t* flags,
+                            void* scratch, size_t scratch_bytes, void* stream);
+/* number of ordered live pairs |min-image dx| < eta over the stencil (the pair-rate unit) */
+int spic_count_live_pairs(const float* xv, int64_t n, const int32_t* cell_start, int32_t M,
+                          double eta, unsigned long long* count, void* stream);
+
+/* ---- blob KDE score (replaces _blob_cell score.py:453-490, silverman_bandwidth
+ *      score.py:493-500, blob_score score.py:503-523) -------------------------------------- */
+size_t spic_blob_scratch_bytes(int64_t n, int32_t M, int32_t dv);
+/* Writes s into sw lanes 0..dv-1 (sorted order). bandwidth <= 0: Silverman per cell over
+ * the stencil. On den <= 0 / non-finite: SPIC_FLAG_ISOLATED and *bad_pid = pid of the first
+ * offending particle in (cell, pid) order (bad_pid must be preset to INT64_MAX). */
+int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_t n, int32_t dv,
+              const int32_t* cell_start, const int32_t* sub_start, int32_t M, int32_t S, double eta,
+              double bandwidth, float uniform_w, float* h_cell, long long* bad_pid, int32_t* flags,
+              void* scratch, size_t scratch_bytes, void* stream);
+
+/* ---- SBTM score network (replaces mlp_forward score.py:80-86, _ism_kernel_shared
+ *      score.py:128-187, _ism_kernel_perparticle score.py:190-251, ism_loss_and_grad
+ *      score.py:303-338, AdamW.step score.py:371-386, sbtm_update score.py:547-588,
+ *      _mse_kernel score.py:254-300) ---------------------------------------------------------
+ * Parameter vector layout (float64 master and float32 working copy), P = 8H+... :
+ *   W1[H][1+dv] row-major, b1[H], W2[dv][H] row-major, b2[dv]. */
+int64_t spic_mlp_num_params(int32_t H, int32_t dv);
+/* s = W2 softsign(W1 [x*x_scale; v] + b1) + b2. Input either sorted records (xv != NULL;
+ * x' < 0 is mapped back by +L = 1/x_scale) or pid-order planes (x, v, ldv). Output either
+ * into sw lanes (sw != NULL) or planes s[dv][lds]. */
+int spic_mlp_forward(const float* params32, int32_t H, int32_t dv, const float* xv,
+                     const float* x, const float* v, int64_t ldv, int64_t n, float x_scale,
+                     float* sw, float* s, int64_t lds, void* stream);
+size_t spic_ism_scratch_bytes(int64_t n, int32_t H, int32_t dv);
+/* Per-block float64 partial sums of [loss, gW1, gb1, gW2, gb2, Phi] into scratch.
+ * mode 0: exact divergence (coefficients sum_i W2[i,h] W1[h,1+i] formed in-kernel);
+ * mode 1: shared Hutchinson probe Z = z[dv] (float32, device);
+ * mode 2: per-particle Rademacher probes Z[dv][ldz];
+ * mode 3: weighted MSE to target Z[dv][ldz] with weights w*inv_wsum (pretraining).
+ * Input: sorted records xv/sw (xv != NULL; x' < 0 mapped back by +L) or planes x, v, w.
+ * idx (nullable) maps kernel particle p to the source row of the planes and of Z. */
+int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv, int32_t mode,
+                         const float* xv, const float* sw, const float* x, const float* v,
+                         int64_t ldv, const float* w, int64_t n, float x_scale, const float* Z,
+                         int64_t ldz, const int32_t* idx, double inv_wsum, void* scratch,
+                         size_t scratch_bytes, void* stream);
+/* Single-CTA finalize of one ISM/MSE step: fixed-order reduction of the partials, the
+ * coefficient-dependence terms of the divergence (div_mode 0 exact, 1 shared Hutchinson with
+ * z_shared float32[dv]; 2 per-particle and 3 MSE have none), then (apply_step != 0) AdamW on
+ * the float64 master parameters with the reference's restore-and-halve recovery.
+ * opt_state (float64[4]) = {t, lr_current, base_lr, 0}; reset_lr restarts lr_current from
+ * base_lr. Writes params64/m/v2 (in place), params32, grads_out[P] and loss_out (nullable). */
+int spic_sbtm_finalize_ex(const void* scratch, int64_t n, int32_t H, int32_t dv,
+                          int32_t div_mode, const float* z_shared, double* params64, double* m,
+                          double* v2, double* opt_state, double beta1, double beta2, double eps,
+                          double weight_decay, int32_t reset_lr, int32_t apply_step,
+                          float* params32, double* grads_out, double* loss_out, int32_t* flags,
+                          void* stream);
+
+/* Plain AdamW step (ref: score.py:371-386) on a flat float64 vector with precomputed
+ * gradients; opt_state = {t, unused, lr, 0}; t is incremented on device. */
+int spic_adamw_step(double* params64, const double* grads64, double* m, double* v2, int64_t P,
+                    double* opt_state, double beta1, double beta2, double eps,
+                    double weight_decay, float* params32, void* stream);
+
+/* ---- PIC (replaces interpolate_fields pic.py:61-74, lorentz_push pic.py:77-88,
+ *      advance_positions pic.py:91-93 + wrap_position state.py:14-27, deposit
+ *      pic.py:43-58, maxwell_step pic.py:96-110, vpl_field_step pic.py:113-115,
+ *      poisson_solve pic.py:118-134, compute_diagnostics diagnostics.py:20-35) ---------------
+ * Fields are float64 [M] arrays on device (E1, E2, B3); J is float64 [dv][M]. */
+/* interpolate + Lorentz (v += dt(E + v x B)) + x += dt v1 + periodic wrap, in place. */
+int spic_push(float* x, float* v, int64_t ldv, int64_t n, int32_t dv, const double* E1,
+              const double* E2, const double* B3, int32_t M, double eta, float dt,
+              int32_t* flags, void* stream);
+size_t spic_deposit_scratch_bytes(int32_t M, int32_t dv);
+/* rho[M], J[dv][M] from sorted records; then (field_mode 1 = VPL: E1 -= dt J1;
+ * 2 = VML maxwell_step; 0 = none). diag_out (nullable) receives [E_E, E_B, E_l2]. */
+int spic_deposit_field(const float* xv, const float* sw, int64_t n, int32_t dv,
+                       const int32_t* cell_start, int32_t M, double eta, float uniform_w,
+                       double* rho, double* J, int32_t field_mode, double dt, double* E1,
+                       double* E2, double* B3, double* diag_out, int32_t* flags, void* scratch,
+                       size_t scratch_bytes, void* stream);
+/* Standalone field updates (for the operator API). */
+int spic_field_step(double* E1, double* E2, double* B3, const double* J, int32_t M, double eta,
+                    double dt, int32_t field_mode, double* diag_out, int32_t* flags,
+                    void* stream);
+/* E1 = spectral solve of -phi'' = rho - rho_ion, E1 = -phi' (single-CTA float64 DFT). */
+int spic_poisson(const double* rho, double rho_ion, int32_t M, double eta, double* E1,
+                 int32_t* flags, void* stream);
+size_t spic_moments_scratch_bytes(int64_t n);
+/* out (float64): [E_K, P_0..P_{dv-1}, sum w] over pid-order planes; also flags non-finite v. */
+int spic_moments(const float* v, int64_t ldv, const float* w, int64_t n, int32_t dv,
+                 float uniform_w, double* out, int32_t* flags, void* scratch,
+                 size_t scratch_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,532 @@
+// sbtm.cu — the SBTM score network on device: forward pass, implicit-score-matching (ISM)
+// loss + gradient partials, and the deterministic reduction + AdamW finalize.
+//
+// Replaces mlp_forward (ref: score.py:80-86), _ism_kernel_shared (score.py:128-187),
+// _ism_kernel_perparticle (score.py:190-251), _mse_kernel (score.py:254-300),
+// ism_loss_and_grad (score.py:303-338), AdamW.step (score.py:371-386) and the per-step body
+// of sbtm_update incl. its restore-and-halve recovery (score.py:547-588).
+//
+// Network: s(u) = W2 softsign(W1 u + b1) + b2, u = [x/L; v], W1 [H][1+dv], W2 [dv][H].
+// The GEMMs have K = 1+dv = 4 and N = dv = 3, far below any tensor-core tile, so the math
+// runs on the FP32 pipes: one thread per particle for the forward sweep over h, and one
+// thread per hidden unit (x particle group) for the backward/outer-product reductions over
+// a 256-particle chunk staged in shared memory. Chunk sums are float32 and are promoted to
+// float64 per chunk; block partials are float64 and are reduced in a fixed order by a
+// single-CTA finalize that also applies the divergence-coefficient terms and AdamW (float64
+// master parameters). Deterministic for a given (n, grid).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace spic {
+
+constexpr int kIsmNT = 256;     // threads per block == particles per chunk
+constexpr int kIsmBlocksMax = 2 * kNumSMs;
+constexpr int kIsmAcc = 10;     // per (h, group): gW1[4], gb1, gW2[3], Phi, pad
+
+__host__ __device__ inline int64_t n_params(int H, int dv) {
+  return (int64_t)H * (1 + dv) + H + (int64_t)dv * H + dv;
+}
+
+// params32 -> packed smem records per hidden unit: Wp[h] = (W1[h,0..3]),
+// Bp[h] = (b1[h], W2[0,h], W2[1,h], W2[2,h]); pad lanes are zero for dv == 2.
+__device__ __forceinline__ void load_packed(const float* __restrict__ p, int H, int dv,
+                                            float4* Wp, float4* Bp, float* b2) {
+  const float* W1 = p;
+  const float* b1 = W1 + H * (1 + dv);
+  const float* W2 = b1 + H;
+  const float* bb2 = W2 + dv * H;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    float4 a, b;
+    a.x = W1[h * (1 + dv) + 0];
+    a.y = W1[h * (1 + dv) + 1];
+    a.z = W1[h * (1 + dv) + 2];
+    a.w = dv > 2 ? W1[h * (1 + dv) + 3] : 0.f;
+    b.x = b1[h];
+    b.y = W2[h];
+    b.z = W2[H + h];
+    b.w = dv > 2 ? W2[2 * H + h] : 0.f;
+    Wp[h] = a;
+    Bp[h] = b;
+  }
+  if (threadIdx.x < 3) b2[threadIdx.x] = threadIdx.x < dv ? bb2[threadIdx.x] : 0.f;
+}
+
+// ------------------------------------------------------------------------------------------
+// forward: s = W2 softsign(W1 [x*x_scale; v] + b1) + b2
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mlp_forward(
+    const float* __restrict__ params, int H, int dv, const float4* __restrict__ xv,
+    const float* __restrict__ x, const float* __restrict__ v, int64_t ldv, int64_t n,
+    float x_scale, float L, float4* __restrict__ sw, float* __restrict__ s, int64_t lds) {
+  extern __shared__ float4 smem4[];
+  float4* Wp = smem4;
+  float4* Bp = smem4 + H;
+  __shared__ float b2[3];
+  load_packed(params, H, dv, Wp, Bp, b2);
+  __syncthreads();
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    float xn, v0, v1, v2;
+    if (xv) {
+      float4 A = xv[p];
+      xn = A.x < 0.f ? A.x + L : A.x;  // % M quirk records carry x - L
+      v0 = A.y; v1 = A.z; v2 = A.w;
+    } else {
+      xn = x[p];
+      v0 = v[p];
+      v1 = v[ldv + p];
+      v2 = dv > 2 ? v[2 * ldv + p] : 0.f;
+    }
+    xn *= x_scale;
+    float s0 = b2[0], s1 = b2[1], s2 = b2[2];
+#pragma unroll 4
+    for (int h = 0; h < H; ++h) {
+      const float4 a = Wp[h];
+      const float4 b = Bp[h];
+      float z = fmaf(a.w, v2, fmaf(a.z, v1, fmaf(a.y, v0, fmaf(a.x, xn, b.x))));
+      float act = z * __frcp_rn(1.f + fabsf(z));
+      s0 = fmaf(b.y, act, s0);
+      s1 = fmaf(b.z, act, s1);
+      s2 = fmaf(b.w, act, s2);
+    }
+    if (sw) {
+      float4 r = sw[p];
+      r.x = s0; r.y = s1; r.z = dv > 2 ? s2 : 0.f;
+      sw[p] = r;
+    } else {
+      s[p] = s0;
+      s[lds + p] = s1;
+      if (dv > 2) s[2 * lds + p] = s2;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// ISM / MSE partials. MODE 0 exact, 1 shared Hutchinson, 2 per-particle probes, 3 MSE.
+// ------------------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kIsmNT) k_ism_partials(
+    const float* __restrict__ params, int H, int dv, const float4* __restrict__ xv,
+    const float4* __restrict__ sw, const float* __restrict__ x, const float* __restrict__ v,
+    int64_t ldv, const float* __restrict__ w, int64_t n, float x_scale, float L,
+    const float* __restrict__ Z, int64_t ldz, const int32_t* __restrict__ idx, float inv_wsum,
+    double* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4* Wp = (float4*)smem_raw;                   // [H]
+  float4* Bp = Wp + H;                              // [H]
+  float4* Uc = Bp + H;                              // [NT] (xn, v0, v1, v2)
+  float4* Gc = Uc + kIsmNT;                         // [NT] (gs0, gs1, gs2, w)
+  float4* Zc = Gc + kIsmNT;                         // [NT] probes (MODE 2)
+  float* coef = (float*)(Zc + kIsmNT);              // [H]
+  double* acc64 = (double*)(((uintptr_t)(coef + H) + 15) & ~(uintptr_t)15);  // [items][10]
+  __shared__ float b2[3];
+  __shared__ double red[8 * 4];
+
+  load_packed(params, H, dv, Wp, Bp, b2);
+  __syncthreads();
+  if (MODE == 0 || MODE == 1) {
+    // exact: coef_h = sum_i W2[i,h] W1[h,1+i] (ref: score.py:94-100, 314)
+    // shared Hutchinson: coef_h = (W2^T z)_h (W1_v z)_h (ref: score.py:324-327)
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+      const float4 a = Wp[h], b = Bp[h];
+      if (MODE == 0) {
+        coef[h] = b.y * a.y + b.z * a.z + b.w * a.w;
+      } else {
+        float z0 = Z[0], z1 = Z[1], z2 = dv > 2 ? Z[2] : 0.f;
+        float t = a.y * z0 + a.z * z1 + a.w * z2;
+        float r = b.y * z0 + b.z * z1 + b.w * z2;
+        coef[h] = r * t;
+      }
+    }
+  }
+  const int G = max(1, kIsmNT / H);        // particle groups per hidden unit
+  const int items = H * G;
+  for (int it = threadIdx.x; it < items; it += blockDim.x)
+    for (int k = 0; k < kIsmAcc; ++k) acc64[it * kIsmAcc + k] = 0.0;
+  double lacc[4] = {0.0, 0.0, 0.0, 0.0};  // loss, gb2[3]
+  __syncthreads();
+
+  const int64_t nchunks = (n + kIsmNT - 1) / kIsmNT;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    // ---- phase 1: one particle per thread, forward + loss + dL/ds -----------------------
+    const int64_t p = ch * kIsmNT + threadIdx.x;
+    const bool valid = p < n;
+    float xn = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, wp = 0.f;
+    float q0 = 0.f, q1 = 0.f, q2 = 0.f;  // probe (MODE 2) or target (MODE 3)
+    if (valid) {
+      const int64_t r = idx ? (int64_t)idx[p] : p;
+      if (xv) {
+        float4 A = xv[p];
+        xn = A.x < 0.f ? A.x + L : A.x;
+        v0 = A.y; v1 = A.z; v2 = A.w;
+        wp = sw[p].w;
+      } else {
+        xn = x[r];
+        v0 = v[r];
+        v1 = v[ldv + r];
+        v2 = dv > 2 ? v[2 * ldv + r] : 0.f;
+        wp = w[r];
+      }
+      xn *= x_scale;
+      if (MODE >= 2) {
+        q0 = Z[r];
+        q1 = Z[ldz + r];
+        q2 = dv > 2 ? Z[2 * ldz + r] : 0.f;
+      }
+    }
+    if (MODE == 3) wp *= inv_wsum;
+    float s0 = b2[0], s1 = b2[1], s2 = b2[2], div = 0.f;
+    for (int h = 0; h < H; ++h) {
+      const float4 a = Wp[h];
+      const float4 b = Bp[h];
+      float z = fmaf(a.w, v2, fmaf(a.z, v1, fmaf(a.y, v0, fmaf(a.x, xn, b.x))));
+      float inv = __frcp_rn(1.f + fabsf(z));
+      float act = z * inv;
+      s0 = fmaf(b.y, act, s0);
+      s1 = fmaf(b.z, act, s1);
+      s2 = fmaf(b.w, act, s2);
+      if (MODE == 0 || MODE == 1) {
+        div = fmaf(coef[h], inv * inv, div);
+      } else if (MODE == 2) {
+        float t = a.y * q0 + a.z * q1 + a.w * q2;
+        float rr = b.y * q0 + b.z * q1 + b.w * q2;
+        div = fmaf(rr * t, inv * inv, div);
+      }
+    }
+    float g0, g1, g2, lp;
+    if (MODE == 3) {
+      float e0 = s0 - q0, e1 = s1 - q1, e2 = s2 - q2;
+      lp = wp * (e0 * e0 + e1 * e1 + e2 * e2);
+      g0 = 2.f * wp * e0; g1 = 2.f * wp * e1; g2 = 2.f * wp * e2;
+    } else {
+      lp = wp * (s0 * s0 + s1 * s1 + s2 * s2 + 2.f * div);
+      g0 = 2.f * wp * s0; g1 = 2.f * wp * s1; g2 = 2.f * wp * s2;
+    }
+    if (dv < 3) g2 = 0.f;
+    if (valid) {
+      lacc[0] += (double)lp;
+      lacc[1] += (double)g0;
+      lacc[2] += (double)g1;
+      lacc[3] += (double)g2;
+    } else {
+      g0 = g1 = g2 = 0.f;
+      wp = 0.f;
+    }
+    Uc[threadIdx.x] = make_float4(xn, v0, v1, v2);
+    Gc[threadIdx.x] = make_float4(g0, g1, g2, wp);
+    if (MODE == 2) Zc[threadIdx.x] = make_float4(q0, q1, q2, 0.f);
+    __syncthreads();
+    // ---- phase 2: one (hidden unit, particle group) per thread, outer-product sums ------
+    const int np = (int)(n - ch * kIsmNT < (int64_t)kIsmNT ? n - ch * kIsmNT : (int64_t)kIsmNT);
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int h = it % H, g = it / H;
+      const float4 a = Wp[h], b = Bp[h];
+      const float ch_ = (MODE == 0 || MODE == 1) ? coef[h] : 0.f;
+      float gw0 = 0.f, gw1 = 0.f, gw2 = 0.f, gw3 = 0.f, gb = 0.f;
+      float gv0 = 0.f, gv1 = 0.f, gv2 = 0.f, phi = 0.f;
+      for (int q = g; q < np; q += G) {
+        const float4 u = Uc[q];
+        const float4 gs = Gc[q];
+        float z = fmaf(a.w, u.w, fmaf(a.z, u.z, fmaf(a.y, u.y, fmaf(a.x, u.x, b.x))));
+        float inv = __frcp_rn(1.f + fabsf(z));
+        float act = z * inv;
+        float sp = inv * inv;
+        float da = fmaf(gs.z, b.w, fmaf(gs.y, b.z, gs.x * b.y));
+        float d = da * sp;
+        if (MODE != 3) {
+          float spp = copysignf(2.f * sp * inv, -z);  // -2 sign(z) inv^3 (0 at z = 0 below)
+          if (z == 0.f) spp = 0.f;
+          float cc;
+          if (MODE == 2) {
+            const float4 zz = Zc[q];
+            float t = a.y * zz.x + a.z * zz.y + a.w * zz.z;
+            float rr = b.y * zz.x + b.z * zz.y + b.w * zz.z;
+            cc = rr * t;
+            float k2 = 2.f * gs.w * sp;
+            // d/dW2: 2 w sp t z_i ; d/dW1_v: 2 w sp r z_k (ref: score.py:242, 250)
+            gv0 = fmaf(k2 * t, zz.x, gv0);
+            gv1 = fmaf(k2 * t, zz.y, gv1);
+            gv2 = fmaf(k2 * t, zz.z, gv2);
+            gw1 = fmaf(k2 * rr, zz.x, gw1);
+            gw2 = fmaf(k2 * rr, zz.y, gw2);
+            gw3 = fmaf(k2 * rr, zz.z, gw3);
+          } else {
+            cc = ch_;
+            phi = fmaf(gs.w, sp, phi);
+          }
+          d = fmaf(2.f * gs.w * cc, spp, d);
+        }
+        gb += d;
+        gw0 = fmaf(d, u.x, gw0);
+        gw1 = fmaf(d, u.y, gw1);
+        gw2 = fmaf(d, u.z, gw2);
+        gw3 = fmaf(d, u.w, gw3);
+        gv0 = fmaf(gs.x, act, gv0);
+        gv1 = fmaf(gs.y, act, gv1);
+        gv2 = fmaf(gs.z, act, gv2);
+      }
+      double* A = acc64 + it * kIsmAcc;
+      A[0] += gw0; A[1] += gw1; A[2] += gw2; A[3] += gw3;
+      A[4] += gb;
+      A[5] += gv0; A[6] += gv1; A[7] += gv2;
+      A[8] += phi;
+    }
+    __syncthreads();
+  }
+  // ---- write block partials: [loss, gW1, gb1, gW2, gb2, Phi] ------------------------------
+  block_sum<4>(lacc, red);
+  const int64_t P = n_params(H, dv);
+  const int64_t width = 1 + P + H;
+  double* out = partials + (size_t)blockIdx.x * width;
+  if (threadIdx.x == 0) {
+    out[0] = lacc[0];
+    for (int i = 0; i < dv; ++i) out[1 + P - dv + i] = lacc[1 + i];
+  }
+  const int64_t oW1 = 1, ob1 = oW1 + (int64_t)H * (1 + dv), oW2 = ob1 + H, oPhi = 1 + P;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int g = 0; g < G; ++g)
+      for (int k = 0; k < 9; ++k) s[k] += acc64[(g * H + h) * kIsmAcc + k];
+    for (int k = 0; k < 1 + dv; ++k) out[oW1 + h * (1 + dv) + k] = s[k];
+    out[ob1 + h] = s[4];
+    for (int i = 0; i < dv; ++i) out[oW2 + i * H + h] = s[5 + i];
+    out[oPhi + h] = s[8];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// finalize: ordered reduction of block partials, divergence terms, AdamW with recovery
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_sbtm_finalize(
+    const double* __restrict__ partials, int nblocks, int H, int dv, int div_mode,
+    const float* __restrict__ z_shared, double* __restrict__ params, double* __restrict__ m,
+    double* __restrict__ v2, double* __restrict__ opt, double beta1, double beta2, double eps,
+    double wd, int reset_lr, int apply_step, float* __restrict__ params32,
+    double* __restrict__ grads_out, double* __restrict__ loss_out, int32_t* flags) {
+  extern __shared__ double g[];  // [1 + P + H], then candidate params [P]
+  const int64_t P = n_params(H, dv);
+  const int64_t width = 1 + P + H;
+  double* cand = g + width;
+  for (int64_t k = threadIdx.x; k < width; k += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += partials[(size_t)b * width + k];
+    g[k] = s;
+  }
+  __syncthreads();
+  double* grad = g + 1;
+  const double* Phi = g + 1 + P;
+  const int64_t oW1 = 0, ob1 = (int64_t)H * (1 + dv), oW2 = ob1 + H;
+  // coefficient-dependence of the divergence term (ref: score.py:317-318, 328-329)
+  if (div_mode == 0 || div_mode == 1) {
+    for (int64_t k = threadIdx.x; k < (int64_t)dv * H; k += blockDim.x) {
+      const int i = (int)(k / H), h = (int)(k % H);
+      if (div_mode == 0) {
+        grad[oW2 + i * H + h] += 2.0 * Phi[h] * params[oW1 + h * (1 + dv) + 1 + i];
+        grad[oW1 + h * (1 + dv) + 1 + i] += 2.0 * Phi[h] * params[oW2 + i * H + h];
+      } else {
+        double t = 0.0, r = 0.0;
+        for (int q = 0; q < dv; ++q) {
+          t += params[oW1 + h * (1 + dv) + 1 + q] * (double)z_shared[q];
+          r += params[oW2 + q * H + h] * (double)z_shared[q];
+        }
+        grad[oW2 + i * H + h] += 2.0 * (double)z_shared[i] * t * Phi[h];
+        grad[oW1 + h * (1 + dv) + 1 + i] += 2.0 * r * Phi[h] * (double)z_shared[i];
+      }
+    }
+  }
+  __syncthreads();
+  const double loss = g[0];
+  if (threadIdx.x == 0 && loss_out) *loss_out = loss;
+  if (grads_out)
+    for (int64_t k = threadIdx.x; k < P; k += blockDim.x) grads_out[k] = grad[k];
+  if (!apply_step) return;
+  double lr = reset_lr ? opt[2] : opt[1];
+  if (!isfinite(loss)) {
+    // ism_loss_and_grad raises before the optimizer step; sbtm_update restores (a no-op),
+    // halves lr and retries the same (non-finite) loss until lr < 1e-12 -> RuntimeError.
+    // The MSE path (pretraining) raises straight away (ref: score.py:348-349).
+    if (threadIdx.x == 0) {
+      int halvings = 0;
+      if (div_mode != 3)
+        do {
+          lr *= 0.5;
+          ++halvings;
+        } while (!(lr < 1e-12));
+      atomicAdd(flags + SPIC_FLAG_LR_HALVINGS, halvings);
+      atomicOr(flags + SPIC_FLAG_TRAIN_FATAL, 1);
+      opt[1] = lr;
+    }
+    return;
+  }
+  double t = opt[0];
+  for (;;) {
+    t += 1.0;
+    const double bc1 = 1.0 - pow(beta1, t), bc2 = 1.0 - pow(beta2, t);
+    int ok = 1;
+    for (int64_t k = threadIdx.x; k < P; k += blockDim.x) {
+      double p = params[k];
+      if (wd != 0.0) p -= lr * wd * p;
+      const double gk = grad[k];
+      const double mk = beta1 * m[k] + (1.0 - beta1) * gk;
+      const double vk = beta2 * v2[k] + (1.0 - beta2) * gk * gk;
+      m[k] = mk;
+      v2[k] = vk;
+      p -= lr * (mk / bc1) / (sqrt(vk / bc2) + eps);
+      cand[k] = p;
+      ok &= isfinite(p) ? 1 : 0;
+    }
+    ok = __syncthreads_and(ok);
+    if (ok || div_mode == 3) {
+      for (int64_t k = threadIdx.x; k < P; k += blockDim.x) {
+        params[k] = cand[k];
+        params32[k] = (float)cand[k];
+      }
+      break;
+    }
+    // restore (params untouched), halve, retry with the same gradient (ref: score.py:578-585)
+    lr *= 0.5;
+    if (threadIdx.x == 0) atomicAdd(flags + SPIC_FLAG_LR_HALVINGS, 1);
+    if (lr < 1e-12) {
+      if (threadIdx.x == 0) atomicOr(flags + SPIC_FLAG_TRAIN_FATAL, 1);
+      break;
+    }
+  }
+  if (threadIdx.x == 0) {
+    opt[0] = t;
+    opt[1] = lr;
+  }
+}
+
+static int ism_blocks(int64_t n) {
+  int64_t chunks = (n + kIsmNT - 1) / kIsmNT;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, kIsmBlocksMax));
+}
+
+static size_t ism_smem(int H) {
+  int G = std::max(1, kIsmNT / H);
+  size_t b = sizeof(float4) * (2 * (size_t)H + 3 * kIsmNT) + sizeof(float) * H + 16;
+  b += sizeof(double) * (size_t)H * G * kIsmAcc;
+  return b;
+}
+
+}  // namespace spic
+
+using namespace spic;
+
+extern "C" int64_t spic_mlp_num_params(int32_t H, int32_t dv) { return n_params(H, dv); }
+
+extern "C" int spic_mlp_forward(const float* params32, int32_t H, int32_t dv, const float* xv,
+                                const float* x, const float* v, int64_t ldv, int64_t n,
+                                float x_scale, float* sw, float* s, int64_t lds, void* stream) {
+  if (n < 0 || H < 1 || H > 4096 || (dv != 2 && dv != 3)) return SPIC_ERR_ARG;
+  if (n == 0) return SPIC_OK;
+  size_t smem = sizeof(float4) * 2 * (size_t)H;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_mlp_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 4);
+  k_mlp_forward<<<blocks, 256, smem, (cudaStream_t)stream>>>(
+      params32, H, dv, (const float4*)xv, x, v, ldv, n, x_scale, 1.0f / x_scale, (float4*)sw, s, lds);
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
+
+extern "C" size_t spic_ism_scratch_bytes(int64_t n, int32_t H, int32_t dv) {
+  return sizeof(double) * (size_t)ism_blocks(n) * (size_t)(1 + n_params(H, dv) + H) + 64;
+}
+
+// mode: 0 exact, 1 shared Hutchinson (Z = z_shared float[dv] on device), 2 per-particle
+// probes Z[dv][ldz], 3 MSE to target Z[dv][ldz]. idx (nullable) maps kernel particle p to the
+// source row of the plane inputs and of Z. Block count is encoded in the scratch header.
+extern "C" int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv, int32_t mode,
+                                    const float* xv, const float* sw, const float* x,
+                                    const float* v, int64_t ldv, const float* w, int64_t n,
+                                    float x_scale, const float* Z, int64_t ldz,
+                                    const int32_t* idx, double inv_wsum, void* scratch,
+                                    size_t scratch_bytes, void* stream) {
+  if (n < 1 || H < 1 || H > 2048 || (dv != 2 && dv != 3) || mode < 0 || mode > 3)
+    return SPIC_ERR_ARG;
+  if (mode >= 1 && !Z) return SPIC_ERR_ARG;
+  if (scratch_bytes < spic_ism_scratch_bytes(n, H, dv)) return SPIC_ERR_SCRATCH;
+  const int blocks = ism_blocks(n);
+  size_t smem = ism_smem(H);
+  cudaStream_t st = (cudaStream_t)stream;
+  const float L = 1.0f / x_scale;
+#define SPIC_ISM_LAUNCH(MD)                                                                    \
+  do {                                                                                         \
+    if (smem > 48 * 1024)                                                                      \
+      cudaFuncSetAttribute(k_ism_partials<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           (int)smem);                                                         \
+    k_ism_partials<MD><<<blocks, kIsmNT, smem, st>>>(params32, H, dv, (const float4*)xv,       \
+                                                     (const float4*)sw, x, v, ldv, w, n,       \
+                                                     x_scale, L, Z, ldz, idx, (float)inv_wsum, \
+                                                     (double*)scratch);                        \
+  } while (0)
+  switch (mode) {
+    case 0: SPIC_ISM_LAUNCH(0); break;
+    case 1: SPIC_ISM_LAUNCH(1); break;
+    case 2: SPIC_ISM_LAUNCH(2); break;
+    default: SPIC_ISM_LAUNCH(3); break;
+  }
+#undef SPIC_ISM_LAUNCH
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
+
+extern "C" int spic_sbtm_finalize_ex(const void* scratch, int64_t n, int32_t H, int32_t dv,
+                                     int32_t div_mode, const float* z_shared, double* params64,
+                                     double* m, double* v2, double* opt_state, double beta1,
+                                     double beta2, double eps, double weight_decay,
+                                     int32_t reset_lr, int32_t apply_step, float* params32,
+                                     double* grads_out, double* loss_out, int32_t* flags,
+                                     void* stream) {
+  if (n < 1 || H < 1 || (dv != 2 && dv != 3) || div_mode < 0 || div_mode > 3) return SPIC_ERR_ARG;
+  const int64_t P = n_params(H, dv);
+  size_t smem = sizeof(double) * (size_t)(1 + P + H + P);
+  if (smem > 200 * 1024) return SPIC_ERR_UNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_sbtm_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sbtm_finalize<<<1, 1024, smem, (cudaStream_t)stream>>>(
+      (const double*)scratch, ism_blocks(n), H, dv, div_mode, z_shared, params64, m, v2, opt_state,
+      beta1, beta2, eps, weight_decay, reset_lr, apply_step, params32, grads_out, loss_out, flags);
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
+
+namespace spic {
+// Plain AdamW step on a flat float64 parameter vector (ref: score.py:371-386), used by the
+// operator-level AdamW.step; the training loop uses k_sbtm_finalize instead.
+__global__ void __launch_bounds__(1024) k_adamw_step(double* __restrict__ params,
+                                                     const double* __restrict__ grads,
+                                                     double* __restrict__ m, double* __restrict__ v2,
+                                                     int64_t P, double* __restrict__ opt,
+                                                     double beta1, double beta2, double eps,
+                                                     double wd, float* __restrict__ params32) {
+  const double t = opt[0] + 1.0, lr = opt[2];
+  const double bc1 = 1.0 - pow(beta1, t), bc2 = 1.0 - pow(beta2, t);
+  for (int64_t k = threadIdx.x; k < P; k += blockDim.x) {
+    double p = params[k];
+    if (wd != 0.0) p -= lr * wd * p;
+    const double g = grads[k];
+    const double mk = beta1 * m[k] + (1.0 - beta1) * g;
+    const double vk = beta2 * v2[k] + (1.0 - beta2) * g * g;
+    m[k] = mk;
+    v2[k] = vk;
+    p -= lr * (mk / bc1) / (sqrt(vk / bc2) + eps);
+    params[k] = p;
+    if (params32) params32[k] = (float)p;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) opt[0] = t;
+}
+}  // namespace spic
+
+extern "C" int spic_adamw_step(double* params64, const double* grads64, double* m, double* v2,
+                               int64_t P, double* opt_state, double beta1, double beta2,
+                               double eps, double weight_decay, float* params32, void* stream) {
+  if (P < 0) return SPIC_ERR_ARG;
+  k_adamw_step<<<1, 1024, 0, (cudaStream_t)stream>>>(params64, grads64, m, v2, P, opt_state, beta1,
+                                                     beta2, eps, weight_decay, params32);
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
