@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 per-timestep hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+Workload (default c2 = BASELINE config 2): two-stream 1D3V, SBTM, n = 2^20 particles,
+M = 128 cells on L = 10 pi, nu = 0.05, dt = 0.05, K = 10 ISM steps per time step, exact
+divergence, H = 128 (reference softsign architecture), Adam lr 1e-3 (AdamW, wd = 0).
+A step is one full Algorithm-1 step (push, bin, deposit + field, K ISM steps, score, Landau
+collision + push, diagnostics) over the synthetic ensemble (seeded sampler, random-init net).
+
+  value  = particle-steps/s, device-timed with CUDA events per step (L2 flushed between
+           timed steps by a 256 MiB write outside the timed windows), max over ranks.
+  e2e    = same metric through Simulation.step_host with pinned HOST buffers: H2D of x, v,
+           the step, D2H of x, v and the diagnostics row, every step.
+  roofline: dominant kernel = the Landau pair kernel (spic_landau), 38 FLOP per ordered
+           live pair (|dx| < eta), against the FP32 peak measured in-run by spic_fp32_probe.
+  cpu_baseline: the float64 oracle port (oracle/, C + OpenMP) on a bounded sample of the same
+           workload, rank 0, N = 1 only.
+`--impl reference` times that CPU port alone (the reference arm; the reference itself is pure
+Python + numba and is not shipped to the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+FLOP_PER_PAIR = 38.0
+METRIC = "particle-steps/s (full VML step, SBTM)"
+
+WORKLOADS = {
+    "c2": dict(workload="config2_two_stream_sbtm", preset="two_stream", mode="VPL", n=1 << 20,
+               M=128, L=10 * math.pi, alpha=0.001, k=0.2, c=2.4, nu=0.05, dt=0.05, K=10,
+               hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact", estimator="sbtm"),
+    "c0": dict(workload="config0_landau_damping_sbtm", preset="landau_damping", mode="VPL",
+               n=65536, M=64, L=4 * math.pi, alpha=0.01, k=0.5, c=0.0, nu=0.1, dt=0.05, K=10,
+               hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact", estimator="sbtm"),
+    "c4": dict(workload="config4_landau_damping_sbtm_n2^24", preset="landau_damping", mode="VPL",
+               n=1 << 24, M=1024, L=4 * math.pi, alpha=0.01, k=0.5, c=0.0, nu=0.1, dt=0.05,
+               K=10, hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact",
+               estimator="sbtm"),
+    "c4blob": dict(workload="config4_landau_damping_blob_n2^24", preset="landau_damping",
+                   mode="VPL", n=1 << 24, M=1024, L=4 * math.pi, alpha=0.01, k=0.5, c=0.0,
+                   nu=0.1, dt=0.05, K=0, hidden=128, lr=1e-3, weight_decay=0.0,
+                   divergence="exact", estimator="blob", bandwidth=0.025),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def make_config(wl: dict, seed: int):
+    from paper_2603_25832_b200.config import SimConfig
+
+    keys = {f for f in SimConfig.__dataclass_fields__}
+    kw = {k: v for k, v in wl.items() if k in keys}
+    if "bandwidth" in kw:
+        kw["bandwidth"] = str(kw["bandwidth"])
+    return SimConfig(seed=seed, t_final=wl["dt"], **kw)
+
+
+# ------------------------------------------------------------------------------------------
+# CPU baseline: the oracle port on a bounded sample
+# ------------------------------------------------------------------------------------------
+
+def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_stride: int = 16,
+                    seed: int = 0):
+    """Seconds for one full step of the workload on the host cores, measured on a bounded
+    sample: push/deposit/field/bin/forward on all n; K ISM steps on n/ism_sub particles
+    (x ism_sub); the pair kernel on every cell_stride-th cell (x cell_stride)."""
+    from oracle import oracle as O
+
+    x, v, w = host_state["x"], host_state["v"], host_state["w"]
+    E1, E2, B3 = host_state["E1"], host_state["E2"], host_state["B3"]
+    M, L = wl["M"], wl["L"]
+    eta = L / M
+    n = x.shape[0]
+    t = {}
+    t0 = time.perf_counter()
+    x1, v1 = O.push(x, v, E1, E2, B3, eta, M, wl["dt"])
+    rho, J = O.deposit(x1, v1, w, eta, M)
+    O.vpl_field_step(E1, J, wl["dt"]) if wl["mode"] == "VPL" else O.maxwell_step(E1, E2, B3, J, eta, wl["dt"])
+    O.build_cell_index(x1, eta, M)
+    t["push_deposit_field_bin"] = time.perf_counter() - t0
+    rng = np.random.default_rng(seed)
+    if wl["estimator"] == "sbtm":
+        net = O.Net.glorot(v.shape[1], wl["hidden"], rng)
+        sub = rng.choice(n, size=max(1, n // ism_sub), replace=False)
+        opt = O.AdamW(lr=wl["lr"], weight_decay=wl["weight_decay"])
+        t0 = time.perf_counter()
+        O.sbtm_update(net, opt, x1[sub], v1[sub], w[sub], wl["K"], L=L, divergence=wl["divergence"])
+        t["ism"] = (time.perf_counter() - t0) * (n / len(sub))
+        t0 = time.perf_counter()
+        s = O.mlp_forward(net, x1 / L, v1)
+        t["forward"] = time.perf_counter() - t0
+    else:
+        t0 = time.perf_counter()
+        s = O.blob_score(x1, v1, w, eta, M, wl.get("bandwidth"), cell_stride=cell_stride)
+        t["blob"] = (time.perf_counter() - t0) * cell_stride
+    t0 = time.perf_counter()
+    O.collision_force(x1, v1, w, s, eta, M, -3.0, cell_stride=cell_stride)
+    t["collision"] = (time.perf_counter() - t0) * cell_stride
+    return sum(t.values()), t
+
+
+def host_initial_state(wl: dict, seed: int):
+    from paper_2603_25832_b200.sampling import sample_arrays
+    from oracle import oracle as O
+
+    cfg = make_config(wl, seed)
+    x, v, w = sample_arrays(cfg, np.random.default_rng(seed))
+    x = x.astype(np.float32).astype(np.float64)
+    v = v.astype(np.float32).astype(np.float64)
+    M, L = wl["M"], wl["L"]
+    eta = L / M
+    rho, _ = O.deposit(x, v, w, eta, M)
+    rho_ion = float(rho.sum() * eta / L)
+    E1 = O.poisson_solve(rho, rho_ion, eta) if wl["mode"] == "VPL" else np.zeros(M)
+    return dict(x=x, v=v, w=w, E1=E1, E2=np.zeros(M), B3=np.zeros(M))
+
+
+def cpu_baseline_line(wl: dict, seed: int, reps: int = 1, warm: int = 0):
+    from oracle import oracle as O
+
+    st = host_initial_state(wl, seed)
+    for _ in range(warm):
+        cpu_sample_step(wl, st, seed=seed)
+    times, parts = [], None
+    for _ in range(reps):
+        T, parts = cpu_sample_step(wl, st, seed=seed)
+        times.append(T)
+    T = statistics.mean(times)
+    n = wl["n"]
+    live = O.count_live_pairs(st["x"], wl["L"] / wl["M"], wl["M"]) if wl["n"] <= (1 << 21) else None
+    return dict(value=n / T, unit="particle-steps/s", cores=O.num_threads(), kind="port",
+                sample=("oracle/ float64 C+OpenMP port; per step: push/deposit/field/bin and "
+                        "score forward on all n, K ISM steps on n/16 particles (x16), pair "
+                        "kernel on every 16th cell (x16)"),
+                seconds_per_step=T, stage_seconds=parts,
+                pair_interactions_per_s=(live / parts["collision"]) if live else None)
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            self.max_mhz = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop_ev.wait(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_ev.set()
+            self.th.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def fp32_peak_tflops(torch, _lib) -> float:
+    import ctypes
+
+    out = torch.zeros(4096, device="cuda")
+    flop = ctypes.c_double(0.0)
+    best = 0.0
+    for it in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.call("spic_fp32_probe", 1 << 14, 148 * 4, _lib.ptr(out), ctypes.byref(flop),
+                  _lib.stream_handle())
+        e1.record()
+        e1.synchronize()
+        if it:
+            best = max(best, flop.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+def build_sim(wl: dict, seed: int, device):
+    import torch
+
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
+    from paper_2603_25832_b200.run import initial_fields
+    from paper_2603_25832_b200.sampling import sample_arrays
+    from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    cfg = make_config(wl, seed)
+    rng = np.random.default_rng(seed)
+    x, v, w = sample_arrays(cfg, rng)
+    grid = Grid(cfg.M, cfg.eta)
+    p = ParticleEnsemble.from_arrays(x, v, w, device=device)
+    rho, J = deposit(p, grid)
+    fields = initial_fields(cfg, grid, rho, J)
+    if wl["estimator"] == "sbtm":
+        net = MlpScoreNet.init_glorot(cfg.dv, cfg.hidden, rng, device=device)
+        est = SbtmEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay,
+                            divergence=cfg.divergence, rademacher=cfg.rademacher)
+    else:
+        est = BlobEstimator(grid, float(wl["bandwidth"]))
+    sim = Simulation(p, fields, grid, dt=cfg.dt, nu=cfg.nu, mode=cfg.mode, gamma=cfg.gamma,
+                     estimator=est, max_rows=4)
+    del torch
+    return sim
+
+
+def main():
+    args = parse_args()
+    wl = WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        reps, warm = max(1, args.steps), max(0, args.warmup)
+        # bounded: each CPU step is a sampled step (a few seconds on 16 cores)
+        line = cpu_baseline_line(wl, args.seed, reps=reps, warm=min(warm, 1))
+        out = {"metric": METRIC, "value": line["value"], "unit": "particle-steps/s",
+               "impl": "reference", "n_gpus": args.gpus, "steps": reps, "warmup": warm,
+               "ms_per_step": 1e3 * line["seconds_per_step"], "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": wl["workload"], "n": wl["n"], "M": wl["M"], "K": wl["K"],
+                          "hidden": wl["hidden"]},
+               "cpu_baseline": {"value": line["value"], "unit": "particle-steps/s",
+                                "cores": line["cores"], "kind": "port", "sample": line["sample"]},
+               "e2e": {"value": line["value"], "unit": "particle-steps/s",
+                       "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+               "pair_interactions_per_s": line["pair_interactions_per_s"],
+               "stage_seconds": line["stage_seconds"]}
+        print(json.dumps(out))
+        return 0
+
+    import torch
+
+    from paper_2603_25832_b200 import _lib
+    from paper_2603_25832_b200.collision import count_live_pairs
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    _lib.load(build_if_missing=False)
+
+    # each rank owns an independent ensemble of the workload's size (weak scaling; the
+    # particle state is partitioned across ranks, no data-path collective)
+    sim = build_sim(wl, args.seed + rank, device)
+    n = wl["n"]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    for _ in range(max(3, args.warmup)):
+        sim.step(0)
+    torch.cuda.synchronize()
+    sim.check()
+    live0 = count_live_pairs(sim.ci, sim.p, sim.grid)
+    peak = fp32_peak_tflops(torch, _lib)
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sim.time_collision = True
+    sim.collision_events.clear()
+    launches0 = _lib.query("spic_launch_count")
+    evs = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sim.step(1)
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+    launches = _lib.query("spic_launch_count") - launches0
+    sim.time_collision = False
+    sim.check()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    coll_ms = [a.elapsed_time(b) for a, b in sim.collision_events]
+    live1 = count_live_pairs(sim.ci, sim.p, sim.grid)
+    live = 0.5 * (live0 + live1)
+    t = torch.tensor([total_ms, statistics.mean(coll_ms)], dtype=torch.float64, device=device)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    total_ms, coll_avg_ms = float(t[0]), float(t[1])
+    value = world * n * args.steps / (total_ms * 1e-3)
+
+    # end to end through the public host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        dv = sim.p.dv
+        xh = torch.empty(n, dtype=torch.float32).pin_memory()
+        vh = torch.empty(dv, n, dtype=torch.float32).pin_memory()
+        dh = torch.empty(sim.diag.shape[1], dtype=torch.float64).pin_memory()
+        xh.copy_(sim.p.x)
+        vh.copy_(sim.p.vp)
+        torch.cuda.synchronize()
+        sim.step_host(2, xh, vh, dh)  # warm
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            sim.step_host(2, xh, vh, dh)
+        e1.record()
+        e1.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n * args.steps / (float(te[0]) * 1e-3), "unit": "particle-steps/s",
+               "h2d_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4),
+               "d2h_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4 + dh.numel() * 8)}
+        sim.check()
+
+    achieved = FLOP_PER_PAIR * live / (coll_avg_ms * 1e-3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "landau_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(args.workload)
+        except Exception:  # noqa: BLE001
+            traffic = None
+    out = {
+        "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded reference sampler; random-init score net, no pretraining)",
+        "config": {"workload": wl["workload"], "n_per_gpu": n, "M": wl["M"], "L": wl["L"],
+                   "mode": wl["mode"], "estimator": wl["estimator"], "K_ism": wl["K"],
+                   "hidden": wl["hidden"],
+                   "net": "softsign 1x{} (reference arch; BASELINE's 2x128 SiLU is extension M1)"
+                   .format(wl["hidden"]),
+                   "divergence": wl["divergence"], "sub_cells": sim.S,
+                   "l2": "flushed between timed steps (256 MiB write, outside timed windows)",
+                   "parallelism": f"{world} rank(s), independent ensembles per rank"},
+        "pair_interactions_per_s": world * live / (coll_avg_ms * 1e-3),
+        "live_pairs_per_step": live,
+        "collision_ms": coll_avg_ms,
+        "roofline": {"bound": "fp32", "kernel": "spic_landau (k_landau)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "flop_per_launch": FLOP_PER_PAIR * live,
+                     "peak_source": "measured in-run: spic_fp32_probe (FFMA2 chains, 592 CTAs)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line = cpu_baseline_line(wl, args.seed)
+            out["cpu_baseline"] = {k: line[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"]["pair_interactions_per_s"] = line["pair_interactions_per_s"]
+        except Exception as exc:  # noqa: BLE001
+            out["cpu_baseline"] = {"error": str(exc)}
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

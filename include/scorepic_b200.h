@@ -56,6 +56,10 @@ enum {
 int spic_version(void);
 /* number of SMs the launch heuristics assume (148 on B200) */
 int spic_num_sms(void);
+/* total kernel launches issued by this library so far (host counter) */
+long long spic_launch_count(void);
+/* FP32 FMA throughput probe (roofline denominator): *flop (host) = FLOPs of the launch. */
+int spic_fp32_probe(int32_t iters, int32_t blocks, float* out, double* flop, void* stream);
 
 /* ---- binning (replaces Grid.cell_of pic.py:27-30, build_cell_index collision.py:39-46) -- */
 /* cell[i] = min(floor(x_i/eta) mod M, M-1), float64 arithmetic on the float32 input. */

@@ -77,16 +77,16 @@ static int stencil_cells(int64_t c, int64_t M, int64_t out[3]) {
  * z = v_i - v_j, u = s_i - s_j, skip |z|^2 <= 1e-24, coef = |z|^(gamma+2),
  * U_i += w_j psi coef (u - (z.u/|z|^2) z).
  * ------------------------------------------------------------------------------------- */
-static void collision_targets(const double* x, const double* v, const double* s,
-                              const double* w, int dv, const int64_t* tgt, int64_t nt,
-                              const int64_t* nbr, int64_t nn, double eta, double L,
-                              double half_pow, double* U) {
+static void collision_targets(const double* xt, const double* vt, const double* st, int64_t nt,
+                              const double* xn, const double* vn, const double* sn,
+                              const double* wn, int64_t nn, int dv, double eta, double L,
+                              double half_pow, double* out) {
+  /* gathered, contiguous target / neighbour blocks like the reference's per-cell call
+   * (ref: collision.py:107-108); out is (nt, dv) */
   for (int64_t a = 0; a < nt; ++a) {
-    int64_t i = tgt[a];
     double acc[3] = {0.0, 0.0, 0.0};
     for (int64_t b = 0; b < nn; ++b) {
-      int64_t j = nbr[b];
-      double dx = x[i] - x[j];
+      double dx = xt[a] - xn[b];
       if (dx > 0.5 * L)
         dx -= L;
       else if (dx < -0.5 * L)
@@ -96,8 +96,8 @@ static void collision_targets(const double* x, const double* v, const double* s,
       double psi = (1.0 - adx / eta) / eta;
       double z2 = 0.0, zu = 0.0;
       for (int k = 0; k < dv; ++k) {
-        double zk = v[i * dv + k] - v[j * dv + k];
-        double uk = s[i * dv + k] - s[j * dv + k];
+        double zk = vt[a * dv + k] - vn[b * dv + k];
+        double uk = st[a * dv + k] - sn[b * dv + k];
         z2 += zk * zk;
         zu += zk * uk;
       }
@@ -109,12 +109,27 @@ static void collision_targets(const double* x, const double* v, const double* s,
         coef = 1.0 / sqrt(z2);
       else
         coef = pow(z2, half_pow);
-      double cw = w[j] * psi * coef;
+      double cw = wn[b] * psi * coef;
       double proj = cw * zu / z2;
       for (int k = 0; k < dv; ++k)
-        acc[k] += cw * (s[i * dv + k] - s[j * dv + k]) - proj * (v[i * dv + k] - v[j * dv + k]);
+        acc[k] += cw * (st[a * dv + k] - sn[b * dv + k]) - proj * (vt[a * dv + k] - vn[b * dv + k]);
     }
-    for (int k = 0; k < dv; ++k) U[i * dv + k] = acc[k];
+    for (int k = 0; k < dv; ++k) out[a * dv + k] = acc[k];
+  }
+}
+
+/* gather rows idx[0..m) of (x, v, s, w) into contiguous blocks */
+static void gather_rows(const double* x, const double* v, const double* s, const double* w,
+                        int dv, const int64_t* idx, int64_t m, double* gx, double* gv, double* gs,
+                        double* gw) {
+  for (int64_t a = 0; a < m; ++a) {
+    int64_t i = idx[a];
+    gx[a] = x[i];
+    if (gw) gw[a] = w[i];
+    for (int k = 0; k < dv; ++k) {
+      gv[a * dv + k] = v[i * dv + k];
+      if (gs) gs[a * dv + k] = s[i * dv + k];
+    }
   }
 }
 
@@ -134,7 +149,11 @@ int oracle_collision_force_sampled(const double* x, const double* v, const doubl
   if (cell_stride < 1) cell_stride = 1;
 #pragma omp parallel
   {
-    int64_t* nbr = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    size_t cap = (size_t)(n > 0 ? n : 1);
+    int64_t* nbr = (int64_t*)malloc(sizeof(int64_t) * cap);
+    double* buf = (double*)malloc(sizeof(double) * cap * (size_t)(3 + 5 * dv));
+    double *xn = buf, *wn = xn + cap, *vn = wn + cap, *sn = vn + cap * dv;
+    double *xt = sn + cap * dv, *vt = xt + cap, *stt = vt + cap * dv, *out = stt + cap * dv;
 #pragma omp for schedule(dynamic, 1)
     for (int64_t c = 0; c < M; ++c) {
       if (c % cell_stride) continue;
@@ -145,8 +164,14 @@ int oracle_collision_force_sampled(const double* x, const double* v, const doubl
       int64_t nn = 0;
       for (int q = 0; q < k; ++q)
         for (int64_t t = starts[cells[q]]; t < starts[cells[q] + 1]; ++t) nbr[nn++] = perm[t];
-      collision_targets(x, v, s, w, dv, perm + starts[c], nt, nbr, nn, eta, L, half_pow, U);
+      const int64_t* tgt = perm + starts[c];
+      gather_rows(x, v, s, w, dv, nbr, nn, xn, vn, sn, wn);
+      gather_rows(x, v, s, w, dv, tgt, nt, xt, vt, stt, NULL);
+      collision_targets(xt, vt, stt, nt, xn, vn, sn, wn, nn, dv, eta, L, half_pow, out);
+      for (int64_t a = 0; a < nt; ++a)
+        for (int kk = 0; kk < dv; ++kk) U[tgt[a] * dv + kk] = out[a * dv + kk];
     }
+    free(buf);
     free(nbr);
   }
   free(perm);

@@ -39,6 +39,8 @@ _SZ = ctypes.c_size_t
 SIGNATURES = {
     "spic_version": (ctypes.c_int, []),
     "spic_num_sms": (ctypes.c_int, []),
+    "spic_launch_count": (ctypes.c_longlong, []),
+    "spic_fp32_probe": (ctypes.c_int, [_I32, _I32, _P, _P, _P]),
     "spic_cell_of": (ctypes.c_int, [_P, _I64, _D, _I32, _P, _P]),
     "spic_bin_scratch_bytes": (_SZ, [_I64, _I32, _I32]),
     "spic_bin": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _I32, _D, _I32, _I32, _P, _P, _P, _P, _P,

@@ -17,6 +17,7 @@
 //                      sub-chunk in lane order with __match_any_sync ranks. Position order is
 //                      therefore (key, tile, warp, group, lane) = (key, pid): stable.
 #include <algorithm>
+#include <atomic>
 
 #include "common.cuh"
 
@@ -240,9 +241,15 @@ __global__ void k_gather_scores(const float* __restrict__ s, int64_t lds,
 
 }  // namespace spic
 
+namespace spic {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace spic
+
 using namespace spic;
 
 extern "C" int spic_version(void) { return 1; }
+extern "C" long long spic_launch_count(void) { return g_launches.load(); }
 extern "C" int spic_num_sms(void) { return kNumSMs; }
 
 extern "C" int spic_cell_of(const float* x, int64_t n, double eta, int32_t M, int32_t* cell,
@@ -250,7 +257,7 @@ extern "C" int spic_cell_of(const float* x, int64_t n, double eta, int32_t M, in
   if (n < 0 || M < 1 || !(eta > 0)) return SPIC_ERR_ARG;
   if (n == 0) return SPIC_OK;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
-  k_cell_of<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, eta, M, cell);
+  k_cell_of<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, eta, M, cell); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -284,14 +291,14 @@ extern "C" int spic_bin(const float* x, const float* v, int64_t ldv, const float
   size_t smem_count = sizeof(int) * p.K;
   if (smem_count > 48 * 1024)
     cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_count);
-  k_bin_count<<<p.n_tiles, 256, smem_count, st>>>(x, n, eta, M, S, p.T, p.n_tiles, counts);
+  k_bin_count<<<p.n_tiles, 256, smem_count, st>>>(x, n, eta, M, S, p.T, p.n_tiles, counts); spic::count_launch();
   SPIC_CHECK_LAUNCH();
-  k_scan_reduce<<<(unsigned)p.nb_scan, kScanThreads, 0, st>>>(counts, p.counts_elems, bsum);
-  k_scan_blocksums<<<1, kScanThreads, 0, st>>>(bsum, p.nb_scan);
-  k_scan_apply<<<(unsigned)p.nb_scan, kScanThreads, 0, st>>>(counts, p.counts_elems, bsum);
+  k_scan_reduce<<<(unsigned)p.nb_scan, kScanThreads, 0, st>>>(counts, p.counts_elems, bsum); spic::count_launch();
+  k_scan_blocksums<<<1, kScanThreads, 0, st>>>(bsum, p.nb_scan); spic::count_launch();
+  k_scan_apply<<<(unsigned)p.nb_scan, kScanThreads, 0, st>>>(counts, p.counts_elems, bsum); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   int sb = (int)std::min<int64_t>(((int64_t)p.K + 256) / 256, 1024);
-  k_bin_starts<<<sb, 256, 0, st>>>(counts, M, S, p.n_tiles, (int32_t)n, cell_start, sub_start);
+  k_bin_starts<<<sb, 256, 0, st>>>(counts, M, S, p.n_tiles, (int32_t)n, cell_start, sub_start); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   size_t smem_scatter = sizeof(int) * (size_t)p.W * p.K;
   if (smem_scatter > 48 * 1024)
@@ -299,7 +306,7 @@ extern "C" int spic_bin(const float* x, const float* v, int64_t ldv, const float
                          (int)smem_scatter);
   k_bin_scatter<<<p.n_tiles, p.W * 32, smem_scatter, st>>>(
       x, v, ldv, w, n, dv, eta, L, M, S, p.W, p.G, p.n_tiles, counts, perm, (float4*)xv,
-      (float4*)sw);
+      (float4*)sw); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -309,7 +316,7 @@ extern "C" int spic_gather_scores(const float* s, int64_t lds, const int32_t* pe
   if (n < 0 || (dv != 2 && dv != 3)) return SPIC_ERR_ARG;
   if (n == 0) return SPIC_OK;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
-  k_gather_scores<<<blocks, 256, 0, (cudaStream_t)stream>>>(s, lds, perm, n, dv, (float4*)sw, flags);
+  k_gather_scores<<<blocks, 256, 0, (cudaStream_t)stream>>>(s, lds, perm, n, dv, (float4*)sw, flags); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }

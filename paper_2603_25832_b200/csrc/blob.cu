@@ -273,22 +273,25 @@ extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_
   const float4* xv4 = (const float4*)xv;
   const float* hc = nullptr;
   if (bandwidth <= 0) {
-    k_blob_cellsum<<<M, 256, 0, st>>>(xv4, cell_start, dv, S1);
-    k_blob_silverman<<<M, 256, 0, st>>>(xv4, cell_start, M, dv, S1, h_cell);
+    k_blob_cellsum<<<M, 256, 0, st>>>(xv4, cell_start, dv, S1); spic::count_launch();
+    k_blob_silverman<<<M, 256, 0, st>>>(xv4, cell_start, M, dv, S1, h_cell); spic::count_launch();
     SPIC_CHECK_LAUNCH();
     hc = h_cell;
   }
-  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, kLandauTI, tile_start);
+  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, kLandauTI, tile_start); spic::count_launch();
   const double L = (double)M * eta;
   const float ie = (float)(1.0 / eta), ie2 = (float)(1.0 / (eta * eta));
   const float wie = (float)((double)uniform_w / eta), wie2 = (float)((double)uniform_w / (eta * eta));
   dim3 grid((unsigned)(n / kLandauTI + M + 1), (unsigned)ns);
   const bool mi = M <= 2, uw = uniform_w > 0.f;
   const float hf = (float)bandwidth;
-#define SPIC_BLOB(DV_, MI_, UW_)                                                                 \
-  k_blob_pairs<DV_, MI_, UW_><<<grid, kLandauNT, 0, st>>>(xv4, (const float4*)sw, cell_start,    \
-                                                         sub_start, tile_start, M, S, (float)L, ie, \
-                                                         ie2, wie, wie2, hc, hf, ns, part, n)
+#define SPIC_BLOB(DV_, MI_, UW_)                                                             \
+  do {                                                                                       \
+    k_blob_pairs<DV_, MI_, UW_><<<grid, kLandauNT, 0, st>>>(                                 \
+        xv4, (const float4*)sw, cell_start, sub_start, tile_start, M, S, (float)L, ie, ie2, \
+        wie, wie2, hc, hf, ns, part, n);                                                     \
+    spic::count_launch();                                                                    \
+  } while (0)
   if (dv == 3) {
     if (mi) { if (uw) SPIC_BLOB(3, true, true); else SPIC_BLOB(3, true, false); }
     else { if (uw) SPIC_BLOB(3, false, true); else SPIC_BLOB(3, false, false); }
@@ -300,7 +303,7 @@ extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_
   SPIC_CHECK_LAUNCH();
   int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
   k_blob_fold<<<blocks, 256, 0, st>>>(part, ns, n, dv, xv4, (float4*)sw, perm, cell_start, M, hc,
-                                      hf, bad_pid, flags);
+                                      hf, bad_pid, flags); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }

@@ -8,10 +8,13 @@
 #define SPIC_CHECK_LAUNCH()                                  \
   do {                                                       \
     cudaError_t e__ = cudaGetLastError();                    \
-    if (e__ != cudaSuccess) return SPIC_ERR_CUDA + (int)e__; \
+    if (e__ != cudaSuccess) return SPIC_ERR_CUDA - (int)e__; \
   } while (0)
 
 namespace spic {
+
+// host-side count of kernel launches issued by this library (bench evidence)
+void count_launch();
 
 constexpr int kWarp = 32;
 constexpr int kNumSMs = 148;

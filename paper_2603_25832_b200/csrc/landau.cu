@@ -247,7 +247,7 @@ static void launch_landau(dim3 grid, cudaStream_t st, const float4* xv, const fl
                           float L, float ie, float ie2, float wie, float wie2, float hp, int nsplit,
                           float* U, int64_t ldu) {
   k_landau<DV, MINIMG, GMODE, UW><<<grid, kLandauNT, 0, st>>>(xv, sw, cs, ss, ts, M, S, L, ie, ie2,
-                                                              wie, wie2, hp, nsplit, U, ldu);
+                                                              wie, wie2, hp, nsplit, U, ldu); spic::count_launch();
 }
 
 template <int DV, bool MINIMG, int GMODE>
@@ -324,7 +324,7 @@ extern "C" int spic_landau(const float* xv, const float* sw, int64_t n, int32_t 
     p = (p + 255) & ~(uintptr_t)255;
     Upart = (float*)p;
   }
-  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, kLandauTI, tile_start);
+  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, kLandauTI, tile_start); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   const double L = (double)M * eta;
   const float ie = (float)(1.0 / eta), ie2 = (float)(1.0 / (eta * eta));
@@ -356,7 +356,7 @@ extern "C" int spic_landau(const float* xv, const float* sw, int64_t n, int32_t 
   SPIC_CHECK_LAUNCH();
   if (nsplit > 1) {  // fold the splits into U_sorted in a fixed order
     int blocks = (int)std::min<int64_t>((n * dv + 255) / 256, kNumSMs * 8);
-    k_fold_splits<<<blocks, 256, 0, st>>>(Upart, nsplit, dv, n, U_sorted);
+    k_fold_splits<<<blocks, 256, 0, st>>>(Upart, nsplit, dv, n, U_sorted); spic::count_launch();
     SPIC_CHECK_LAUNCH();
   }
   return SPIC_OK;
@@ -367,7 +367,7 @@ extern "C" int spic_landau_fold(const float* U_part, int32_t nsplit, int32_t dv,
                                 float* U_sorted, void* stream) {
   int blocks = (int)std::min<int64_t>((n * dv + 255) / 256, kNumSMs * 8);
   if (blocks < 1) return SPIC_OK;
-  k_fold_splits<<<blocks, 256, 0, (cudaStream_t)stream>>>(U_part, nsplit, dv, n, U_sorted);
+  k_fold_splits<<<blocks, 256, 0, (cudaStream_t)stream>>>(U_part, nsplit, dv, n, U_sorted); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -386,9 +386,10 @@ extern "C" int spic_collision_epilogue(const float* U_sorted, const float* sw, c
   else
     k_collision_epilogue<2><<<kEpiBlocks, 256, 0, st>>>(U_sorted, 1, n, (const float4*)sw, perm,
                                                         nu_dt, v, ldv, U_pid, ldu, part, flags);
+  spic::count_launch();
   SPIC_CHECK_LAUNCH();
   if (red_out) {
-    k_reduce_rows<<<1, 256, 0, st>>>(part, kEpiBlocks, 5, red_out);
+    k_reduce_rows<<<1, 256, 0, st>>>(part, kEpiBlocks, 5, red_out); spic::count_launch();
     SPIC_CHECK_LAUNCH();
   }
   return SPIC_OK;
@@ -402,7 +403,7 @@ extern "C" int spic_count_live_pairs(const float* xv, int64_t n, const int32_t* 
   cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
   if (n == 0) return SPIC_OK;
   k_count_live<<<M, 256, 0, st>>>((const float4*)xv, cell_start, M, (float)(M * eta), (float)eta,
-                                  count);
+                                  count); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }

@@ -284,6 +284,7 @@ extern "C" int spic_push(float* x, float* v, int64_t ldv, int64_t n, int32_t dv,
     k_push<3><<<blocks, 256, 0, st>>>(x, v, ldv, n, E1, E2, B3, M, (float)(1.0 / eta), dt, Ld, flags);
   else
     k_push<2><<<blocks, 256, 0, st>>>(x, v, ldv, n, E1, E2, B3, M, (float)(1.0 / eta), dt, Ld, flags);
+  spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -311,9 +312,10 @@ extern "C" int spic_deposit_field(const float* xv, const float* sw, int64_t n, i
   else
     k_deposit_partials<2><<<M * CH, kDepThreads, 0, st>>>((const float4*)xv, (const float4*)sw,
                                                           cell_start, M, CH, eta, uniform_w, part);
+  spic::count_launch();
   SPIC_CHECK_LAUNCH();
   k_deposit_finalize<<<1, 1024, 0, st>>>(part, M, CH, dv, eta, rho, J, field_mode, dt, E1, E2, B3,
-                                         diag_out, flags);
+                                         diag_out, flags); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -323,7 +325,7 @@ extern "C" int spic_field_step(double* E1, double* E2, double* B3, const double*
                                int32_t* flags, void* stream) {
   if (M < 1 || field_mode < 0 || field_mode > 2) return SPIC_ERR_ARG;
   k_field_step<<<1, 1024, 0, (cudaStream_t)stream>>>(E1, E2, B3, J, M, eta, dt, field_mode,
-                                                     diag_out, flags);
+                                                     diag_out, flags); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -335,7 +337,7 @@ extern "C" int spic_poisson(const double* rho, double rho_ion, int32_t M, double
   size_t smem = sizeof(double) * ((size_t)M + 2 * (M / 2 + 1));
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_poisson, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_poisson<<<1, 1024, smem, (cudaStream_t)stream>>>(rho, rho_ion, M, eta, E1, flags);
+  k_poisson<<<1, 1024, smem, (cudaStream_t)stream>>>(rho, rho_ion, M, eta, E1, flags); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -356,8 +358,9 @@ extern "C" int spic_moments(const float* v, int64_t ldv, const float* w, int64_t
     k_moments<3><<<kMomBlocks, 256, 0, st>>>(v, ldv, w, n, uniform_w, part, flags);
   else
     k_moments<2><<<kMomBlocks, 256, 0, st>>>(v, ldv, w, n, uniform_w, part, flags);
+  spic::count_launch();
   SPIC_CHECK_LAUNCH();
-  k_reduce_rows_pic<<<1, 256, 0, st>>>(part, kMomBlocks, 5, out);
+  k_reduce_rows_pic<<<1, 256, 0, st>>>(part, kMomBlocks, 5, out); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }

@@ -426,7 +426,7 @@ extern "C" int spic_mlp_forward(const float* params32, int32_t H, int32_t dv, co
     cudaFuncSetAttribute(k_mlp_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 4);
   k_mlp_forward<<<blocks, 256, smem, (cudaStream_t)stream>>>(
-      params32, H, dv, (const float4*)xv, x, v, ldv, n, x_scale, 1.0f / x_scale, (float4*)sw, s, lds);
+      params32, H, dv, (const float4*)xv, x, v, ldv, n, x_scale, 1.0f / x_scale, (float4*)sw, s, lds); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -460,7 +460,7 @@ extern "C" int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv
     k_ism_partials<MD><<<blocks, kIsmNT, smem, st>>>(params32, H, dv, (const float4*)xv,       \
                                                      (const float4*)sw, x, v, ldv, w, n,       \
                                                      x_scale, L, Z, ldz, idx, (float)inv_wsum, \
-                                                     (double*)scratch);                        \
+                                                     (double*)scratch); spic::count_launch();                        \
   } while (0)
   switch (mode) {
     case 0: SPIC_ISM_LAUNCH(0); break;
@@ -488,7 +488,7 @@ extern "C" int spic_sbtm_finalize_ex(const void* scratch, int64_t n, int32_t H, 
     cudaFuncSetAttribute(k_sbtm_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_sbtm_finalize<<<1, 1024, smem, (cudaStream_t)stream>>>(
       (const double*)scratch, ism_blocks(n), H, dv, div_mode, z_shared, params64, m, v2, opt_state,
-      beta1, beta2, eps, weight_decay, reset_lr, apply_step, params32, grads_out, loss_out, flags);
+      beta1, beta2, eps, weight_decay, reset_lr, apply_step, params32, grads_out, loss_out, flags); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
@@ -526,7 +526,7 @@ extern "C" int spic_adamw_step(double* params64, const double* grads64, double* 
                                double eps, double weight_decay, float* params32, void* stream) {
   if (P < 0) return SPIC_ERR_ARG;
   k_adamw_step<<<1, 1024, 0, (cudaStream_t)stream>>>(params64, grads64, m, v2, P, opt_state, beta1,
-                                                     beta2, eps, weight_decay, params32);
+                                                     beta2, eps, weight_decay, params32); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }

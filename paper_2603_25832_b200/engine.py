@@ -103,6 +103,18 @@ class Simulation:
             _lib.call("spic_moments", _lib.ptr(p.vp), n, _lib.ptr(p.w), n, dv, float(p.uniform_w),
                       _lib.ptr(d[4:9]), _lib.ptr(self.flags), _lib.ptr(buf), nb, st)
 
+    def step_host(self, row: int, x_host: torch.Tensor, v_host: torch.Tensor,
+                  diag_host: torch.Tensor) -> None:
+        """Public end-to-end step on HOST buffers (pinned float32 x (n,), v planes (dv, n),
+        float64 diag (DIAG_W,)): H2D of the state, one device step, D2H of the updated state
+        and of the step's diagnostics row — all enqueued on the current stream."""
+        self.p.x.copy_(x_host, non_blocking=True)
+        self.p.vp.copy_(v_host, non_blocking=True)
+        self.step(row)
+        x_host.copy_(self.p.x, non_blocking=True)
+        v_host.copy_(self.p.vp, non_blocking=True)
+        diag_host.copy_(self.diag[row], non_blocking=True)
+
     # ---- host reads -------------------------------------------------------------------------
     def check(self) -> None:
         """Raise the reference's exception for any flagged condition (one D2H read)."""

@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "scorepic_b200.h")
 
 def header_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|int64_t)\s+(spic_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|int64_t|long long)\s+(spic_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_expected_entry_points():
