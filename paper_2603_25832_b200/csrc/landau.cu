@@ -17,6 +17,7 @@
 // per-pair minimum image like the reference. Accumulation is float32 per (target, split) in
 // a fixed order; splits are summed in a fixed order by the epilogue: deterministic.
 #include <algorithm>
+#include <cstdlib>
 
 #include "pairs.cuh"
 
@@ -165,6 +166,200 @@ __global__ void __launch_bounds__(kLandauNT, 4)
   }
 }
 
+// ---- packed-FP32 (f32x2, sm_100) variant of the dominant case ---------------------------
+// DV = 3, M >= 3, gamma = -3. Each thread owns 2*RP targets held as (even, odd) pairs in
+// 64-bit registers so every arithmetic step is one FFMA2/FADD2/FMUL2 for two pairs; the
+// broadcast j-record enters as a scalar operand. |dx| is taken with FMNMX (ALU pipe) and
+// the eps2 test with FSETP+FSEL, keeping the FMA pipe for the 21 packed ops per two pairs.
+struct f2 {
+  unsigned long long r;
+};
+__device__ __forceinline__ f2 mk2(float a, float b) {
+  f2 o;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(o.r) : "f"(a), "f"(b));
+  return o;
+}
+__device__ __forceinline__ void un2(f2 a, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.r));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 o;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
+  return o;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 o;
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
+  return o;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 o;
+  asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
+  return o;
+}
+// sign-bit ops on both halves: integer LOP3 on the ALU pipe (ptxas would otherwise turn
+// fabs / negation into FADDs on the FMA pipe)
+__device__ __forceinline__ f2 abs2(f2 a) {
+  f2 o;
+  asm("and.b64 %0, %1, 0x7fffffff7fffffff;" : "=l"(o.r) : "l"(a.r));
+  return o;
+}
+__device__ __forceinline__ f2 neg2(f2 a) {
+  f2 o;
+  asm("xor.b64 %0, %1, 0x8000000080000000;" : "=l"(o.r) : "l"(a.r));
+  return o;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 o;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r));
+  return o;
+}
+
+template <int RP, int MINB, bool UNIFORM_W>
+__global__ void __launch_bounds__(kLandauNT, MINB)
+    k_landau_x2(const float4* __restrict__ xv, const float4* __restrict__ sw,
+                const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
+                int32_t* __restrict__ tile_start, int M, int S, float L, float ie, float ie2,
+                float wie, float wie2, int nsplit, float* __restrict__ Uout, int64_t ldu) {
+  // One CTA per work item (target tile, j-split): blockIdx.x = tile, blockIdx.y = split.
+  // (A persistent atomic-queue variant raised register pressure past 128/thread and cost
+  // more in register moves than it saved in tail; the host picks nsplit for full waves.)
+  constexpr int TI = kLandauNT * 2 * RP;
+  __shared__ alignas(128) float4 s_xv[kLandauStages][kLandauTJ];
+  __shared__ alignas(128) float4 s_sw[kLandauStages][kLandauTJ];
+  __shared__ alignas(8) uint64_t s_bar[kLandauStages];
+  const int tile = blockIdx.x, split = blockIdx.y;
+  if (tile >= tile_start[M]) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kLandauStages; ++s) mbar_init(&s_bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const f2 W1c = UNIFORM_W ? mk2(wie, wie) : mk2(ie, ie);
+  const f2 nW2 = UNIFORM_W ? mk2(-wie2, -wie2) : mk2(-ie2, -ie2);
+  const int qg = 0;
+  {
+    int lo = 0, hi = M;  // cell of this tile: largest c with tile_start[c] <= tile
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(tile_start + mid) <= tile) lo = mid; else hi = mid;
+    }
+    const int c = lo;
+    const int cs = cell_start[c], ce = cell_start[c + 1];
+    const int t0 = cs + (tile - tile_start[c]) * TI;
+    const int t1 = min(t0 + TI, ce);
+    Window win = build_window(cell_start, sub_start, M, S, c, t0, t1, L);
+    int wlen = 0;
+    for (int s = 0; s < win.nseg; ++s) wlen += win.len[s];
+    const int jlo = (int)(((long long)wlen * split) / nsplit);
+    const int jhi = (int)(((long long)wlen * (split + 1)) / nsplit);
+    const int ntiles = window_tiles(win, jlo, jhi);
+
+    f2 X[RP], V0[RP], V1[RP], V2[RP], S0[RP], S1[RP], S2[RP], A0[RP], A1[RP], A2[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      float4 Ae = make_float4(1e30f, 0.f, 0.f, 0.f), Be = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 Ao = Ae, Bo = Be;
+      const int pe = t0 + threadIdx.x + (2 * r) * kLandauNT;
+      const int po = pe + kLandauNT;
+      if (pe < t1) { Ae = xv[pe]; Be = sw[pe]; }
+      if (po < t1) { Ao = xv[po]; Bo = sw[po]; }
+      X[r] = mk2(Ae.x, Ao.x);
+      V0[r] = mk2(Ae.y, Ao.y); V1[r] = mk2(Ae.z, Ao.z); V2[r] = mk2(Ae.w, Ao.w);
+      S0[r] = mk2(Be.x, Bo.x); S1[r] = mk2(Be.y, Bo.y); S2[r] = mk2(Be.z, Bo.z);
+      A0[r] = A1[r] = A2[r] = mk2(0.f, 0.f);
+    }
+    auto issue = [&](int q) {
+      TileDesc d = window_tile(win, jlo, jhi, q);
+      const int st = (qg + q) % kLandauStages;
+      mbar_expect_tx(&s_bar[st], (uint32_t)(2 * d.cnt * sizeof(float4)));
+      bulk_g2s(&s_xv[st][0], xv + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
+      bulk_g2s(&s_sw[st][0], sw + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
+    };
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      for (int q = 0; q < min(ntiles, kLandauStages); ++q) issue(q);
+    }
+    for (int q = 0; q < ntiles; ++q) {
+      const int st = (qg + q) % kLandauStages;
+      TileDesc d = window_tile(win, jlo, jhi, q);
+      f2 XA[RP];
+      const f2 sh = mk2(d.shift, d.shift);
+#pragma unroll
+      for (int r = 0; r < RP; ++r) XA[r] = sub2(X[r], sh);
+      mbar_wait(&s_bar[st], (uint32_t)(((qg + q) / kLandauStages) & 1));
+      const float4* __restrict__ P = s_xv[st];
+      const float4* __restrict__ Q = s_sw[st];
+#pragma unroll 2
+      for (int jj = 0; jj < d.cnt; ++jj) {
+        const float4 A = P[jj];
+        const float4 B = Q[jj];
+        const f2 xj = mk2(A.x, A.x), vj0 = mk2(A.y, A.y), vj1 = mk2(A.z, A.z), vj2 = mk2(A.w, A.w);
+        const f2 sj0 = mk2(B.x, B.x), sj1 = mk2(B.y, B.y), sj2 = mk2(B.z, B.z);
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          const f2 dx = sub2(XA[r], xj);
+          // w psi(dx) = max(0, w/eta - |dx| w/eta^2)
+          float ce, co;
+          un2(fma2(abs2(dx), nW2, W1c), ce, co);
+          ce = fmaxf(ce, 0.f);
+          co = fmaxf(co, 0.f);
+          if (!UNIFORM_W) {
+            ce *= B.w;
+            co *= B.w;
+          }
+          const f2 z0 = sub2(V0[r], vj0), z1 = sub2(V1[r], vj1), z2 = sub2(V2[r], vj2);
+          const f2 u0 = sub2(S0[r], sj0), u1 = sub2(S1[r], sj1), u2 = sub2(S2[r], sj2);
+          const f2 zz = fma2(z2, z2, fma2(z1, z1, mul2(z0, z0)));
+          const f2 zu = fma2(z2, u2, fma2(z1, u1, mul2(z0, u0)));
+          float zze, zzo;
+          un2(zz, zze, zzo);
+          const float qe = rsqrtf(zze), qo = rsqrtf(zzo);
+          // 1/|z|, or 0 for the eps2-skipped pairs (incl. the self pair)
+          const f2 rp = mk2(zze > kEps2 ? qe : 0.f, zzo > kEps2 ? qo : 0.f);
+          const f2 cw = mul2(mk2(ce, co), rp);           // w psi / |z|
+          const f2 nq = neg2(mul2(mul2(rp, rp), zu));    // -(z.u)/|z|^2
+          A0[r] = fma2(cw, fma2(nq, z0, u0), A0[r]);
+          A1[r] = fma2(cw, fma2(nq, z1, u1), A1[r]);
+          A2[r] = fma2(cw, fma2(nq, z2, u2), A2[r]);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && q + kLandauStages < ntiles) {
+        fence_proxy_async();
+        issue(q + kLandauStages);
+      }
+    }
+    float* out = Uout + (size_t)split * 3 * ldu;
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      float a0e, a0o, a1e, a1o, a2e, a2o;
+      un2(A0[r], a0e, a0o);
+      un2(A1[r], a1e, a1o);
+      un2(A2[r], a2e, a2o);
+      const int pe = t0 + threadIdx.x + (2 * r) * kLandauNT;
+      const int po = pe + kLandauNT;
+      if (pe < t1) { out[pe] = a0e; out[ldu + pe] = a1e; out[2 * ldu + pe] = a2e; }
+      if (po < t1) { out[po] = a0o; out[ldu + po] = a1o; out[2 * ldu + po] = a2o; }
+    }
+  }
+}
+
+// resident CTAs per SM of a kernel (cached) x SM count
+template <typename K>
+static int persistent_grid_unused(K kernel, int threads) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = kNumSMs;
+  }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+  return std::max(1, per) * sms;
+}
+
 // Epilogue: sum splits in order, scatter U to pid order, collision push, H_dot/E_K/P partials.
 template <int DV>
 __global__ void __launch_bounds__(256) k_collision_epilogue(
@@ -240,6 +435,7 @@ __global__ void k_count_live(const float4* __restrict__ xv, const int32_t* __res
 }
 
 constexpr int kEpiBlocks = 2 * kNumSMs;
+constexpr int kLandauRP = 2;  // packed pairs per thread in k_landau_x2 (4 targets)
 
 template <int DV, bool MINIMG, int GMODE, bool UW>
 static void launch_landau(dim3 grid, cudaStream_t st, const float4* xv, const float4* sw,
@@ -276,14 +472,27 @@ static void dispatch_g(int gm, bool uw, dim3 g, cudaStream_t st, const float4* x
     dispatch_w<DV, MINIMG, 2>(uw, g, st, xv, sw, cs, ss, ts, M, S, L, ie, ie2, wie, wie2, hp, ns, U, ldu);
 }
 
-static int auto_nsplit(int64_t n, int M) {
-  int64_t tiles = n / kLandauTI + (M + 1) / 2;
-  if (tiles < 1) tiles = 1;
-  int64_t want = (4 * kNumSMs + tiles - 1) / tiles;
-  int64_t window = 3 * n / std::max(M, 1);  // records per window (upper bound)
-  int64_t cap = std::max<int64_t>(1, window / 512);
-  want = std::min<int64_t>(want, cap);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, 16));
+static int auto_nsplit(int64_t n, int M, int dv) {
+  // choose the j-split so the (tile, split) CTA count fills whole waves of the resident
+  // CTA slots (4 per SM): wave quantisation, not the pair count, sets the tail
+  const bool packed = dv == 3 && M >= 3;
+  const int TI = packed ? kLandauNT * 2 * 2 : kLandauTI;
+  const double tiles = std::max<double>(1.0, (double)(n / TI) + 0.5 * M);
+  const double slots = 4.0 * kNumSMs;
+  const int64_t window = 2 * n / std::max(M, 1);  // records in a culled j-window (approx.)
+  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(16, window / 1024));
+  int best = 1;
+  double best_eff = -1.0;
+  for (int ns = 1; ns <= cap; ++ns) {
+    const double waves = tiles * ns / slots;
+    double eff = waves < 1.0 ? waves : waves / std::ceil(waves);
+    eff -= 0.004 * (ns - 1);  // each split re-reads targets and writes a partial U
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = ns;
+    }
+  }
+  return best;
 }
 
 __global__ void k_fold_splits(const float* __restrict__ part, int nsplit, int dv, int64_t n,
@@ -301,7 +510,7 @@ __global__ void k_fold_splits(const float* __restrict__ part, int nsplit, int dv
 using namespace spic;
 
 extern "C" size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nsplit) {
-  if (nsplit <= 0) nsplit = auto_nsplit(n, M);
+  if (nsplit <= 0) nsplit = auto_nsplit(n, M, dv);
   size_t b = sizeof(int32_t) * (size_t)(M + 1 + 31);
   if (nsplit > 1) b += sizeof(float) * (size_t)nsplit * dv * n + 256;
   return b;
@@ -313,7 +522,7 @@ extern "C" int spic_landau(const float* xv, const float* sw, int64_t n, int32_t 
                            float* U_sorted, void* scratch, size_t scratch_bytes, void* stream) {
   if (n < 0 || n > INT32_MAX || M < 1 || S < 1 || !(eta > 0) || (dv != 2 && dv != 3))
     return SPIC_ERR_ARG;
-  if (nsplit <= 0) nsplit = auto_nsplit(n, M);
+  if (nsplit <= 0) nsplit = auto_nsplit(n, M, dv);
   if (scratch_bytes < spic_landau_scratch_bytes(n, M, dv, nsplit)) return SPIC_ERR_SCRATCH;
   if (n == 0) return SPIC_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -324,8 +533,6 @@ extern "C" int spic_landau(const float* xv, const float* sw, int64_t n, int32_t 
     p = (p + 255) & ~(uintptr_t)255;
     Upart = (float*)p;
   }
-  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, kLandauTI, tile_start); spic::count_launch();
-  SPIC_CHECK_LAUNCH();
   const double L = (double)M * eta;
   const float ie = (float)(1.0 / eta), ie2 = (float)(1.0 / (eta * eta));
   const float wie = (float)((double)uniform_w / eta), wie2 = (float)((double)uniform_w / (eta * eta));
@@ -333,8 +540,37 @@ extern "C" int spic_landau(const float* xv, const float* sw, int64_t n, int32_t 
   const float hp = (float)((gamma + 2.0) / 2.0);
   const bool minimg = M <= 2;
   const bool uw = uniform_w > 0.f;
-  dim3 grid((unsigned)(n / kLandauTI + M + 1), (unsigned)nsplit);
-  if (dv == 3) {
+  // packed f32x2 kernel for the dominant case (dv = 3, M >= 3, Coulomb gamma = -3)
+  const char* var = getenv("SPIC_LANDAU_VARIANT");
+  const bool packed = dv == 3 && !minimg && gm == 0 && !(var && var[0] == 's');
+  // experiment knob: SPIC_LANDAU_VARIANT = s (scalar) | 1 (RP1) | 3 (RP3) | 4 (RP2, 4 CTA/SM)
+  const int cfg = (var && var[0] >= '1' && var[0] <= '4') ? var[0] - '0' : 2;
+  const int rp = cfg == 1 ? 1 : (cfg == 3 ? 3 : 2);
+  const int TI = packed ? kLandauNT * 2 * rp : kLandauTI;
+  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start); spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  dim3 grid((unsigned)(n / TI + M + 1), (unsigned)nsplit);
+  if (packed) {
+#define SPIC_X2(RP_, MB_)                                                                    \
+  do {                                                                                        \
+    if (uw)                                                                                   \
+      k_landau_x2<RP_, MB_, true><<<grid, kLandauNT, 0, st>>>(                                \
+          (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,      \
+          (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                    \
+    else                                                                                      \
+      k_landau_x2<RP_, MB_, false><<<grid, kLandauNT, 0, st>>>(                               \
+          (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,      \
+          (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                    \
+  } while (0)
+    switch (cfg) {
+      case 1: SPIC_X2(1, 6); break;
+      case 3: SPIC_X2(3, 2); break;
+      case 4: SPIC_X2(2, 3); break;
+      default: SPIC_X2(2, 4); break;
+    }
+#undef SPIC_X2
+    spic::count_launch();
+  } else if (dv == 3) {
     if (minimg)
       dispatch_g<3, true>(gm, uw, grid, st, (const float4*)xv, (const float4*)sw, cell_start,
                           sub_start, tile_start, M, S, (float)L, ie, ie2, wie, wie2, hp, nsplit,

@@ -180,7 +180,10 @@ static __global__ void k_landau_tiles(const int32_t* __restrict__ cell_start, in
     carry += ws[32];
     __syncthreads();
   }
-  if (threadIdx.x == 0) tile_start[M] = carry;
+  if (threadIdx.x == 0) {
+    tile_start[M] = carry;
+    tile_start[M + 1] = 0;  // work-queue counter of the persistent pair kernels
+  }
 }
 
 }  // namespace spic
