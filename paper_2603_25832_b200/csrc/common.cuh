@@ -19,6 +19,14 @@ void count_launch();
 constexpr int kWarp = 32;
 constexpr int kNumSMs = 148;
 
+// MUFU.RCP without the IEEE slow path (__frcp_rn compiles to a refinement + a CALL);
+// ~1 ulp, used where the argument is >= 1 (softsign) or the result feeds float32 sums.
+__device__ __forceinline__ float fast_rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -134,11 +134,11 @@ __global__ void __launch_bounds__(kLandauNT, 4)
           cw = cpsi * rr;
           q2 = zu * (rr * rr);
         } else if (GMODE == 1) {
-          float iz = live ? __frcp_rn(zz) : 0.f;
+          float iz = live ? fast_rcp(zz) : 0.f;
           cw = live ? cpsi : 0.f;
           q2 = zu * iz;
         } else {
-          float iz = live ? __frcp_rn(zz) : 0.f;
+          float iz = live ? fast_rcp(zz) : 0.f;
           cw = live ? cpsi * exp2f(half_pow * __log2f(zz)) : 0.f;
           q2 = zu * iz;
         }

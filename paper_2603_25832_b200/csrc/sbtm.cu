@@ -21,7 +21,7 @@
 namespace spic {
 
 constexpr int kIsmNT = 256;     // threads per block == particles per chunk
-constexpr int kIsmBlocksMax = 2 * kNumSMs;
+constexpr int kIsmBlocksMax = 4 * kNumSMs;
 constexpr int kIsmAcc = 10;     // per (h, group): gW1[4], gb1, gW2[3], Phi, pad
 
 __host__ __device__ inline int64_t n_params(int H, int dv) {
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) k_mlp_forward(
       const float4 a = Wp[h];
       const float4 b = Bp[h];
       float z = fmaf(a.w, v2, fmaf(a.z, v1, fmaf(a.y, v0, fmaf(a.x, xn, b.x))));
-      float act = z * __frcp_rn(1.f + fabsf(z));
+      float act = z * fast_rcp(1.f + fabsf(z));
       s0 = fmaf(b.y, act, s0);
       s1 = fmaf(b.z, act, s1);
       s2 = fmaf(b.w, act, s2);
@@ -177,11 +177,12 @@ __global__ void __launch_bounds__(kIsmNT) k_ism_partials(
     }
     if (MODE == 3) wp *= inv_wsum;
     float s0 = b2[0], s1 = b2[1], s2 = b2[2], div = 0.f;
+#pragma unroll 4
     for (int h = 0; h < H; ++h) {
       const float4 a = Wp[h];
       const float4 b = Bp[h];
       float z = fmaf(a.w, v2, fmaf(a.z, v1, fmaf(a.y, v0, fmaf(a.x, xn, b.x))));
-      float inv = __frcp_rn(1.f + fabsf(z));
+      float inv = fast_rcp(1.f + fabsf(z));
       float act = z * inv;
       s0 = fmaf(b.y, act, s0);
       s1 = fmaf(b.z, act, s1);
@@ -225,11 +226,12 @@ __global__ void __launch_bounds__(kIsmNT) k_ism_partials(
       const float ch_ = (MODE == 0 || MODE == 1) ? coef[h] : 0.f;
       float gw0 = 0.f, gw1 = 0.f, gw2 = 0.f, gw3 = 0.f, gb = 0.f;
       float gv0 = 0.f, gv1 = 0.f, gv2 = 0.f, phi = 0.f;
+#pragma unroll 4
       for (int q = g; q < np; q += G) {
         const float4 u = Uc[q];
         const float4 gs = Gc[q];
         float z = fmaf(a.w, u.w, fmaf(a.z, u.z, fmaf(a.y, u.y, fmaf(a.x, u.x, b.x))));
-        float inv = __frcp_rn(1.f + fabsf(z));
+        float inv = fast_rcp(1.f + fabsf(z));
         float act = z * inv;
         float sp = inv * inv;
         float da = fmaf(gs.z, b.w, fmaf(gs.y, b.z, gs.x * b.y));
@@ -398,6 +400,17 @@ __global__ void __launch_bounds__(1024) k_sbtm_finalize(
   }
 }
 
+// Deterministic column sums of the [rows][width] block partials into one row (multi-CTA:
+// one thread per column, rows in order), so the single-CTA finalize reads one row.
+__global__ void k_ism_reduce_cols(const double* __restrict__ part, int rows, int64_t width,
+                                  double* __restrict__ out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= width) return;
+  double s = 0.0;
+  for (int r = 0; r < rows; ++r) s += part[(size_t)r * width + k];
+  out[k] = s;
+}
+
 static int ism_blocks(int64_t n) {
   int64_t chunks = (n + kIsmNT - 1) / kIsmNT;
   return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, kIsmBlocksMax));
@@ -432,7 +445,8 @@ extern "C" int spic_mlp_forward(const float* params32, int32_t H, int32_t dv, co
 }
 
 extern "C" size_t spic_ism_scratch_bytes(int64_t n, int32_t H, int32_t dv) {
-  return sizeof(double) * (size_t)ism_blocks(n) * (size_t)(1 + n_params(H, dv) + H) + 64;
+  // [blocks][width] partials + one reduced row
+  return sizeof(double) * (size_t)(ism_blocks(n) + 1) * (size_t)(1 + n_params(H, dv) + H) + 64;
 }
 
 // mode: 0 exact, 1 shared Hutchinson (Z = z_shared float[dv] on device), 2 per-particle
@@ -470,6 +484,11 @@ extern "C" int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv
   }
 #undef SPIC_ISM_LAUNCH
   SPIC_CHECK_LAUNCH();
+  const int64_t width = 1 + n_params(H, dv) + H;
+  double* part = (double*)scratch;
+  k_ism_reduce_cols<<<(unsigned)((width + 127) / 128), 128, 0, st>>>(
+      part, blocks, width, part + (size_t)blocks * width); spic::count_launch();
+  SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
 
@@ -487,7 +506,8 @@ extern "C" int spic_sbtm_finalize_ex(const void* scratch, int64_t n, int32_t H, 
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_sbtm_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_sbtm_finalize<<<1, 1024, smem, (cudaStream_t)stream>>>(
-      (const double*)scratch, ism_blocks(n), H, dv, div_mode, z_shared, params64, m, v2, opt_state,
+      (const double*)scratch + (size_t)ism_blocks(n) * (size_t)(1 + n_params(H, dv) + H), 1, H, dv,
+      div_mode, z_shared, params64, m, v2, opt_state,
       beta1, beta2, eps, weight_decay, reset_lr, apply_step, params32, grads_out, loss_out, flags); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
