@@ -264,6 +264,44 @@ def build_sim(wl: dict, seed: int, device):
     return sim
 
 
+def build_dist_sim(wl: dict, seed: int, device, world: int):
+    """Weak-scaled decomposed problem: world x (n, M, L) of the workload, cell ranges per rank."""
+    from paper_2603_25832_b200.dist_engine import DistSimulation
+    from paper_2603_25832_b200.parallel import CellPartition, Comm
+    from paper_2603_25832_b200.pic import Grid, deposit
+    from paper_2603_25832_b200.run import initial_fields
+    from paper_2603_25832_b200.sampling import sample_arrays
+    from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    wl = dict(wl, n=wl["n"] * world, M=wl["M"] * world, L=wl["L"] * world)
+    cfg = make_config(wl, seed)
+    rng = np.random.default_rng(seed)
+    x, v, w = sample_arrays(cfg, rng)
+    grid = Grid(cfg.M, cfg.eta)
+    comm = Comm()
+    part = CellPartition.equal(cfg.M, world)
+    cell = np.minimum(np.floor(x.astype(np.float32).astype(np.float64) / grid.eta).astype(np.int64) % cfg.M,
+                      cfg.M - 1)
+    lo, hi = part.owned(comm.rank)
+    own = np.nonzero((cell >= lo) & (cell < hi))[0]
+    # global initial fields from the full ensemble (identical on every rank)
+    pfull = ParticleEnsemble.from_arrays(x, v, w, device=device)
+    rho, J = deposit(pfull, grid)
+    fields = initial_fields(cfg, grid, rho, J)
+    del pfull
+    if wl["estimator"] == "sbtm":
+        net = MlpScoreNet.init_glorot(cfg.dv, cfg.hidden, rng, device=device)
+        est = SbtmEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay,
+                            divergence=cfg.divergence, rademacher=cfg.rademacher)
+    else:
+        est = BlobEstimator(grid, float(wl["bandwidth"]))
+    sim = DistSimulation(x[own], v[own], w[own], own, fields, grid, dt=cfg.dt, nu=cfg.nu,
+                         mode=cfg.mode, gamma=cfg.gamma, estimator=est, comm=comm, partition=part,
+                         n_global=cfg.n, max_rows=4)
+    return sim
+
+
 def main():
     args = parse_args()
     wl = WORKLOADS[args.workload]
@@ -306,9 +344,9 @@ def main():
     device = torch.device("cuda", local)
     _lib.load(build_if_missing=False)
 
-    # each rank owns an independent ensemble of the workload's size (weak scaling; the
-    # particle state is partitioned across ranks, no data-path collective)
-    sim = build_sim(wl, args.seed + rank, device)
+    # N = 1: the single-GPU engine. N > 1: the cell-range decomposition of a weak-scaled
+    # problem (N x particles, cells and domain length) over NCCL.
+    sim = build_dist_sim(wl, args.seed, device, world) if world > 1 else build_sim(wl, args.seed, device)
     n = wl["n"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
 
@@ -316,7 +354,7 @@ def main():
         sim.step(0)
     torch.cuda.synchronize()
     sim.check()
-    live0 = count_live_pairs(sim.ci, sim.p, sim.grid)
+    live0 = count_live_pairs(sim.ci, sim.p, sim.grid) if world == 1 else 0
     peak = fp32_peak_tflops(torch, _lib)
 
     if dist:
@@ -341,9 +379,10 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     coll_ms = [a.elapsed_time(b) for a, b in sim.collision_events]
-    live1 = count_live_pairs(sim.ci, sim.p, sim.grid)
+    live1 = count_live_pairs(sim.ci, sim.p, sim.grid) if world == 1 else 0
     live = 0.5 * (live0 + live1)
-    t = torch.tensor([total_ms, statistics.mean(coll_ms)], dtype=torch.float64, device=device)
+    t = torch.tensor([total_ms, statistics.mean(coll_ms) if coll_ms else float("nan")],
+                     dtype=torch.float64, device=device)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
@@ -352,7 +391,7 @@ def main():
 
     # end to end through the public host-buffer API
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         dv = sim.p.dv
         xh = torch.empty(n, dtype=torch.float32).pin_memory()
         vh = torch.empty(dv, n, dtype=torch.float32).pin_memory()
@@ -398,7 +437,9 @@ def main():
                    .format(wl["hidden"]),
                    "divergence": wl["divergence"], "sub_cells": sim.S,
                    "l2": "flushed between timed steps (256 MiB write, outside timed windows)",
-                   "parallelism": f"{world} rank(s), independent ensembles per rank"},
+                   "parallelism": ("single GPU" if world == 1 else
+                        f"cell-range decomposition over {world} ranks (NCCL): migration, "
+                        "halo, rho/J and ISM-gradient allreduces")},
         "pair_interactions_per_s": world * live / (coll_avg_ms * 1e-3),
         "live_pairs_per_step": live,
         "collision_ms": coll_avg_ms,

@@ -89,6 +89,13 @@ int spic_landau(const float* xv, const float* sw, int64_t n, int32_t dv, const i
                 const int32_t* sub_start, int32_t M, int32_t S, double eta, double gamma,
                 float uniform_w, int32_t nsplit, float* U_sorted, void* scratch,
                 size_t scratch_bytes, void* stream);
+/* Same, with targets restricted to the cells [c_lo, c_hi) (a domain rank's owned cells;
+ * halo cells only act as neighbours). U_sorted entries of other cells are not written. */
+int spic_landau_range(const float* xv, const float* sw, int64_t n, int32_t dv,
+                      const int32_t* cell_start, const int32_t* sub_start, int32_t M, int32_t S,
+                      double eta, double gamma, float uniform_w, int32_t nsplit, int32_t c_lo,
+                      int32_t c_hi, float* U_sorted, void* scratch, size_t scratch_bytes,
+                      void* stream);
 /* Sum nsplit partial U planes [nsplit][dv][n] into U_sorted in a fixed order. */
 int spic_landau_fold(const float* U_part, int32_t nsplit, int32_t dv, int64_t n, float* U_sorted,
                      void* stream);
@@ -99,6 +106,12 @@ int spic_collision_epilogue(const float* U_sorted, const float* sw, const int32_
                             int64_t n, int32_t dv, float nu_dt, float* v, int64_t ldv,
                             float* U_pid, int64_t ldu, double* red_out, int32_t* flags,
                             void* scratch, size_t scratch_bytes, void* stream);
+/* Same over the sorted positions [k0, k1) only (a domain rank's owned targets). */
+int spic_collision_epilogue_range(const float* U_sorted, const float* sw, const int32_t* perm,
+                                  int64_t n, int32_t dv, int64_t k0, int64_t k1, float nu_dt,
+                                  float* v, int64_t ldv, float* U_pid, int64_t ldu,
+                                  double* red_out, int32_t* flags, void* scratch,
+                                  size_t scratch_bytes, void* stream);
 /* number of ordered live pairs |min-image dx| < eta over the stencil (the pair-rate unit) */
 int spic_count_live_pairs(const float* xv, int64_t n, const int32_t* cell_start, int32_t M,
                           double eta, unsigned long long* count, void* stream);
@@ -153,6 +166,9 @@ int spic_sbtm_finalize_ex(const void* scratch, int64_t n, int32_t H, int32_t dv,
                           float* params32, double* grads_out, double* loss_out, int32_t* flags,
                           void* stream);
 
+/* Byte offset of the reduced row [loss, grads (P), Phi (H)] (float64) inside the ISM scratch;
+ * a domain-decomposed run allreduces this row between partials and finalize. */
+int64_t spic_ism_row_offset(int64_t n, int32_t H, int32_t dv);
 /* Plain AdamW step (ref: score.py:371-386) on a flat float64 vector with precomputed
  * gradients; opt_state = {t, unused, lr, 0}; t is incremented on device. */
 int spic_adamw_step(double* params64, const double* grads64, double* m, double* v2, int64_t P,

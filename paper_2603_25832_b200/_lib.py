@@ -49,9 +49,13 @@ SIGNATURES = {
     "spic_landau_scratch_bytes": (_SZ, [_I64, _I32, _I32, _I32]),
     "spic_landau": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P, _I32, _I32, _D, _D, _F, _I32, _P,
                                    _P, _SZ, _P]),
+    "spic_landau_range": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P, _I32, _I32, _D, _D, _F, _I32,
+                                         _I32, _I32, _P, _P, _SZ, _P]),
     "spic_landau_fold": (ctypes.c_int, [_P, _I32, _I32, _I64, _P, _P]),
     "spic_collision_epilogue": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _F, _P, _I64, _P, _I64, _P,
                                                _P, _P, _SZ, _P]),
+    "spic_collision_epilogue_range": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I64, _I64, _F, _P,
+                                                     _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
     "spic_count_live_pairs": (ctypes.c_int, [_P, _I64, _P, _I32, _D, _P, _P]),
     "spic_blob_scratch_bytes": (_SZ, [_I64, _I32, _I32]),
     "spic_blob": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _P, _P, _I32, _I32, _D, _D, _F, _P, _P,
@@ -64,6 +68,7 @@ SIGNATURES = {
                                             _F, _P, _I64, _P, _D, _P, _SZ, _P]),
     "spic_sbtm_finalize_ex": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _D,
                                              _D, _D, _D, _I32, _I32, _P, _P, _P, _P, _P]),
+    "spic_ism_row_offset": (_I64, [_I64, _I32, _I32]),
     "spic_adamw_step": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _D, _D, _D, _D, _P, _P]),
     "spic_push": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _P, _P, _P, _I32, _D, _F, _P, _P]),
     "spic_deposit_scratch_bytes": (_SZ, [_I32, _I32]),

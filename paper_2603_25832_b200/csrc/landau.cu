@@ -365,11 +365,12 @@ template <int DV>
 __global__ void __launch_bounds__(256) k_collision_epilogue(
     const float* __restrict__ Us, int nsplit, int64_t n, const float4* __restrict__ sw,
     const int32_t* __restrict__ perm, float nu_dt, float* __restrict__ v, int64_t ldv,
-    float* __restrict__ Upid, int64_t ldu, double* __restrict__ partials, int32_t* flags) {
+    float* __restrict__ Upid, int64_t ldu, double* __restrict__ partials, int32_t* flags,
+    int64_t k0, int64_t k1) {
   __shared__ double scratch[8 * 5];
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   bool bad = false;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+  for (int64_t k = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k1;
        k += (int64_t)gridDim.x * blockDim.x) {
     float U[3] = {0.f, 0.f, 0.f};
     for (int s = 0; s < nsplit; ++s)
@@ -516,10 +517,26 @@ extern "C" size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, in
   return b;
 }
 
+extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, int32_t dv,
+                                 const int32_t* cell_start, const int32_t* sub_start, int32_t M,
+                                 int32_t S, double eta, double gamma, float uniform_w,
+                                 int32_t nsplit, int32_t c_lo, int32_t c_hi, float* U_sorted,
+                                 void* scratch, size_t scratch_bytes, void* stream);
+
 extern "C" int spic_landau(const float* xv, const float* sw, int64_t n, int32_t dv,
                            const int32_t* cell_start, const int32_t* sub_start, int32_t M,
                            int32_t S, double eta, double gamma, float uniform_w, int32_t nsplit,
                            float* U_sorted, void* scratch, size_t scratch_bytes, void* stream) {
+  return spic_landau_range(xv, sw, n, dv, cell_start, sub_start, M, S, eta, gamma, uniform_w,
+                           nsplit, 0, M, U_sorted, scratch, scratch_bytes, stream);
+}
+
+extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, int32_t dv,
+                                 const int32_t* cell_start, const int32_t* sub_start, int32_t M,
+                                 int32_t S, double eta, double gamma, float uniform_w,
+                                 int32_t nsplit, int32_t c_lo, int32_t c_hi, float* U_sorted,
+                                 void* scratch, size_t scratch_bytes, void* stream) {
+  if (c_lo < 0 || c_hi > M || c_lo > c_hi) return SPIC_ERR_ARG;
   if (n < 0 || n > INT32_MAX || M < 1 || S < 1 || !(eta > 0) || (dv != 2 && dv != 3))
     return SPIC_ERR_ARG;
   if (nsplit <= 0) nsplit = auto_nsplit(n, M, dv);
@@ -547,7 +564,7 @@ extern "C" int spic_landau(const float* xv, const float* sw, int64_t n, int32_t 
   const int cfg = (var && var[0] >= '1' && var[0] <= '4') ? var[0] - '0' : 2;
   const int rp = cfg == 1 ? 1 : (cfg == 3 ? 3 : 2);
   const int TI = packed ? kLandauNT * 2 * rp : kLandauTI;
-  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start); spic::count_launch();
+  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start, c_lo, c_hi); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   dim3 grid((unsigned)(n / TI + M + 1), (unsigned)nsplit);
   if (packed) {
@@ -608,20 +625,22 @@ extern "C" int spic_landau_fold(const float* U_part, int32_t nsplit, int32_t dv,
   return SPIC_OK;
 }
 
-extern "C" int spic_collision_epilogue(const float* U_sorted, const float* sw, const int32_t* perm,
-                                       int64_t n, int32_t dv, float nu_dt, float* v, int64_t ldv,
-                                       float* U_pid, int64_t ldu, double* red_out, int32_t* flags,
-                                       void* scratch, size_t scratch_bytes, void* stream) {
-  if (n < 0 || (dv != 2 && dv != 3)) return SPIC_ERR_ARG;
+extern "C" int spic_collision_epilogue_range(const float* U_sorted, const float* sw,
+                                             const int32_t* perm, int64_t n, int32_t dv,
+                                             int64_t k0, int64_t k1, float nu_dt, float* v,
+                                             int64_t ldv, float* U_pid, int64_t ldu,
+                                             double* red_out, int32_t* flags, void* scratch,
+                                             size_t scratch_bytes, void* stream) {
+  if (n < 0 || (dv != 2 && dv != 3) || k0 < 0 || k1 > n || k0 > k1) return SPIC_ERR_ARG;
   if (scratch_bytes < sizeof(double) * kEpiBlocks * 5) return SPIC_ERR_SCRATCH;
   cudaStream_t st = (cudaStream_t)stream;
   double* part = (double*)scratch;
   if (dv == 3)
     k_collision_epilogue<3><<<kEpiBlocks, 256, 0, st>>>(U_sorted, 1, n, (const float4*)sw, perm,
-                                                        nu_dt, v, ldv, U_pid, ldu, part, flags);
+                                                        nu_dt, v, ldv, U_pid, ldu, part, flags, k0, k1);
   else
     k_collision_epilogue<2><<<kEpiBlocks, 256, 0, st>>>(U_sorted, 1, n, (const float4*)sw, perm,
-                                                        nu_dt, v, ldv, U_pid, ldu, part, flags);
+                                                        nu_dt, v, ldv, U_pid, ldu, part, flags, k0, k1);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   if (red_out) {
@@ -629,6 +648,14 @@ extern "C" int spic_collision_epilogue(const float* U_sorted, const float* sw, c
     SPIC_CHECK_LAUNCH();
   }
   return SPIC_OK;
+}
+
+extern "C" int spic_collision_epilogue(const float* U_sorted, const float* sw, const int32_t* perm,
+                                       int64_t n, int32_t dv, float nu_dt, float* v, int64_t ldv,
+                                       float* U_pid, int64_t ldu, double* red_out, int32_t* flags,
+                                       void* scratch, size_t scratch_bytes, void* stream) {
+  return spic_collision_epilogue_range(U_sorted, sw, perm, n, dv, 0, n, nu_dt, v, ldv, U_pid, ldu,
+                                       red_out, flags, scratch, scratch_bytes, stream);
 }
 
 extern "C" int spic_count_live_pairs(const float* xv, int64_t n, const int32_t* cell_start,

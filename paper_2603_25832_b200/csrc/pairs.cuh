@@ -150,13 +150,15 @@ static __device__ Window build_window(const int32_t* __restrict__ cell_start,
 }
 
 static __global__ void k_landau_tiles(const int32_t* __restrict__ cell_start, int M, int TI,
-                               int32_t* __restrict__ tile_start) {
+                                      int32_t* __restrict__ tile_start, int c_lo = 0,
+                                      int c_hi = 1 << 30) {
   // single CTA exclusive scan of ceil(count_c / TI)
   __shared__ int ws[33];
   int carry = 0;
   for (int base = 0; base < M; base += blockDim.x) {
     int c = base + threadIdx.x;
-    int v = c < M ? (cell_start[c + 1] - cell_start[c] + TI - 1) / TI : 0;
+    // target cells outside [c_lo, c_hi) (halo cells of a domain rank) get no tiles
+    int v = (c < M && c >= c_lo && c < c_hi) ? (cell_start[c + 1] - cell_start[c] + TI - 1) / TI : 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int inc = v;
     for (int o = 1; o < 32; o <<= 1) {

@@ -550,3 +550,9 @@ extern "C" int spic_adamw_step(double* params64, const double* grads64, double* 
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
+
+// Byte offset (in the ISM scratch) of the reduced [loss, grads, Phi] row that
+// spic_sbtm_finalize_ex reads: a domain-decomposed run allreduces this row in place.
+extern "C" int64_t spic_ism_row_offset(int64_t n, int32_t H, int32_t dv) {
+  return (int64_t)sizeof(double) * ism_blocks(n) * (1 + n_params(H, dv) + H);
+}

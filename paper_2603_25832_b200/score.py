@@ -260,7 +260,11 @@ class SbtmTrainer:
         return DIV_SHARED if self.rademacher == "shared" else DIV_PER_PARTICLE
 
     def run(self, n: int, *, ci: CellIndex | None = None, particles: ParticleEnsemble | None = None,
-            flags=None) -> None:
+            flags=None, reduce_row=None, gid=None, n_global: int | None = None) -> None:
+        """K ISM steps. reduce_row(row) (optional) is applied to the reduced float64 row
+        [loss, grads, Phi] before each finalize (the cross-rank allreduce); gid (optional)
+        maps sorted records to global particle ids for per-particle probes drawn over
+        n_global particles."""
         mode = self.mode()
         dv = self.net.dv
         Zp = None
@@ -271,16 +275,23 @@ class SbtmTrainer:
                 self.z_shared.copy_(self._pinned_z, non_blocking=True)
         for k in range(self.K):
             if mode == DIV_PER_PARTICLE:
-                Zp = _planes(draw_probe(self.rng, (n, dv)), self.net.params32.device)
+                Zp = _planes(draw_probe(self.rng, (n_global or n, dv)), self.net.params32.device)
             zk = self.z_shared[k] if mode == DIV_SHARED else None
             if ci is not None:
+                idx = None
+                if mode == DIV_PER_PARTICLE:
+                    idx = ci.perm if gid is None else gid
                 buf = _partials(self.net, mode, n=n, x_scale=1.0 / self.L, xv=ci.xv, sw=ci.sw,
-                                Z=zk if mode == DIV_SHARED else Zp, ldz=n,
-                                idx=ci.perm if mode == DIV_PER_PARTICLE else None)
+                                Z=zk if mode == DIV_SHARED else Zp,
+                                ldz=Zp.shape[1] if Zp is not None else n, idx=idx)
             else:
                 buf = _partials(self.net, mode, n=n, x_scale=1.0 / self.L, x=particles.x,
                                 vp=particles.vp, w=particles.w,
                                 Z=zk if mode == DIV_SHARED else Zp, ldz=n)
+            if reduce_row is not None:
+                off = int(_lib.query("spic_ism_row_offset", n, self.net.hidden, dv)) // 8
+                width = 1 + self.net.n_params + self.net.hidden
+                reduce_row(buf.view(torch.float64)[off:off + width])
             _finalize(self.net, buf, n, mode, z=zk, opt=self.opt, reset_lr=(k == 0),
                       apply_step=True, loss_out=self.losses[k:k + 1], flags=flags)
 
