@@ -264,6 +264,49 @@ def build_sim(wl: dict, seed: int, device):
     return sim
 
 
+def config1_microbench(torch, device, n: int = 131072, reps: int = 3) -> dict:
+    """BASELINE config 1: one cell, co-located x (so w psi = 1/n), v from the equal mixture of
+    N((+-1.5, 0, 0), I3), exact mixture score; all n^2 ordered pairs are live. Times the pair
+    kernel alone (CUDA events) and checks momentum / energy conservation of U."""
+    from paper_2603_25832_b200 import _lib
+    from paper_2603_25832_b200.collision import build_cell_index, landau_sorted
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    rng = np.random.default_rng(1)
+    L = 2.0
+    v = rng.normal(size=(n, 3))
+    v[:, 0] += np.where(rng.random(n) < 0.5, 1.5, -1.5)
+    s = -v.copy()
+    s[:, 0] = -v[:, 0] + 1.5 * np.tanh(1.5 * v[:, 0])
+    p = ParticleEnsemble.from_arrays(np.full(n, 1.0), v, np.full(n, L / n), device=device)
+    grid = Grid(1, L)
+    ci = build_cell_index(p, grid)
+    sp = torch.as_tensor(s, dtype=torch.float32, device=device).t().contiguous()
+    _lib.call("spic_gather_scores", _lib.ptr(sp), n, _lib.ptr(ci.perm), n, 3, _lib.ptr(ci.sw), None,
+              _lib.stream_handle())
+    U = torch.empty(3, n, dtype=torch.float32, device=device)
+    landau_sorted(ci, p, grid, -3.0, U)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        landau_sorted(ci, p, grid, -3.0, U)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    Us = U.double().cpu().numpy().T
+    vs = ci.xv[:, 1:4].double().cpu().numpy()
+    wU = (L / n) * Us
+    mom = float(np.max(np.abs(wU.sum(0))) / (np.max(np.abs(wU)) * n))
+    en = abs(float(np.sum((L / n) * np.einsum("ij,ij->i", vs, Us))))
+    en /= float(np.sum((L / n) * np.linalg.norm(vs, axis=1) * np.linalg.norm(Us, axis=1)))
+    pairs = float(n) * n
+    return {"n": n, "ms": ms, "pair_interactions_per_s": pairs / (ms * 1e-3),
+            "tflops": FLOP_PER_PAIR * pairs / (ms * 1e-3) / 1e12,
+            "momentum_rel": mom, "energy_rel": en}
+
+
 def build_dist_sim(wl: dict, seed: int, device, world: int):
     """Weak-scaled decomposed problem: world x (n, M, L) of the workload, cell ranges per rank."""
     from paper_2603_25832_b200.dist_engine import DistSimulation
@@ -452,6 +495,13 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    if world == 1:
+        try:
+            mb = config1_microbench(torch, device)
+            mb["frac_of_fp32_peak"] = mb["tflops"] / peak
+            out["config1_microbench"] = mb
+        except Exception as exc:  # noqa: BLE001
+            out["config1_microbench"] = {"error": str(exc)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line = cpu_baseline_line(wl, args.seed)

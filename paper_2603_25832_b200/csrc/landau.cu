@@ -209,13 +209,18 @@ __device__ __forceinline__ f2 neg2(f2 a) {
   asm("xor.b64 %0, %1, 0x8000000080000000;" : "=l"(o.r) : "l"(a.r));
   return o;
 }
+__device__ __forceinline__ f2 rint2(f2 a) {
+  float lo, hi;
+  un2(a, lo, hi);
+  return mk2(rintf(lo), rintf(hi));
+}
 __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   f2 o;
   asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r));
   return o;
 }
 
-template <int RP, int MINB, bool UNIFORM_W>
+template <int RP, int MINB, bool UNIFORM_W, bool MINIMG>
 __global__ void __launch_bounds__(kLandauNT, MINB)
     k_landau_x2(const float4* __restrict__ xv, const float4* __restrict__ sw,
                 const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
@@ -237,6 +242,7 @@ __global__ void __launch_bounds__(kLandauNT, MINB)
   __syncthreads();
   const f2 W1c = UNIFORM_W ? mk2(wie, wie) : mk2(ie, ie);
   const f2 nW2 = UNIFORM_W ? mk2(-wie2, -wie2) : mk2(-ie2, -ie2);
+  const f2 invL2 = mk2(1.0f / L, 1.0f / L), negL2 = mk2(-L, -L);
   const int qg = 0;
   {
     int lo = 0, hi = M;  // cell of this tile: largest c with tile_start[c] <= tile
@@ -298,7 +304,8 @@ __global__ void __launch_bounds__(kLandauNT, MINB)
         const f2 sj0 = mk2(B.x, B.x), sj1 = mk2(B.y, B.y), sj2 = mk2(B.z, B.z);
 #pragma unroll
         for (int r = 0; r < RP; ++r) {
-          const f2 dx = sub2(XA[r], xj);
+          f2 dx = sub2(XA[r], xj);
+          if (MINIMG) dx = fma2(rint2(mul2(dx, invL2)), negL2, dx);  // M <= 2: minimum image
           // w psi(dx) = max(0, w/eta - |dx| w/eta^2)
           float ce, co;
           un2(fma2(abs2(dx), nW2, W1c), ce, co);
@@ -476,7 +483,7 @@ static void dispatch_g(int gm, bool uw, dim3 g, cudaStream_t st, const float4* x
 static int auto_nsplit(int64_t n, int M, int dv) {
   // choose the j-split so the (tile, split) CTA count fills whole waves of the resident
   // CTA slots (4 per SM): wave quantisation, not the pair count, sets the tail
-  const bool packed = dv == 3 && M >= 3;
+  const bool packed = dv == 3;
   const int TI = packed ? kLandauNT * 2 * 2 : kLandauTI;
   const double tiles = std::max<double>(1.0, (double)(n / TI) + 0.5 * M);
   const double slots = 4.0 * kNumSMs;
@@ -559,7 +566,7 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   const bool uw = uniform_w > 0.f;
   // packed f32x2 kernel for the dominant case (dv = 3, M >= 3, Coulomb gamma = -3)
   const char* var = getenv("SPIC_LANDAU_VARIANT");
-  const bool packed = dv == 3 && !minimg && gm == 0 && !(var && var[0] == 's');
+  const bool packed = dv == 3 && gm == 0 && !(var && var[0] == 's');
   // experiment knob: SPIC_LANDAU_VARIANT = s (scalar) | 1 (RP1) | 3 (RP3) | 4 (RP2, 4 CTA/SM)
   const int cfg = (var && var[0] >= '1' && var[0] <= '4') ? var[0] - '0' : 2;
   const int rp = cfg == 1 ? 1 : (cfg == 3 ? 3 : 2);
@@ -570,14 +577,25 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   if (packed) {
 #define SPIC_X2(RP_, MB_)                                                                    \
   do {                                                                                        \
-    if (uw)                                                                                   \
-      k_landau_x2<RP_, MB_, true><<<grid, kLandauNT, 0, st>>>(                                \
-          (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,      \
-          (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                    \
-    else                                                                                      \
-      k_landau_x2<RP_, MB_, false><<<grid, kLandauNT, 0, st>>>(                               \
-          (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,      \
-          (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                    \
+    if (minimg) {                                                                             \
+      if (uw)                                                                                 \
+        k_landau_x2<RP_, MB_, true, true><<<grid, kLandauNT, 0, st>>>(                        \
+            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
+            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
+      else                                                                                    \
+        k_landau_x2<RP_, MB_, false, true><<<grid, kLandauNT, 0, st>>>(                       \
+            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
+            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
+    } else {                                                                                  \
+      if (uw)                                                                                 \
+        k_landau_x2<RP_, MB_, true, false><<<grid, kLandauNT, 0, st>>>(                       \
+            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
+            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
+      else                                                                                    \
+        k_landau_x2<RP_, MB_, false, false><<<grid, kLandauNT, 0, st>>>(                      \
+            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
+            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
+    }                                                                                         \
   } while (0)
     switch (cfg) {
       case 1: SPIC_X2(1, 6); break;
