@@ -429,3 +429,43 @@ def test_dist_engine_single_rank_matches_engine(spic, estimator):
     gid, x2, v2 = s2.gather_state()
     np.testing.assert_allclose(x2, p1.x.double().cpu().numpy()[gid], rtol=0, atol=1e-6)
     np.testing.assert_allclose(v2, p1.v.double().cpu().numpy()[gid], rtol=1e-6, atol=1e-6)
+
+
+# ---------------------------------------------------------------------------- run() end to end
+@pytest.mark.parametrize("tag", ["sbtm", "blob", "vml"])
+def test_run_matches_reference_run(spic, golden, tmp_path, tag):
+    """The solver entry point run() (sampling, Poisson init, SBTM pretraining on device, the
+    step engine, CSV + snapshot output) against the reference's own run() traces."""
+    from paper_2603_25832_b200.config import build_config
+    from paper_2603_25832_b200.diagnostics import read_diagnostics_csv, read_snapshot
+    from paper_2603_25832_b200.run import run
+
+    g = golden("run.npz")
+    cfgs = {
+        "sbtm": dict(preset="landau_damping", n=4096, M=16, dt=0.05, t_final=0.25, nu=0.1, K=3,
+                     hidden=16, lr=1e-3, weight_decay=0.0, divergence="exact",
+                     pretrain_budget=40, pretrain_batch=512, alpha=0.1, seed=3),
+        "blob": dict(preset="two_stream", n=4096, M=16, dt=0.05, t_final=0.25, nu=0.05,
+                     estimator="blob", bandwidth="silverman", alpha=0.01, seed=4),
+        "vml": dict(preset="weibel", n=4096, M=16, dt=0.05, t_final=0.25, nu=0.0,
+                    estimator="none", seed=5),
+    }
+    log = []
+    recs = run(build_config(overrides=cfgs[tag]), str(tmp_path), stage_log=log)
+    ref = g[f"{tag}_diag"]
+    got = np.array([[r.step, r.t, r.E_K, r.E_E, r.E_B, r.E_total, r.H_dot, r.E_l2] for r in recs])
+    assert np.array_equal(got[:, 0], ref[:, 0])
+    np.testing.assert_allclose(got[:, [2, 5]], ref[:, [2, 5]], rtol=1e-5)
+    np.testing.assert_allclose(got[:, [3, 7]], ref[:, [3, 7]], rtol=2e-3, atol=1e-9)
+    if tag != "vml":
+        np.testing.assert_allclose(got[1:, 6], ref[1:, 6], rtol=2e-2)
+    stages = ["interpolate", "lorentz", "advance", "deposit", "field"]
+    if tag != "vml":
+        stages += ["score", "collide"]
+    assert log == stages * 5
+    cols = read_diagnostics_csv(str(tmp_path / "diagnostics.csv"))
+    assert list(cols) == ["step", "t", "E_K", "E_E", "E_B", "E_total", "H_dot", "P1", "P2", "P3", "E_l2"]
+    np.testing.assert_allclose(cols["E_total"], got[:, 5], rtol=1e-15)
+    (x0, v0, w0), fields0, meta = read_snapshot(str(tmp_path / "snapshot_000000.bin"))
+    np.testing.assert_allclose(x0, g[f"{tag}_x0"], rtol=0, atol=1e-6 * 10 * math.pi)
+    assert meta["step"] == 0 and meta["config"]["n"] == 4096
