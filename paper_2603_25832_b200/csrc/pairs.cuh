@@ -10,7 +10,7 @@ namespace spic {
 constexpr int kLandauNT = 128;  // threads per CTA
 constexpr int kLandauR = 2;     // targets per thread
 constexpr int kLandauTI = kLandauNT * kLandauR;
-constexpr int kLandauTJ = 128;  // records per stage
+constexpr int kLandauTJ = 256;  // records per stage
 constexpr int kLandauStages = 3;
 constexpr float kEps2 = 1e-24f;  // ref: kernels.py:7 EPS_Z^2, collision.py:100
 
