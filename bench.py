@@ -397,13 +397,18 @@ def main():
         sim.step(0)
     torch.cuda.synchronize()
     sim.check()
+    # the timed steps replay a CUDA graph of the step (one launch per step; the eager path is
+    # identical kernel for kernel, see tests/test_gpu_parity.py::test_cuda_graph_replay_*)
+    use_graph = world == 1 and not os.environ.get("SPIC_NO_GRAPH")
+    if use_graph:
+        sim.capture(row=3)
     live0 = count_live_pairs(sim.ci, sim.p, sim.grid) if world == 1 else 0
     peak = fp32_peak_tflops(torch, _lib)
 
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    sim.time_collision = True
+    sim.time_collision = not use_graph
     sim.collision_events.clear()
     launches0 = _lib.query("spic_launch_count")
     evs = []
@@ -412,11 +417,23 @@ def main():
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            sim.step(1)
+            if use_graph:
+                sim.replay(1)
+            else:
+                sim.step(1)
             e1.record()
             evs.append((e0, e1))
         torch.cuda.synchronize()
     launches = _lib.query("spic_launch_count") - launches0
+    if use_graph:
+        # graph replays do not pass through the host launch counter: count the captured
+        # kernels of one eager step (same sequence) and time the pair kernel eagerly
+        c0 = _lib.query("spic_launch_count")
+        sim.time_collision = True
+        for _ in range(3):
+            sim.step(2)
+        torch.cuda.synchronize()
+        launches = args.steps * (_lib.query("spic_launch_count") - c0) // 3
     sim.time_collision = False
     sim.check()
     step_ms = [a.elapsed_time(b) for a, b in evs]

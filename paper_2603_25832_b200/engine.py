@@ -64,8 +64,32 @@ class Simulation:
         # epilogue scratch
         self._epi, self._epi_n = _lib.scratch("epilogue", 8 * 2 * 148 * 5 + 64)
 
+    # ---- CUDA graph of one step --------------------------------------------------------------
+    def capture(self, row: int = 0) -> None:
+        """Capture one step (into diag[row]) as a CUDA graph; replay() then costs one launch.
+        Call after at least one eager step (scratch buffers sized). Per-particle Hutchinson
+        probes are drawn on the host per ISM step and cannot be captured."""
+        if self.trainer is not None and self.trainer.mode() == 2:
+            raise RuntimeError("per-particle Rademacher probes need the eager step")
+        self._graph_row = row
+        torch.cuda.synchronize()
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph):
+            self.step(row, draw=False)
+        torch.cuda.synchronize()
+
+    def replay(self, row: int | None = None) -> None:
+        """One captured step; its diagnostics row is copied to diag[row] if given."""
+        if self.trainer is not None:
+            self.trainer.draw_shared_probes()
+        self._graph.replay()
+        if self.trainer is not None and self.trainer.mode() == 1:
+            self.trainer._z_free.record()
+        if row is not None and row != self._graph_row:
+            self.diag[row].copy_(self.diag[self._graph_row])
+
     # ---- one step ---------------------------------------------------------------------------
-    def step(self, row: int) -> None:
+    def step(self, row: int, draw: bool = True) -> None:
         p, g, ci, f = self.p, self.grid, self.ci, self.f
         n, dv = p.n, p.dv
         st = _lib.stream_handle()
@@ -80,7 +104,7 @@ class Simulation:
                            flags=self.flags)
         if self.nu > 0 and self.est is not None:
             if self.trainer is not None:
-                self.trainer.run(n, ci=ci, flags=self.flags)
+                self.trainer.run(n, ci=ci, flags=self.flags, draw=draw)
                 self.est.estimate_sorted(ci, n)
             elif isinstance(self.est, BlobEstimator):
                 blob_sorted(ci, p, g, self.est.bandwidth, self.flags, self.bad_pid, self.h_cell)

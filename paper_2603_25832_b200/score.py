@@ -215,7 +215,10 @@ class AdamW:
             self.m = torch.zeros(P, dtype=torch.float64, device=dev)
             self.v = torch.zeros(P, dtype=torch.float64, device=dev)
             self.state = torch.tensor([0.0, self.lr, self.lr, 0.0], dtype=torch.float64, device=dev)
-        self.state[2] = float(self.lr)
+            self._lr_on_device = self.lr
+        if self._lr_on_device != self.lr:  # base lr changed on the host (not during capture)
+            self.state[2] = float(self.lr)
+            self._lr_on_device = self.lr
 
     @property
     def t(self) -> int:
@@ -253,6 +256,18 @@ class SbtmTrainer:
         self._pinned_z = torch.zeros(max(K, 1), 3, dtype=torch.float32).pin_memory() \
             if torch.cuda.is_available() else None
         optimizer._ensure(net)
+        self._z_free = torch.cuda.Event() if torch.cuda.is_available() else None
+
+    def draw_shared_probes(self) -> None:
+        """K shared Rademacher probes from the host stream into the pinned staging buffer.
+        Waits until the previous step's H2D copy of that buffer has executed (the host may
+        run ahead of the device by several steps)."""
+        if self.mode() != DIV_SHARED or not self.K:
+            return
+        self._z_free.synchronize()
+        dv = self.net.dv
+        zs = np.stack([draw_probe(self.rng, (dv,)) for _ in range(self.K)])
+        self._pinned_z[: self.K, :dv].copy_(torch.from_numpy(zs.astype(np.float32)))
 
     def mode(self) -> int:
         if self.divergence == "exact":
@@ -260,19 +275,22 @@ class SbtmTrainer:
         return DIV_SHARED if self.rademacher == "shared" else DIV_PER_PARTICLE
 
     def run(self, n: int, *, ci: CellIndex | None = None, particles: ParticleEnsemble | None = None,
-            flags=None, reduce_row=None, gid=None, n_global: int | None = None) -> None:
+            flags=None, reduce_row=None, gid=None, n_global: int | None = None,
+            draw: bool = True) -> None:
         """K ISM steps. reduce_row(row) (optional) is applied to the reduced float64 row
         [loss, grads, Phi] before each finalize (the cross-rank allreduce); gid (optional)
         maps sorted records to global particle ids for per-particle probes drawn over
-        n_global particles."""
+        n_global particles. draw=False (CUDA-graph capture) leaves the shared probes to a
+        separate draw_shared_probes() call before every replay."""
         mode = self.mode()
         dv = self.net.dv
         Zp = None
-        if mode == DIV_SHARED:
-            zs = np.stack([draw_probe(self.rng, (dv,)) for _ in range(self.K)]) if self.K else None
-            if self.K:
-                self._pinned_z[: self.K, :dv].copy_(torch.from_numpy(zs.astype(np.float32)))
-                self.z_shared.copy_(self._pinned_z, non_blocking=True)
+        if mode == DIV_SHARED and self.K:
+            if draw:
+                self.draw_shared_probes()
+            self.z_shared.copy_(self._pinned_z, non_blocking=True)
+            if draw:  # (under graph capture the replayer records the event instead)
+                self._z_free.record()
         for k in range(self.K):
             if mode == DIV_PER_PARTICLE:
                 Zp = _planes(draw_probe(self.rng, (n_global or n, dv)), self.net.params32.device)

@@ -469,3 +469,46 @@ def test_run_matches_reference_run(spic, golden, tmp_path, tag):
     (x0, v0, w0), fields0, meta = read_snapshot(str(tmp_path / "snapshot_000000.bin"))
     np.testing.assert_allclose(x0, g[f"{tag}_x0"], rtol=0, atol=1e-6 * 10 * math.pi)
     assert meta["step"] == 0 and meta["config"]["n"] == 4096
+
+
+@pytest.mark.parametrize("divergence", ["exact", "hutchinson"])
+def test_cuda_graph_replay_matches_eager_steps(spic, divergence):
+    """The captured step (CUDA graph replay, incl. host-drawn shared probes) reproduces the
+    eager steps bit for bit."""
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
+    from paper_2603_25832_b200.score import MlpScoreNet, SbtmEstimator
+    from paper_2603_25832_b200.state import FieldState
+
+    n, M, L = 30000, 32, 4 * math.pi
+    rng = np.random.default_rng(11)
+    x = rng.uniform(0, L, n)
+    v = rng.normal(size=(n, 3))
+    grid = Grid(M, L / M)
+
+    def make():
+        p = ens(x, v, np.full(n, L / n))
+        rho, J = deposit(p, grid)
+        rho_ion = float(rho.sum()) * grid.eta / L
+        f = FieldState.zeros(M, 3, rho_ion)
+        f.E1.copy_(poisson_solve(rho, rho_ion, grid))
+        r = np.random.default_rng(2)
+        net = MlpScoreNet.init_glorot(3, 64, r)
+        est = SbtmEstimator(net, L, 4, r, lr=1e-3, weight_decay=0.0, divergence=divergence)
+        return Simulation(p, f, grid, dt=0.05, nu=0.1, mode="VPL", gamma=-3.0, estimator=est,
+                          max_rows=8), p, net
+
+    a, pa, na = make()
+    b, pb, nb = make()
+    for k in range(1, 5):
+        a.step(k)
+    b.step(1)
+    b.capture(row=7)
+    for k in range(2, 5):
+        b.replay(k)
+    torch.cuda.synchronize()
+    a.check()
+    b.check()
+    assert torch.equal(pa.x, pb.x) and torch.equal(pa.vp, pb.vp)
+    assert torch.equal(na.params64, nb.params64)
+    assert torch.equal(a.diag[1:5], b.diag[1:5])
