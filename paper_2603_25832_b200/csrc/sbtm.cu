@@ -400,15 +400,17 @@ __global__ void __launch_bounds__(1024) k_sbtm_finalize(
   }
 }
 
-// Deterministic column sums of the [rows][width] block partials into one row (multi-CTA:
-// one thread per column, rows in order), so the single-CTA finalize reads one row.
+// Deterministic column sums of the [rows][width] block partials into one row, one warp per
+// column (lane-strided rows, fixed shuffle tree), so the single-CTA finalize reads one row.
 __global__ void k_ism_reduce_cols(const double* __restrict__ part, int rows, int64_t width,
                                   double* __restrict__ out) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= width) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t col = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (col >= width) return;
   double s = 0.0;
-  for (int r = 0; r < rows; ++r) s += part[(size_t)r * width + k];
-  out[k] = s;
+  for (int r = lane; r < rows; r += 32) s += part[(size_t)r * width + col];
+  s = warp_sum(s);
+  if (lane == 0) out[col] = s;
 }
 
 static int ism_blocks(int64_t n) {
@@ -486,7 +488,7 @@ extern "C" int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv
   SPIC_CHECK_LAUNCH();
   const int64_t width = 1 + n_params(H, dv) + H;
   double* part = (double*)scratch;
-  k_ism_reduce_cols<<<(unsigned)((width + 127) / 128), 128, 0, st>>>(
+  k_ism_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(
       part, blocks, width, part + (size_t)blocks * width); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
