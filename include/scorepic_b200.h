@@ -184,6 +184,14 @@ int spic_adamw_step(double* params64, const double* grads64, double* m, double* 
 int spic_push(float* x, float* v, int64_t ldv, int64_t n, int32_t dv, const double* E1,
               const double* E2, const double* B3, int32_t M, double eta, float dt,
               int32_t* flags, void* stream);
+/* Unfused forms of the push for the operator API: interpolate_fields (pic.py:61-74) ->
+ * E_p float[dv][lde] = (E1, E2, 0), B_p float[3][ldb] = (0, 0, B3); lorentz_push
+ * (pic.py:77-88): v += dt (E_p + v x B_p) with B = (0, 0, B3). */
+int spic_interpolate(const float* x, int64_t n, int32_t dv, const double* E1, const double* E2,
+                     const double* B3, int32_t M, double eta, float* Ep, int64_t lde, float* Bp,
+                     int64_t ldb, void* stream);
+int spic_lorentz(float* v, int64_t ldv, int64_t n, int32_t dv, const float* Ep, int64_t lde,
+                 const float* Bp, int64_t ldb, float dt, int32_t* flags, void* stream);
 size_t spic_deposit_scratch_bytes(int32_t M, int32_t dv);
 /* rho[M], J[dv][M] from sorted records; then (field_mode 1 = VPL: E1 -= dt J1;
  * 2 = VML maxwell_step; 0 = none). diag_out (nullable) receives [E_E, E_B, E_l2]. */

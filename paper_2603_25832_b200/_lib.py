@@ -71,6 +71,9 @@ SIGNATURES = {
     "spic_ism_row_offset": (_I64, [_I64, _I32, _I32]),
     "spic_adamw_step": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _D, _D, _D, _D, _P, _P]),
     "spic_push": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _P, _P, _P, _I32, _D, _F, _P, _P]),
+    "spic_interpolate": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _I32, _D, _P, _I64, _P, _I64,
+                                        _P]),
+    "spic_lorentz": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _I64, _P, _I64, _F, _P, _P]),
     "spic_deposit_scratch_bytes": (_SZ, [_I32, _I32]),
     "spic_deposit_field": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _I32, _D, _F, _P, _P, _I32, _D,
                                           _P, _P, _P, _P, _P, _P, _SZ, _P]),

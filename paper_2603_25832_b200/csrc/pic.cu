@@ -364,3 +364,74 @@ extern "C" int spic_moments(const float* v, int64_t ldv, const float* w, int64_t
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
+
+// ---- unfused operator forms (API parity with interpolate_fields / lorentz_push) ----------
+namespace spic {
+template <int DV>
+__global__ void k_interpolate(const float* __restrict__ x, int64_t n, const double* __restrict__ E1,
+                              const double* __restrict__ E2, const double* __restrict__ B3, int M,
+                              float ie, float* __restrict__ Ep, int64_t lde,
+                              float* __restrict__ Bp, int64_t ldb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float g = fmaf(x[i], ie, -0.5f);
+    const float fl = floorf(g);
+    const float f1 = g - fl, f0 = 1.f - f1;
+    int i0 = (int)fl;
+    i0 = i0 < 0 ? i0 + M : (i0 >= M ? i0 - M : i0);
+    const int i1 = i0 + 1 == M ? 0 : i0 + 1;
+    Ep[i] = f0 * (float)E1[i0] + f1 * (float)E1[i1];
+    Ep[lde + i] = f0 * (float)E2[i0] + f1 * (float)E2[i1];
+    if (DV == 3) Ep[2 * lde + i] = 0.f;
+    Bp[i] = 0.f;
+    Bp[ldb + i] = 0.f;
+    Bp[2 * ldb + i] = f0 * (float)B3[i0] + f1 * (float)B3[i1];
+  }
+}
+
+__global__ void k_lorentz(float* __restrict__ v, int64_t ldv, int64_t n, int dv,
+                          const float* __restrict__ Ep, int64_t lde, const float* __restrict__ Bp,
+                          int64_t ldb, float dt, int32_t* flags) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float b3 = Bp[2 * ldb + i];
+    const float v0 = v[i], v1 = v[ldv + i];
+    const float a0 = Ep[i] + v1 * b3, a1 = Ep[lde + i] - v0 * b3;
+    v[i] = fmaf(dt, a0, v0);
+    v[ldv + i] = fmaf(dt, a1, v1);
+    if (dv == 3) v[2 * ldv + i] = fmaf(dt, Ep[2 * lde + i], v[2 * ldv + i]);
+    bad |= !(isfinite(v[i]) && isfinite(v[ldv + i]));
+  }
+  if (bad) raise_flag(flags, SPIC_FLAG_NONFINITE_V);
+}
+}  // namespace spic
+
+extern "C" int spic_interpolate(const float* x, int64_t n, int32_t dv, const double* E1,
+                                const double* E2, const double* B3, int32_t M, double eta,
+                                float* Ep, int64_t lde, float* Bp, int64_t ldb, void* stream) {
+  if (n < 0 || M < 1 || (dv != 2 && dv != 3)) return SPIC_ERR_ARG;
+  if (n == 0) return SPIC_OK;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+  if (dv == 3)
+    k_interpolate<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, E1, E2, B3, M, (float)(1.0 / eta),
+                                                               Ep, lde, Bp, ldb);
+  else
+    k_interpolate<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, E1, E2, B3, M, (float)(1.0 / eta),
+                                                               Ep, lde, Bp, ldb);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
+
+extern "C" int spic_lorentz(float* v, int64_t ldv, int64_t n, int32_t dv, const float* Ep,
+                            int64_t lde, const float* Bp, int64_t ldb, float dt, int32_t* flags,
+                            void* stream) {
+  if (n < 0 || (dv != 2 && dv != 3)) return SPIC_ERR_ARG;
+  if (n == 0) return SPIC_OK;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+  k_lorentz<<<blocks, 256, 0, (cudaStream_t)stream>>>(v, ldv, n, dv, Ep, lde, Bp, ldb, dt, flags);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}

@@ -73,6 +73,30 @@ def push_particles(particles: ParticleEnsemble, fields: FieldState, grid: Grid, 
             raise ValueError("non-finite position")
 
 
+def interpolate_fields(particles: ParticleEnsemble, fields: FieldState, grid: Grid):
+    """E_p (n, dv) = (E1, E2, 0...), B_p (n, 3) = (0, 0, B3) at the particles
+    (ref: pic.py:61-74); the hot loop fuses this into push_particles."""
+    n, dv = particles.n, particles.dv
+    dev = particles.x.device
+    Ep = torch.empty(dv, n, dtype=torch.float32, device=dev)
+    Bp = torch.empty(3, n, dtype=torch.float32, device=dev)
+    _lib.call("spic_interpolate", _lib.ptr(particles.x), n, dv, _lib.ptr(fields.E1),
+              _lib.ptr(fields.E2), _lib.ptr(fields.B3), grid.M, float(grid.eta), _lib.ptr(Ep), n,
+              _lib.ptr(Bp), n, _lib.stream_handle())
+    return Ep.t(), Bp.t()
+
+
+def lorentz_push(particles: ParticleEnsemble, E_p, B_p, dt: float) -> None:
+    """v <- v + dt (E + v x B), B = (0, 0, B3) (ref: pic.py:77-88), in place."""
+    n, dv = particles.n, particles.dv
+    dev = particles.x.device
+    Ep = torch.as_tensor(E_p, dtype=torch.float32, device=dev).t().contiguous()
+    Bp = torch.as_tensor(B_p, dtype=torch.float32, device=dev).t().contiguous()
+    flags = new_flags(dev)
+    _lib.call("spic_lorentz", _lib.ptr(particles.vp), n, n, dv, _lib.ptr(Ep), n, _lib.ptr(Bp), n,
+              float(dt), _lib.ptr(flags), _lib.stream_handle())
+
+
 def advance_positions(particles: ParticleEnsemble, dt: float, L: float) -> None:
     """x <- (x + dt v1) mod L (ref: pic.py:91-93): the fused push with zero fields."""
     M = 1

@@ -77,3 +77,8 @@ def anisotropic_ensemble(n: int, L: float, temps, rng: np.random.Generator, *, d
     for i in range(dv):
         v[:, i] = np.sqrt(temps[i]) * rng.normal(size=n)
     return x, v, np.full(n, L / n)
+
+
+def seeded_b3_noise(M: int, amplitude: float, rng: np.random.Generator) -> np.ndarray:
+    """Extension (BASELINE config 3): B3 at the cell centres = amplitude x N(0, 1) noise."""
+    return amplitude * rng.normal(size=M)

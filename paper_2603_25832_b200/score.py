@@ -505,3 +505,40 @@ class SbtmEstimator:
             self.warnings.append(f"pretraining budget exhausted: mse {res.final_mse:.3e} "
                                  f"above tol {res.tol:.3e} after {res.steps} steps")
         return res
+
+
+# ------------------------------------------------------------------------------------------
+# SBTM checkpoint (flat little-endian binary, ref: score.py:631-657)
+# ------------------------------------------------------------------------------------------
+CHECKPOINT_MAGIC = b"SBTM"
+CHECKPOINT_VERSION = 1
+
+
+def save_checkpoint(net: MlpScoreNet, path: str) -> None:
+    """magic "SBTM", u32 version, u32 H, u32 dv, then W1, b1, W2, b2 as <f8 (row-major)."""
+    import struct
+
+    body = net.params64.cpu().numpy().astype("<f8").tobytes()
+    with open(path, "wb") as fh:
+        fh.write(CHECKPOINT_MAGIC + struct.pack("<III", CHECKPOINT_VERSION, net.hidden, net.dv) + body)
+
+
+def load_checkpoint(path: str, device=None) -> MlpScoreNet:
+    import struct
+
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    if raw[:4] != CHECKPOINT_MAGIC:
+        raise ValueError(f"bad checkpoint magic: {raw[:4]!r}")
+    version, hidden, dv = struct.unpack_from("<III", raw, 4)
+    if version != CHECKPOINT_VERSION:
+        raise ValueError(f"unsupported checkpoint version: {version}")
+    net = MlpScoreNet(dv, hidden, device)
+    P = net.n_params
+    if len(raw) < 16 + 8 * P:
+        raise ValueError("truncated checkpoint")
+    if len(raw) > 16 + 8 * P:
+        raise ValueError("trailing bytes in checkpoint")
+    net.params64.copy_(torch.from_numpy(np.frombuffer(raw, dtype="<f8", offset=16).copy()))
+    net.refresh32()
+    return net

@@ -512,3 +512,54 @@ def test_cuda_graph_replay_matches_eager_steps(spic, divergence):
     assert torch.equal(pa.x, pb.x) and torch.equal(pa.vp, pb.vp)
     assert torch.equal(na.params64, nb.params64)
     assert torch.equal(a.diag[1:5], b.diag[1:5])
+
+
+def test_unfused_push_operators_and_checkpoint(spic, golden, tmp_path):
+    """interpolate_fields -> lorentz_push -> advance_positions (the unfused operator API)
+    equals the reference; SBTM checkpoints round-trip bit-exactly in the reference layout."""
+    import struct
+
+    from paper_2603_25832_b200.pic import Grid, advance_positions, interpolate_fields, lorentz_push
+    from paper_2603_25832_b200.score import MlpScoreNet, load_checkpoint, save_checkpoint
+    from paper_2603_25832_b200.state import FieldState
+
+    g = golden("pic.npz")
+    for k in range(int(g["ncases"])):
+        p = f"c{k}_"
+        x, v, w = g[p + "x"], g[p + "v"], g[p + "w"]
+        M, eta, dt = int(g[p + "M"]), float(g[p + "eta"]), float(g[p + "dt"])
+        grid = Grid(M, eta)
+        parts = ens(x, v, w)
+        fields = FieldState.from_arrays(g[p + "E1"], g[p + "E2"], g[p + "B3"], dv=v.shape[1])
+        Ep, Bp = interpolate_fields(parts, fields, grid)
+        lorentz_push(parts, Ep, Bp, dt)
+        advance_positions(parts, dt, grid.L)
+        x1 = parts.x.double().cpu().numpy()
+        dxx = np.abs(x1 - g[p + "x1"])
+        assert np.max(np.minimum(dxx, grid.L - dxx)) <= 1e-5 * grid.L
+        check_field(parts.v.double().cpu().numpy(), g[p + "v1"], tol=1e-6)
+    net = MlpScoreNet.init_glorot(3, 16, np.random.default_rng(4))
+    path = str(tmp_path / "net.sbtm")
+    save_checkpoint(net, path)
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"SBTM" and struct.unpack_from("<III", raw, 4) == (1, 16, 3)
+    assert len(raw) == 16 + 8 * net.n_params
+    back = load_checkpoint(path)
+    assert torch.equal(back.params64, net.params64)
+    with pytest.raises(ValueError, match="magic"):
+        open(path, "wb").write(b"XXXX" + raw[4:])
+        load_checkpoint(path)
+
+
+def test_score_test_mode(spic, tmp_path):
+    from paper_2603_25832_b200.config import build_config
+    from paper_2603_25832_b200.run import score_test
+
+    cfg = build_config(overrides=dict(preset="landau_damping", n=4000, M=8, hidden=32,
+                                      pretrain_budget=300, pretrain_batch=1000, seed=1))
+    rep = score_test(cfg, str(tmp_path))
+    assert set(rep) == {"blob", "sbtm"}
+    for name in rep:
+        assert np.isfinite(rep[name]["mse"]) and rep[name]["mse"] < 3.0
+        hdr = open(rep[name]["csv"]).readline().strip().split(",")
+        assert hdr[:4] == ["x", "v1", "v2", "v3"] and hdr[-1] == "U3"
