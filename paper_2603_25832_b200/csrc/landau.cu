@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "pairs.cuh"
+#include "f32x2.cuh"
 
 namespace spic {
 
@@ -171,55 +172,6 @@ __global__ void __launch_bounds__(kLandauNT, 4)
 // 64-bit registers so every arithmetic step is one FFMA2/FADD2/FMUL2 for two pairs; the
 // broadcast j-record enters as a scalar operand. |dx| is taken with FMNMX (ALU pipe) and
 // the eps2 test with FSETP+FSEL, keeping the FMA pipe for the 21 packed ops per two pairs.
-struct f2 {
-  unsigned long long r;
-};
-__device__ __forceinline__ f2 mk2(float a, float b) {
-  f2 o;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(o.r) : "f"(a), "f"(b));
-  return o;
-}
-__device__ __forceinline__ void un2(f2 a, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.r));
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) {
-  f2 o;
-  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
-  return o;
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-  f2 o;
-  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
-  return o;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  f2 o;
-  asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
-  return o;
-}
-// sign-bit ops on both halves: integer LOP3 on the ALU pipe (ptxas would otherwise turn
-// fabs / negation into FADDs on the FMA pipe)
-__device__ __forceinline__ f2 abs2(f2 a) {
-  f2 o;
-  asm("and.b64 %0, %1, 0x7fffffff7fffffff;" : "=l"(o.r) : "l"(a.r));
-  return o;
-}
-__device__ __forceinline__ f2 neg2(f2 a) {
-  f2 o;
-  asm("xor.b64 %0, %1, 0x8000000080000000;" : "=l"(o.r) : "l"(a.r));
-  return o;
-}
-__device__ __forceinline__ f2 rint2(f2 a) {
-  float lo, hi;
-  un2(a, lo, hi);
-  return mk2(rintf(lo), rintf(hi));
-}
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  f2 o;
-  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r));
-  return o;
-}
-
 template <int RP, int MINB, bool UNIFORM_W, bool MINIMG>
 __global__ void __launch_bounds__(kLandauNT, MINB)
     k_landau_x2(const float4* __restrict__ xv, const float4* __restrict__ sw,
@@ -568,7 +520,7 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   const char* var = getenv("SPIC_LANDAU_VARIANT");
   const bool packed = dv == 3 && gm == 0 && !(var && var[0] == 's');
   // experiment knob: SPIC_LANDAU_VARIANT = s (scalar) | 1 (RP1) | 3 (RP3) | 4 (RP2, 4 CTA/SM)
-  const int cfg = (var && var[0] >= '1' && var[0] <= '4') ? var[0] - '0' : 2;
+  const int cfg = (var && var[0] >= '1' && var[0] <= '5') ? var[0] - '0' : 2;
   const int rp = cfg == 1 ? 1 : (cfg == 3 ? 3 : 2);
   const int TI = packed ? kLandauNT * 2 * rp : kLandauTI;
   k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start, c_lo, c_hi); spic::count_launch();
@@ -601,6 +553,7 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
       case 1: SPIC_X2(1, 6); break;
       case 3: SPIC_X2(3, 2); break;
       case 4: SPIC_X2(2, 3); break;
+      case 5: SPIC_X2(2, 5); break;
       default: SPIC_X2(2, 4); break;
     }
 #undef SPIC_X2

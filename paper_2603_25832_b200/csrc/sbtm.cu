@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "f32x2.cuh"
 
 namespace spic {
 
@@ -298,6 +299,258 @@ __global__ void __launch_bounds__(kIsmNT) k_ism_partials(
 }
 
 // ------------------------------------------------------------------------------------------
+// Packed-FP32 ISM / MSE partials: two particles per f32x2 lane pair. Same math, same partial
+// layout as k_ism_partials; chunks of 2*NT particles, thread t of phase 1 owns particles
+// (t, t+NT), phase 2 item (h, g) sweeps the staged particle pairs k = g, g+G, ...
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ f2 bc2(float a) { return mk2(a, a); }
+
+__device__ __forceinline__ f2 rcp2(f2 a) {
+  float lo, hi;
+  un2(a, lo, hi);
+  return mk2(fast_rcp(lo), fast_rcp(hi));
+}
+
+template <int MODE>
+__device__ __forceinline__ void ism_load_particle(
+    int64_t p, int64_t n, const float4* __restrict__ xv, const float4* __restrict__ sw,
+    const float* __restrict__ x, const float* __restrict__ v, int64_t ldv,
+    const float* __restrict__ w, float x_scale, float L, const float* __restrict__ Z, int64_t ldz,
+    const int32_t* __restrict__ idx, int dv, float (&u)[4], float& wp, float (&q)[3]) {
+  u[0] = u[1] = u[2] = u[3] = 0.f;
+  q[0] = q[1] = q[2] = 0.f;
+  wp = 0.f;
+  if (p >= n) return;
+  const int64_t r = idx ? (int64_t)idx[p] : p;
+  if (xv) {
+    const float4 A = xv[p];
+    u[0] = A.x < 0.f ? A.x + L : A.x;
+    u[1] = A.y; u[2] = A.z; u[3] = A.w;
+    wp = sw[p].w;
+  } else {
+    u[0] = x[r];
+    u[1] = v[r];
+    u[2] = v[ldv + r];
+    u[3] = dv > 2 ? v[2 * ldv + r] : 0.f;
+    wp = w[r];
+  }
+  u[0] *= x_scale;
+  if (MODE >= 2) {
+    q[0] = Z[r];
+    q[1] = Z[ldz + r];
+    q[2] = dv > 2 ? Z[2 * ldz + r] : 0.f;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kIsmNT) k_ism_partials_x2(
+    const float* __restrict__ params, int H, int dv, const float4* __restrict__ xv,
+    const float4* __restrict__ sw, const float* __restrict__ x, const float* __restrict__ v,
+    int64_t ldv, const float* __restrict__ w, int64_t n, float x_scale, float L,
+    const float* __restrict__ Z, int64_t ldz, const int32_t* __restrict__ idx, float inv_wsum,
+    double* __restrict__ partials) {
+  constexpr int CP = 2 * kIsmNT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4* Wp = (float4*)smem_raw;        // [H]
+  float4* Bp = Wp + H;                   // [H]
+  float4* U2 = Bp + H;                   // [NT][2]: (x_a, x_b, v0_a, v0_b), (v1_a, v1_b, v2_a, v2_b)
+  float4* G2 = U2 + 2 * kIsmNT;          // [NT][2]: (g0_a, g0_b, g1_a, g1_b), (g2_a, g2_b, w_a, w_b)
+  float4* Z2 = G2 + 2 * kIsmNT;          // [NT][2]: probes (MODE 2)
+  float* coef = (float*)(Z2 + 2 * kIsmNT);
+  double* acc64 = (double*)(((uintptr_t)(coef + H) + 15) & ~(uintptr_t)15);  // [items][10]
+  __shared__ float b2[3];
+  __shared__ double red[8 * 4];
+
+  load_packed(params, H, dv, Wp, Bp, b2);
+  __syncthreads();
+  if (MODE == 0 || MODE == 1) {
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+      const float4 a = Wp[h], b = Bp[h];
+      if (MODE == 0) {
+        coef[h] = b.y * a.y + b.z * a.z + b.w * a.w;
+      } else {
+        const float z0 = Z[0], z1 = Z[1], z2 = dv > 2 ? Z[2] : 0.f;
+        coef[h] = (b.y * z0 + b.z * z1 + b.w * z2) * (a.y * z0 + a.z * z1 + a.w * z2);
+      }
+    }
+  }
+  const int G = max(1, kIsmNT / H);
+  const int items = H * G;
+  for (int it = threadIdx.x; it < items; it += blockDim.x)
+    for (int k = 0; k < kIsmAcc; ++k) acc64[it * kIsmAcc + k] = 0.0;
+  double lacc[4] = {0.0, 0.0, 0.0, 0.0};
+  __syncthreads();
+  const f2 one2 = bc2(1.f);
+
+  const int64_t nchunks = (n + CP - 1) / CP;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    // ---- phase 1: particles (t, t+NT) as one packed pair ------------------------------
+    float ua[4], ub[4], qa[3], qb[3], wa, wb;
+    const int64_t pa = ch * CP + threadIdx.x, pb = pa + kIsmNT;
+    ism_load_particle<MODE>(pa, n, xv, sw, x, v, ldv, w, x_scale, L, Z, ldz, idx, dv, ua, wa, qa);
+    ism_load_particle<MODE>(pb, n, xv, sw, x, v, ldv, w, x_scale, L, Z, ldz, idx, dv, ub, wb, qb);
+    if (MODE == 3) {
+      wa *= inv_wsum;
+      wb *= inv_wsum;
+    }
+    // stage the inputs first so the scalar copies die before the h loop (keeps the packed
+    // pairs resident in register pairs instead of being rebuilt every iteration)
+    U2[2 * threadIdx.x] = make_float4(ua[0], ub[0], ua[1], ub[1]);
+    U2[2 * threadIdx.x + 1] = make_float4(ua[2], ub[2], ua[3], ub[3]);
+    if (MODE == 2) {
+      Z2[2 * threadIdx.x] = make_float4(qa[0], qb[0], qa[1], qb[1]);
+      Z2[2 * threadIdx.x + 1] = make_float4(qa[2], qb[2], 0.f, 0.f);
+    }
+    const f2 X = mk2(ua[0], ub[0]), V0 = mk2(ua[1], ub[1]), V1 = mk2(ua[2], ub[2]),
+             V2 = mk2(ua[3], ub[3]);
+    const f2 Q0 = mk2(qa[0], qb[0]), Q1 = mk2(qa[1], qb[1]), Q2 = mk2(qa[2], qb[2]);
+    f2 S0 = bc2(b2[0]), S1 = bc2(b2[1]), S2 = bc2(b2[2]), DIV = bc2(0.f);
+#pragma unroll 4
+    for (int h = 0; h < H; ++h) {
+      const float4 a = Wp[h];
+      const float4 b = Bp[h];
+      const f2 z = fma2(V2, bc2(a.w), fma2(V1, bc2(a.z), fma2(V0, bc2(a.y), fma2(X, bc2(a.x), bc2(b.x)))));
+      const f2 inv = rcp2(add2(abs2(z), one2));
+      const f2 act = mul2(z, inv);
+      S0 = fma2(act, bc2(b.y), S0);
+      S1 = fma2(act, bc2(b.z), S1);
+      S2 = fma2(act, bc2(b.w), S2);
+      const f2 sp = mul2(inv, inv);
+      if (MODE == 0 || MODE == 1) {
+        DIV = fma2(sp, bc2(coef[h]), DIV);
+      } else if (MODE == 2) {
+        const f2 t = fma2(Q2, bc2(a.w), fma2(Q1, bc2(a.z), mul2(Q0, bc2(a.y))));
+        const f2 r = fma2(Q2, bc2(b.w), fma2(Q1, bc2(b.z), mul2(Q0, bc2(b.y))));
+        DIV = fma2(mul2(r, t), sp, DIV);
+      }
+    }
+    float s[2][3], dvv[2];
+    un2(S0, s[0][0], s[1][0]);
+    un2(S1, s[0][1], s[1][1]);
+    un2(S2, s[0][2], s[1][2]);
+    un2(DIV, dvv[0], dvv[1]);
+    float g[2][3];
+    const float wv[2] = {wa, wb};
+    float qq[2][3];
+    un2(Q0, qq[0][0], qq[1][0]);
+    un2(Q1, qq[0][1], qq[1][1]);
+    un2(Q2, qq[0][2], qq[1][2]);
+    const bool val[2] = {pa < n, pb < n};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      float lp;
+      if (MODE == 3) {
+        const float e0 = s[e][0] - qq[e][0], e1 = s[e][1] - qq[e][1], e2 = s[e][2] - qq[e][2];
+        lp = wv[e] * (e0 * e0 + e1 * e1 + e2 * e2);
+        g[e][0] = 2.f * wv[e] * e0; g[e][1] = 2.f * wv[e] * e1; g[e][2] = 2.f * wv[e] * e2;
+      } else {
+        lp = wv[e] * (s[e][0] * s[e][0] + s[e][1] * s[e][1] + s[e][2] * s[e][2] + 2.f * dvv[e]);
+        g[e][0] = 2.f * wv[e] * s[e][0]; g[e][1] = 2.f * wv[e] * s[e][1];
+        g[e][2] = 2.f * wv[e] * s[e][2];
+      }
+      if (dv < 3) g[e][2] = 0.f;
+      if (val[e]) {
+        lacc[0] += (double)lp;
+        lacc[1] += (double)g[e][0];
+        lacc[2] += (double)g[e][1];
+        lacc[3] += (double)g[e][2];
+      } else {
+        g[e][0] = g[e][1] = g[e][2] = 0.f;
+      }
+    }
+    G2[2 * threadIdx.x] = make_float4(g[0][0], g[1][0], g[0][1], g[1][1]);
+    G2[2 * threadIdx.x + 1] = make_float4(g[0][2], g[1][2], val[0] ? wa : 0.f, val[1] ? wb : 0.f);
+    __syncthreads();
+    // ---- phase 2: one (hidden unit, pair group) per thread, packed outer products ------
+    const int64_t rem = n - ch * CP;
+    const int npairs = (int)(rem < (int64_t)kIsmNT ? rem : (int64_t)kIsmNT);
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int h = it % H, gq = it / H;
+      const float4 a = Wp[h], b = Bp[h];
+      const float cc4 = (MODE == 0 || MODE == 1) ? 4.f * coef[h] : 0.f;
+      f2 gw0 = bc2(0.f), gw1 = gw0, gw2 = gw0, gw3 = gw0, gb = gw0;
+      f2 gv0 = gw0, gv1 = gw0, gv2 = gw0, phi = gw0;
+#pragma unroll 2
+      for (int k = gq; k < npairs; k += G) {
+        const float4 A0 = U2[2 * k], A1 = U2[2 * k + 1];
+        const float4 B0 = G2[2 * k], B1 = G2[2 * k + 1];
+        const f2 X = mk2(A0.x, A0.y), V0 = mk2(A0.z, A0.w), V1 = mk2(A1.x, A1.y), V2 = mk2(A1.z, A1.w);
+        const f2 g0 = mk2(B0.x, B0.y), g1 = mk2(B0.z, B0.w), g2 = mk2(B1.x, B1.y), W = mk2(B1.z, B1.w);
+        const f2 z = fma2(V2, bc2(a.w), fma2(V1, bc2(a.z), fma2(V0, bc2(a.y), fma2(X, bc2(a.x), bc2(b.x)))));
+        const f2 inv = rcp2(add2(abs2(z), one2));
+        const f2 act = mul2(z, inv);
+        const f2 sp = mul2(inv, inv);
+        f2 d = mul2(fma2(g2, bc2(b.w), fma2(g1, bc2(b.z), mul2(g0, bc2(b.y)))), sp);
+        if (MODE != 3) {
+          // spp = -2 sign(z) sp inv (0 at z == 0); the factor -2 sign(z) is folded into
+          // the sign bit (LOP3) and the weight (4 w c_h), keeping the FMA pipe for the math
+          float ze, zo, me, mo;
+          un2(z, ze, zo);
+          un2(mul2(sp, inv), me, mo);
+          const f2 spp = mk2(ze == 0.f ? 0.f : copysignf(me, -ze), zo == 0.f ? 0.f : copysignf(mo, -zo));
+          f2 cw;  // 4 w c_h per particle
+          if (MODE == 2) {
+            const float4 Z0 = Z2[2 * k], Z1 = Z2[2 * k + 1];
+            const f2 q0 = mk2(Z0.x, Z0.y), q1 = mk2(Z0.z, Z0.w), q2 = mk2(Z1.x, Z1.y);
+            const f2 t = fma2(q2, bc2(a.w), fma2(q1, bc2(a.z), mul2(q0, bc2(a.y))));
+            const f2 r = fma2(q2, bc2(b.w), fma2(q1, bc2(b.z), mul2(q0, bc2(b.y))));
+            const f2 W2x = add2(W, W);
+            const f2 k2 = mul2(W2x, sp);
+            const f2 k2t = mul2(k2, t), k2r = mul2(k2, r);
+            gv0 = fma2(k2t, q0, gv0);
+            gv1 = fma2(k2t, q1, gv1);
+            gv2 = fma2(k2t, q2, gv2);
+            gw1 = fma2(k2r, q0, gw1);
+            gw2 = fma2(k2r, q1, gw2);
+            gw3 = fma2(k2r, q2, gw3);
+            cw = mul2(add2(W2x, W2x), mul2(r, t));
+          } else {
+            cw = mul2(W, bc2(cc4));
+            phi = fma2(W, sp, phi);
+          }
+          d = fma2(cw, spp, d);
+        }
+        gb = add2(gb, d);
+        gw0 = fma2(d, X, gw0);
+        gw1 = fma2(d, V0, gw1);
+        gw2 = fma2(d, V1, gw2);
+        gw3 = fma2(d, V2, gw3);
+        gv0 = fma2(g0, act, gv0);
+        gv1 = fma2(g1, act, gv1);
+        gv2 = fma2(g2, act, gv2);
+      }
+      double* A = acc64 + it * kIsmAcc;
+      const f2 accs[9] = {gw0, gw1, gw2, gw3, gb, gv0, gv1, gv2, phi};
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        float lo, hi;
+        un2(accs[k], lo, hi);
+        A[k] += (double)lo + (double)hi;
+      }
+    }
+    __syncthreads();
+  }
+  block_sum<4>(lacc, red);
+  const int64_t P = n_params(H, dv);
+  const int64_t width = 1 + P + H;
+  double* out = partials + (size_t)blockIdx.x * width;
+  if (threadIdx.x == 0) {
+    out[0] = lacc[0];
+    for (int i = 0; i < dv; ++i) out[1 + P - dv + i] = lacc[1 + i];
+  }
+  const int64_t oW1 = 1, ob1 = oW1 + (int64_t)H * (1 + dv), oW2 = ob1 + H, oPhi = 1 + P;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    double sacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int gq = 0; gq < G; ++gq)
+      for (int k = 0; k < 9; ++k) sacc[k] += acc64[(gq * H + h) * kIsmAcc + k];
+    for (int k = 0; k < 1 + dv; ++k) out[oW1 + h * (1 + dv) + k] = sacc[k];
+    out[ob1 + h] = sacc[4];
+    for (int i = 0; i < dv; ++i) out[oW2 + i * H + h] = sacc[5 + i];
+    out[oPhi + h] = sacc[8];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // finalize: ordered reduction of block partials, divergence terms, AdamW with recovery
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_sbtm_finalize(
@@ -414,13 +667,13 @@ __global__ void k_ism_reduce_cols(const double* __restrict__ part, int rows, int
 }
 
 static int ism_blocks(int64_t n) {
-  int64_t chunks = (n + kIsmNT - 1) / kIsmNT;
+  int64_t chunks = (n + 2 * kIsmNT - 1) / (2 * kIsmNT);  // packed kernel: 2*NT per chunk
   return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, kIsmBlocksMax));
 }
 
 static size_t ism_smem(int H) {
   int G = std::max(1, kIsmNT / H);
-  size_t b = sizeof(float4) * (2 * (size_t)H + 3 * kIsmNT) + sizeof(float) * H + 16;
+  size_t b = sizeof(float4) * (2 * (size_t)H + 6 * kIsmNT) + sizeof(float) * H + 16;
   b += sizeof(double) * (size_t)H * G * kIsmAcc;
   return b;
 }
@@ -471,9 +724,9 @@ extern "C" int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv
 #define SPIC_ISM_LAUNCH(MD)                                                                    \
   do {                                                                                         \
     if (smem > 48 * 1024)                                                                      \
-      cudaFuncSetAttribute(k_ism_partials<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+      cudaFuncSetAttribute(k_ism_partials_x2<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                         \
-    k_ism_partials<MD><<<blocks, kIsmNT, smem, st>>>(params32, H, dv, (const float4*)xv,       \
+    k_ism_partials_x2<MD><<<blocks, kIsmNT, smem, st>>>(params32, H, dv, (const float4*)xv,    \
                                                      (const float4*)sw, x, v, ldv, w, n,       \
                                                      x_scale, L, Z, ldz, idx, (float)inv_wsum, \
                                                      (double*)scratch); spic::count_launch();                        \
