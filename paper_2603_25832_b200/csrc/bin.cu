@@ -37,9 +37,11 @@ static BinPlan bin_plan(int64_t n, int M, int S) {
   p.K = M * S;
   int W = 32768 / p.K;
   p.W = W < 1 ? 1 : (W > 8 ? 8 : W);
-  long long per = (long long)p.W * 32 * 512;
+  // about one tile per SM: the (key, tile) count table then stays ~K x 148 entries (small
+  // next to n) and the scatter kernel runs one wave
+  long long per = (long long)p.W * 32 * kNumSMs;
   long long G = (n + per - 1) / per;
-  p.G = (int)(G < 4 ? 4 : (G > 256 ? 256 : G));
+  p.G = (int)(G < 4 ? 4 : (G > 8192 ? 8192 : G));
   p.T = p.W * 32 * p.G;
   p.n_tiles = (int)((n + p.T - 1) / p.T);
   if (p.n_tiles < 1) p.n_tiles = 1;
