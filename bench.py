@@ -355,11 +355,13 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        reps, warm = max(1, args.steps), max(0, args.warmup)
-        # bounded: each CPU step is a sampled step (a few seconds on 16 cores)
-        line = cpu_baseline_line(wl, args.seed, reps=reps, warm=min(warm, 1))
+        # bounded: each CPU step is a sampled step (a few seconds on 16 host cores); at most 3
+        # timed sample steps and 1 warm-up so any --steps/--warmup finishes in minutes
+        reps, warm = min(max(1, args.steps), 3), min(max(0, args.warmup), 1)
+        line = cpu_baseline_line(wl, args.seed, reps=reps, warm=warm)
         out = {"metric": METRIC, "value": line["value"], "unit": "particle-steps/s",
                "impl": "reference", "n_gpus": args.gpus, "steps": reps, "warmup": warm,
+               "requested_steps": args.steps, "requested_warmup": args.warmup,
                "ms_per_step": 1e3 * line["seconds_per_step"], "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": {"workload": wl["workload"], "n": wl["n"], "M": wl["M"], "K": wl["K"],
