@@ -17,9 +17,11 @@ from .state import ParticleEnsemble, new_flags
 
 
 def auto_sub_cells(n: int, M: int) -> int:
-    """Sub-cell sort depth: keep M*S <= 16384 and >= ~64 particles per sub-cell."""
+    """Sub-cell sort depth S (power of two <= 64): keys M*S <= 32768 (the binning kernel's
+    shared-memory histogram) and >= ~64 particles per sub-cell. Finer sub-cells let the pair
+    kernels skip more of the stencil beyond eta of a target tile."""
     S = 1
-    while S < 64 and M * S * 2 <= 16384 and n // (M * S * 2) >= 64:
+    while S < 64 and M * S * 2 <= 32768 and n // (M * S * 2) >= 64:
         S *= 2
     return S
 

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kLandauNT, 4)
 // 64-bit registers so every arithmetic step is one FFMA2/FADD2/FMUL2 for two pairs; the
 // broadcast j-record enters as a scalar operand. |dx| is taken with FMNMX (ALU pipe) and
 // the eps2 test with FSETP+FSEL, keeping the FMA pipe for the 21 packed ops per two pairs.
-template <int RP, int MINB, bool UNIFORM_W, bool MINIMG>
+template <int RP, int MINB, bool UNIFORM_W, bool MINIMG, int UNR = 2>
 __global__ void __launch_bounds__(kLandauNT, MINB)
     k_landau_x2(const float4* __restrict__ xv, const float4* __restrict__ sw,
                 const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kLandauNT, MINB)
       mbar_wait(&s_bar[st], (uint32_t)(((qg + q) / kLandauStages) & 1));
       const float4* __restrict__ P = s_xv[st];
       const float4* __restrict__ Q = s_sw[st];
-#pragma unroll 2
+#pragma unroll UNR
       for (int jj = 0; jj < d.cnt; ++jj) {
         const float4 A = P[jj];
         const float4 B = Q[jj];
@@ -520,31 +520,32 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   const char* var = getenv("SPIC_LANDAU_VARIANT");
   const bool packed = dv == 3 && gm == 0 && !(var && var[0] == 's');
   // experiment knob: SPIC_LANDAU_VARIANT = s (scalar) | 1 (RP1) | 3 (RP3) | 4 (RP2, 4 CTA/SM)
-  const int cfg = (var && var[0] >= '1' && var[0] <= '5') ? var[0] - '0' : 2;
+  const int cfg = (var && var[0] >= '1' && var[0] <= '7') ? var[0] - '0' : 2;
   const int rp = cfg == 1 ? 1 : (cfg == 3 ? 3 : 2);
   const int TI = packed ? kLandauNT * 2 * rp : kLandauTI;
   k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start, c_lo, c_hi); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   dim3 grid((unsigned)(n / TI + M + 1), (unsigned)nsplit);
   if (packed) {
-#define SPIC_X2(RP_, MB_)                                                                    \
+#define SPIC_X2(RP_, MB_) SPIC_X2U(RP_, MB_, 2)
+#define SPIC_X2U(RP_, MB_, U_)                                                               \
   do {                                                                                        \
     if (minimg) {                                                                             \
       if (uw)                                                                                 \
-        k_landau_x2<RP_, MB_, true, true><<<grid, kLandauNT, 0, st>>>(                        \
+        k_landau_x2<RP_, MB_, true, true, U_><<<grid, kLandauNT, 0, st>>>(                    \
             (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
             (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
       else                                                                                    \
-        k_landau_x2<RP_, MB_, false, true><<<grid, kLandauNT, 0, st>>>(                       \
+        k_landau_x2<RP_, MB_, false, true, U_><<<grid, kLandauNT, 0, st>>>(                   \
             (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
             (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
     } else {                                                                                  \
       if (uw)                                                                                 \
-        k_landau_x2<RP_, MB_, true, false><<<grid, kLandauNT, 0, st>>>(                       \
+        k_landau_x2<RP_, MB_, true, false, U_><<<grid, kLandauNT, 0, st>>>(                   \
             (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
             (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
       else                                                                                    \
-        k_landau_x2<RP_, MB_, false, false><<<grid, kLandauNT, 0, st>>>(                      \
+        k_landau_x2<RP_, MB_, false, false, U_><<<grid, kLandauNT, 0, st>>>(                  \
             (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
             (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
     }                                                                                         \
@@ -554,9 +555,12 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
       case 3: SPIC_X2(3, 2); break;
       case 4: SPIC_X2(2, 3); break;
       case 5: SPIC_X2(2, 5); break;
+      case 6: SPIC_X2U(2, 4, 4); break;
+      case 7: SPIC_X2U(2, 4, 1); break;
       default: SPIC_X2(2, 4); break;
     }
 #undef SPIC_X2
+#undef SPIC_X2U
     spic::count_launch();
   } else if (dv == 3) {
     if (minimg)
