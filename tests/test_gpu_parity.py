@@ -563,3 +563,74 @@ def test_score_test_mode(spic, tmp_path):
         assert np.isfinite(rep[name]["mse"]) and rep[name]["mse"] < 3.0
         hdr = open(rep[name]["csv"]).readline().strip().split(",")
         assert hdr[:4] == ["x", "v1", "v2", "v3"] and hdr[-1] == "U3"
+
+
+def test_per_particle_probe_training_matches_oracle(spic):
+    """sbtm_update with per-particle Rademacher probes on the cell-sorted records (probes
+    indexed through perm) against the oracle drawing from the same PCG64 stream."""
+    from paper_2603_25832_b200.collision import build_cell_index
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.score import AdamW, MlpScoreNet, SbtmTrainer
+
+    n, L, M, H, K = 3000, 4 * math.pi, 8, 24, 4
+    rng = np.random.default_rng(21)
+    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    x[x >= L] = 0
+    v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
+    w = np.full(n, L / n)
+    p = ens(x, v, w)
+    ci = build_cell_index(p, Grid(M, L / M), S=4)
+    net = MlpScoreNet.init_glorot(3, H, np.random.default_rng(5))
+    onet = O.Net(*[a.cpu().numpy().copy() for a in net.params()])
+    opt = AdamW(lr=1e-3, weight_decay=0.0)
+    tr = SbtmTrainer(net, opt, K, L, "hutchinson", "per_particle", np.random.default_rng(77))
+    tr.run(n, ci=ci)
+    losses = tr.losses[:K].cpu().numpy()
+    ow = p.w.double().cpu().numpy()
+    ref = O.sbtm_update(onet, O.AdamW(lr=1e-3, weight_decay=0.0), x, v, ow, K, L=L,
+                        rng=np.random.default_rng(77), divergence="hutchinson",
+                        rademacher="per_particle")
+    np.testing.assert_allclose(losses, ref, rtol=2e-4)
+    S_dev = net.params64.cpu().numpy()
+    S_ref = np.concatenate([a.ravel() for a in onet.params()])
+    assert relL2(S_dev, S_ref) <= 1e-3
+
+
+def test_vml_engine_with_collisions_matches_oracle(spic):
+    """Full VML (Maxwell) steps with blob collisions (config-3 physics at small n) against
+    the oracle's full steps on the same float32 initial state."""
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.sampling import anisotropic_ensemble, seeded_b3_noise
+    from paper_2603_25832_b200.score import BlobEstimator
+    from paper_2603_25832_b200.state import FieldState
+
+    n, M, L, dt, nu = 8192, 16, 2 * math.pi / 1.25, 0.02, 0.01
+    rng = np.random.default_rng(3)
+    x, v, w = anisotropic_ensemble(n, L, (0.01, 0.04, 0.04), rng)
+    x = x.astype(np.float32).astype(np.float64)
+    v = v.astype(np.float32).astype(np.float64)
+    B3 = seeded_b3_noise(M, 1e-4, rng)
+    grid = Grid(M, L / M)
+    p = ens(x, v, w)
+    f = FieldState.from_arrays(np.zeros(M), np.zeros(M), B3, dv=3)
+    sim = Simulation(p, f, grid, dt=dt, nu=nu, mode="VML", gamma=-3.0,
+                     estimator=BlobEstimator(grid, 0.05), max_rows=8)
+    steps = 3
+    for k in range(1, steps + 1):
+        sim.step(k)
+    sim.check()
+    got = sim.records(range(1, steps + 1), range(1, steps + 1), [dt * k for k in range(1, steps + 1)])
+    ow = p.w.double().cpu().numpy()
+    st = dict(x=x.copy(), v=v.copy(), w=ow, E1=np.zeros(M), E2=np.zeros(M), B3=B3.copy())
+    ref = [O.full_step(st, eta=grid.eta, M=M, dt=dt, nu=nu, mode="VML", gamma=-3.0, net=None,
+                       opt=None, K=0, estimator="blob", bandwidth=0.05) for _ in range(steps)]
+    for a, b in zip(got, ref):
+        assert a.E_K == pytest.approx(b["E_K"], rel=1e-5)
+        assert a.E_B == pytest.approx(b["E_B"], rel=1e-3, abs=1e-14)
+        assert a.E_E == pytest.approx(b["E_E"], rel=1e-3, abs=1e-14)
+        assert a.H_dot == pytest.approx(b["H_dot"], rel=1e-3)
+    xs = p.x.double().cpu().numpy()
+    dxx = np.abs(xs - st["x"])
+    assert np.max(np.minimum(dxx, L - dxx)) <= 1e-5 * L
+    check_field(p.v.double().cpu().numpy(), st["v"], tol=1e-5)
