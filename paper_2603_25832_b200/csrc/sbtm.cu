@@ -104,201 +104,6 @@ __global__ void __launch_bounds__(256) k_mlp_forward(
 }
 
 // ------------------------------------------------------------------------------------------
-// ISM / MSE partials. MODE 0 exact, 1 shared Hutchinson, 2 per-particle probes, 3 MSE.
-// ------------------------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(kIsmNT) k_ism_partials(
-    const float* __restrict__ params, int H, int dv, const float4* __restrict__ xv,
-    const float4* __restrict__ sw, const float* __restrict__ x, const float* __restrict__ v,
-    int64_t ldv, const float* __restrict__ w, int64_t n, float x_scale, float L,
-    const float* __restrict__ Z, int64_t ldz, const int32_t* __restrict__ idx, float inv_wsum,
-    double* __restrict__ partials) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float4* Wp = (float4*)smem_raw;                   // [H]
-  float4* Bp = Wp + H;                              // [H]
-  float4* Uc = Bp + H;                              // [NT] (xn, v0, v1, v2)
-  float4* Gc = Uc + kIsmNT;                         // [NT] (gs0, gs1, gs2, w)
-  float4* Zc = Gc + kIsmNT;                         // [NT] probes (MODE 2)
-  float* coef = (float*)(Zc + kIsmNT);              // [H]
-  double* acc64 = (double*)(((uintptr_t)(coef + H) + 15) & ~(uintptr_t)15);  // [items][10]
-  __shared__ float b2[3];
-  __shared__ double red[8 * 4];
-
-  load_packed(params, H, dv, Wp, Bp, b2);
-  __syncthreads();
-  if (MODE == 0 || MODE == 1) {
-    // exact: coef_h = sum_i W2[i,h] W1[h,1+i] (ref: score.py:94-100, 314)
-    // shared Hutchinson: coef_h = (W2^T z)_h (W1_v z)_h (ref: score.py:324-327)
-    for (int h = threadIdx.x; h < H; h += blockDim.x) {
-      const float4 a = Wp[h], b = Bp[h];
-      if (MODE == 0) {
-        coef[h] = b.y * a.y + b.z * a.z + b.w * a.w;
-      } else {
-        float z0 = Z[0], z1 = Z[1], z2 = dv > 2 ? Z[2] : 0.f;
-        float t = a.y * z0 + a.z * z1 + a.w * z2;
-        float r = b.y * z0 + b.z * z1 + b.w * z2;
-        coef[h] = r * t;
-      }
-    }
-  }
-  const int G = max(1, kIsmNT / H);        // particle groups per hidden unit
-  const int items = H * G;
-  for (int it = threadIdx.x; it < items; it += blockDim.x)
-    for (int k = 0; k < kIsmAcc; ++k) acc64[it * kIsmAcc + k] = 0.0;
-  double lacc[4] = {0.0, 0.0, 0.0, 0.0};  // loss, gb2[3]
-  __syncthreads();
-
-  const int64_t nchunks = (n + kIsmNT - 1) / kIsmNT;
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    // ---- phase 1: one particle per thread, forward + loss + dL/ds -----------------------
-    const int64_t p = ch * kIsmNT + threadIdx.x;
-    const bool valid = p < n;
-    float xn = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, wp = 0.f;
-    float q0 = 0.f, q1 = 0.f, q2 = 0.f;  // probe (MODE 2) or target (MODE 3)
-    if (valid) {
-      const int64_t r = idx ? (int64_t)idx[p] : p;
-      if (xv) {
-        float4 A = xv[p];
-        xn = A.x < 0.f ? A.x + L : A.x;
-        v0 = A.y; v1 = A.z; v2 = A.w;
-        wp = sw[p].w;
-      } else {
-        xn = x[r];
-        v0 = v[r];
-        v1 = v[ldv + r];
-        v2 = dv > 2 ? v[2 * ldv + r] : 0.f;
-        wp = w[r];
-      }
-      xn *= x_scale;
-      if (MODE >= 2) {
-        q0 = Z[r];
-        q1 = Z[ldz + r];
-        q2 = dv > 2 ? Z[2 * ldz + r] : 0.f;
-      }
-    }
-    if (MODE == 3) wp *= inv_wsum;
-    float s0 = b2[0], s1 = b2[1], s2 = b2[2], div = 0.f;
-#pragma unroll 4
-    for (int h = 0; h < H; ++h) {
-      const float4 a = Wp[h];
-      const float4 b = Bp[h];
-      float z = fmaf(a.w, v2, fmaf(a.z, v1, fmaf(a.y, v0, fmaf(a.x, xn, b.x))));
-      float inv = fast_rcp(1.f + fabsf(z));
-      float act = z * inv;
-      s0 = fmaf(b.y, act, s0);
-      s1 = fmaf(b.z, act, s1);
-      s2 = fmaf(b.w, act, s2);
-      if (MODE == 0 || MODE == 1) {
-        div = fmaf(coef[h], inv * inv, div);
-      } else if (MODE == 2) {
-        float t = a.y * q0 + a.z * q1 + a.w * q2;
-        float rr = b.y * q0 + b.z * q1 + b.w * q2;
-        div = fmaf(rr * t, inv * inv, div);
-      }
-    }
-    float g0, g1, g2, lp;
-    if (MODE == 3) {
-      float e0 = s0 - q0, e1 = s1 - q1, e2 = s2 - q2;
-      lp = wp * (e0 * e0 + e1 * e1 + e2 * e2);
-      g0 = 2.f * wp * e0; g1 = 2.f * wp * e1; g2 = 2.f * wp * e2;
-    } else {
-      lp = wp * (s0 * s0 + s1 * s1 + s2 * s2 + 2.f * div);
-      g0 = 2.f * wp * s0; g1 = 2.f * wp * s1; g2 = 2.f * wp * s2;
-    }
-    if (dv < 3) g2 = 0.f;
-    if (valid) {
-      lacc[0] += (double)lp;
-      lacc[1] += (double)g0;
-      lacc[2] += (double)g1;
-      lacc[3] += (double)g2;
-    } else {
-      g0 = g1 = g2 = 0.f;
-      wp = 0.f;
-    }
-    Uc[threadIdx.x] = make_float4(xn, v0, v1, v2);
-    Gc[threadIdx.x] = make_float4(g0, g1, g2, wp);
-    if (MODE == 2) Zc[threadIdx.x] = make_float4(q0, q1, q2, 0.f);
-    __syncthreads();
-    // ---- phase 2: one (hidden unit, particle group) per thread, outer-product sums ------
-    const int np = (int)(n - ch * kIsmNT < (int64_t)kIsmNT ? n - ch * kIsmNT : (int64_t)kIsmNT);
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int h = it % H, g = it / H;
-      const float4 a = Wp[h], b = Bp[h];
-      const float ch_ = (MODE == 0 || MODE == 1) ? coef[h] : 0.f;
-      float gw0 = 0.f, gw1 = 0.f, gw2 = 0.f, gw3 = 0.f, gb = 0.f;
-      float gv0 = 0.f, gv1 = 0.f, gv2 = 0.f, phi = 0.f;
-#pragma unroll 4
-      for (int q = g; q < np; q += G) {
-        const float4 u = Uc[q];
-        const float4 gs = Gc[q];
-        float z = fmaf(a.w, u.w, fmaf(a.z, u.z, fmaf(a.y, u.y, fmaf(a.x, u.x, b.x))));
-        float inv = fast_rcp(1.f + fabsf(z));
-        float act = z * inv;
-        float sp = inv * inv;
-        float da = fmaf(gs.z, b.w, fmaf(gs.y, b.z, gs.x * b.y));
-        float d = da * sp;
-        if (MODE != 3) {
-          float spp = copysignf(2.f * sp * inv, -z);  // -2 sign(z) inv^3 (0 at z = 0 below)
-          if (z == 0.f) spp = 0.f;
-          float cc;
-          if (MODE == 2) {
-            const float4 zz = Zc[q];
-            float t = a.y * zz.x + a.z * zz.y + a.w * zz.z;
-            float rr = b.y * zz.x + b.z * zz.y + b.w * zz.z;
-            cc = rr * t;
-            float k2 = 2.f * gs.w * sp;
-            // d/dW2: 2 w sp t z_i ; d/dW1_v: 2 w sp r z_k (ref: score.py:242, 250)
-            gv0 = fmaf(k2 * t, zz.x, gv0);
-            gv1 = fmaf(k2 * t, zz.y, gv1);
-            gv2 = fmaf(k2 * t, zz.z, gv2);
-            gw1 = fmaf(k2 * rr, zz.x, gw1);
-            gw2 = fmaf(k2 * rr, zz.y, gw2);
-            gw3 = fmaf(k2 * rr, zz.z, gw3);
-          } else {
-            cc = ch_;
-            phi = fmaf(gs.w, sp, phi);
-          }
-          d = fmaf(2.f * gs.w * cc, spp, d);
-        }
-        gb += d;
-        gw0 = fmaf(d, u.x, gw0);
-        gw1 = fmaf(d, u.y, gw1);
-        gw2 = fmaf(d, u.z, gw2);
-        gw3 = fmaf(d, u.w, gw3);
-        gv0 = fmaf(gs.x, act, gv0);
-        gv1 = fmaf(gs.y, act, gv1);
-        gv2 = fmaf(gs.z, act, gv2);
-      }
-      double* A = acc64 + it * kIsmAcc;
-      A[0] += gw0; A[1] += gw1; A[2] += gw2; A[3] += gw3;
-      A[4] += gb;
-      A[5] += gv0; A[6] += gv1; A[7] += gv2;
-      A[8] += phi;
-    }
-    __syncthreads();
-  }
-  // ---- write block partials: [loss, gW1, gb1, gW2, gb2, Phi] ------------------------------
-  block_sum<4>(lacc, red);
-  const int64_t P = n_params(H, dv);
-  const int64_t width = 1 + P + H;
-  double* out = partials + (size_t)blockIdx.x * width;
-  if (threadIdx.x == 0) {
-    out[0] = lacc[0];
-    for (int i = 0; i < dv; ++i) out[1 + P - dv + i] = lacc[1 + i];
-  }
-  const int64_t oW1 = 1, ob1 = oW1 + (int64_t)H * (1 + dv), oW2 = ob1 + H, oPhi = 1 + P;
-  for (int h = threadIdx.x; h < H; h += blockDim.x) {
-    double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int g = 0; g < G; ++g)
-      for (int k = 0; k < 9; ++k) s[k] += acc64[(g * H + h) * kIsmAcc + k];
-    for (int k = 0; k < 1 + dv; ++k) out[oW1 + h * (1 + dv) + k] = s[k];
-    out[ob1 + h] = s[4];
-    for (int i = 0; i < dv; ++i) out[oW2 + i * H + h] = s[5 + i];
-    out[oPhi + h] = s[8];
-  }
-}
-
-// ------------------------------------------------------------------------------------------
 // Packed-FP32 ISM / MSE partials: two particles per f32x2 lane pair. Same math, same partial
 // layout as k_ism_partials; chunks of 2*NT particles, thread t of phase 1 owns particles
 // (t, t+NT), phase 2 item (h, g) sweeps the staged particle pairs k = g, g+G, ...
@@ -342,21 +147,21 @@ __device__ __forceinline__ void ism_load_particle(
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kIsmNT) k_ism_partials_x2(
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NT) k_ism_partials_x2(
     const float* __restrict__ params, int H, int dv, const float4* __restrict__ xv,
     const float4* __restrict__ sw, const float* __restrict__ x, const float* __restrict__ v,
     int64_t ldv, const float* __restrict__ w, int64_t n, float x_scale, float L,
     const float* __restrict__ Z, int64_t ldz, const int32_t* __restrict__ idx, float inv_wsum,
     double* __restrict__ partials) {
-  constexpr int CP = 2 * kIsmNT;
+  constexpr int CP = 2 * NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float4* Wp = (float4*)smem_raw;        // [H]
   float4* Bp = Wp + H;                   // [H]
   float4* U2 = Bp + H;                   // [NT][2]: (x_a, x_b, v0_a, v0_b), (v1_a, v1_b, v2_a, v2_b)
-  float4* G2 = U2 + 2 * kIsmNT;          // [NT][2]: (g0_a, g0_b, g1_a, g1_b), (g2_a, g2_b, w_a, w_b)
-  float4* Z2 = G2 + 2 * kIsmNT;          // [NT][2]: probes (MODE 2)
-  float* coef = (float*)(Z2 + 2 * kIsmNT);
+  float4* G2 = U2 + 2 * NT;          // [NT][2]: (g0_a, g0_b, g1_a, g1_b), (g2_a, g2_b, w_a, w_b)
+  float4* Z2 = G2 + 2 * NT;          // [NT][2]: probes (MODE 2)
+  float* coef = (float*)(Z2 + 2 * NT);
   double* acc64 = (double*)(((uintptr_t)(coef + H) + 15) & ~(uintptr_t)15);  // [items][10]
   __shared__ float b2[3];
   __shared__ double red[8 * 4];
@@ -374,7 +179,7 @@ __global__ void __launch_bounds__(kIsmNT) k_ism_partials_x2(
       }
     }
   }
-  const int G = max(1, kIsmNT / H);
+  const int G = max(1, NT / H);
   const int items = H * G;
   for (int it = threadIdx.x; it < items; it += blockDim.x)
     for (int k = 0; k < kIsmAcc; ++k) acc64[it * kIsmAcc + k] = 0.0;
@@ -386,7 +191,7 @@ __global__ void __launch_bounds__(kIsmNT) k_ism_partials_x2(
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     // ---- phase 1: particles (t, t+NT) as one packed pair ------------------------------
     float ua[4], ub[4], qa[3], qb[3], wa, wb;
-    const int64_t pa = ch * CP + threadIdx.x, pb = pa + kIsmNT;
+    const int64_t pa = ch * CP + threadIdx.x, pb = pa + NT;
     ism_load_particle<MODE>(pa, n, xv, sw, x, v, ldv, w, x_scale, L, Z, ldz, idx, dv, ua, wa, qa);
     ism_load_particle<MODE>(pb, n, xv, sw, x, v, ldv, w, x_scale, L, Z, ldz, idx, dv, ub, wb, qb);
     if (MODE == 3) {
@@ -463,7 +268,7 @@ __global__ void __launch_bounds__(kIsmNT) k_ism_partials_x2(
     __syncthreads();
     // ---- phase 2: one (hidden unit, pair group) per thread, packed outer products ------
     const int64_t rem = n - ch * CP;
-    const int npairs = (int)(rem < (int64_t)kIsmNT ? rem : (int64_t)kIsmNT);
+    const int npairs = (int)(rem < (int64_t)NT ? rem : (int64_t)NT);
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
       const int h = it % H, gq = it / H;
       const float4 a = Wp[h], b = Bp[h];
@@ -666,14 +471,18 @@ __global__ void k_ism_reduce_cols(const double* __restrict__ part, int rows, int
   if (lane == 0) out[col] = s;
 }
 
+// threads per block of the packed ISM kernel: 128 for small n (more blocks to hide latency)
+static int ism_nt(int64_t n) { return n < (1 << 18) ? 128 : kIsmNT; }
+
 static int ism_blocks(int64_t n) {
-  int64_t chunks = (n + 2 * kIsmNT - 1) / (2 * kIsmNT);  // packed kernel: 2*NT per chunk
+  const int nt = ism_nt(n);
+  int64_t chunks = (n + 2 * nt - 1) / (2 * nt);  // packed kernel: 2*NT particles per chunk
   return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, kIsmBlocksMax));
 }
 
-static size_t ism_smem(int H) {
-  int G = std::max(1, kIsmNT / H);
-  size_t b = sizeof(float4) * (2 * (size_t)H + 6 * kIsmNT) + sizeof(float) * H + 16;
+static size_t ism_smem(int H, int nt) {
+  int G = std::max(1, nt / H);
+  size_t b = sizeof(float4) * (2 * (size_t)H + 6 * (size_t)nt) + sizeof(float) * H + 16;
   b += sizeof(double) * (size_t)H * G * kIsmAcc;
   return b;
 }
@@ -718,18 +527,23 @@ extern "C" int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv
   if (mode >= 1 && !Z) return SPIC_ERR_ARG;
   if (scratch_bytes < spic_ism_scratch_bytes(n, H, dv)) return SPIC_ERR_SCRATCH;
   const int blocks = ism_blocks(n);
-  size_t smem = ism_smem(H);
+  const int nt = ism_nt(n);
+  size_t smem = ism_smem(H, nt);
   cudaStream_t st = (cudaStream_t)stream;
   const float L = 1.0f / x_scale;
-#define SPIC_ISM_LAUNCH(MD)                                                                    \
+#define SPIC_ISM_LAUNCH_NT(MD, NT_)                                                           \
   do {                                                                                         \
     if (smem > 48 * 1024)                                                                      \
-      cudaFuncSetAttribute(k_ism_partials_x2<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                         \
-    k_ism_partials_x2<MD><<<blocks, kIsmNT, smem, st>>>(params32, H, dv, (const float4*)xv,    \
-                                                     (const float4*)sw, x, v, ldv, w, n,       \
-                                                     x_scale, L, Z, ldz, idx, (float)inv_wsum, \
-                                                     (double*)scratch); spic::count_launch();                        \
+      cudaFuncSetAttribute(k_ism_partials_x2<MD, NT_>,                                         \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    k_ism_partials_x2<MD, NT_><<<blocks, NT_, smem, st>>>(                                     \
+        params32, H, dv, (const float4*)xv, (const float4*)sw, x, v, ldv, w, n, x_scale, L, Z, \
+        ldz, idx, (float)inv_wsum, (double*)scratch);                                          \
+    spic::count_launch();                                                                      \
+  } while (0)
+#define SPIC_ISM_LAUNCH(MD)                                                                    \
+  do {                                                                                         \
+    if (nt == 128) SPIC_ISM_LAUNCH_NT(MD, 128); else SPIC_ISM_LAUNCH_NT(MD, kIsmNT);           \
   } while (0)
   switch (mode) {
     case 0: SPIC_ISM_LAUNCH(0); break;
@@ -738,6 +552,7 @@ extern "C" int spic_ism_partials_ex(const float* params32, int32_t H, int32_t dv
     default: SPIC_ISM_LAUNCH(3); break;
   }
 #undef SPIC_ISM_LAUNCH
+#undef SPIC_ISM_LAUNCH_NT
   SPIC_CHECK_LAUNCH();
   const int64_t width = 1 + n_params(H, dv) + H;
   double* part = (double*)scratch;
