@@ -52,6 +52,10 @@ WORKLOADS = {
                n=1 << 24, M=1024, L=4 * math.pi, alpha=0.01, k=0.5, c=0.0, nu=0.1, dt=0.05,
                K=10, hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact",
                estimator="sbtm"),
+    "c2blob": dict(workload="config2_two_stream_blob", preset="two_stream", mode="VPL",
+                   n=1 << 20, M=128, L=10 * math.pi, alpha=0.001, k=0.2, c=2.4, nu=0.05,
+                   dt=0.05, K=0, hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact",
+                   estimator="blob", bandwidth="silverman"),
     "c4blob": dict(workload="config4_landau_damping_blob_n2^24", preset="landau_damping",
                    mode="VPL", n=1 << 24, M=1024, L=4 * math.pi, alpha=0.01, k=0.5, c=0.0,
                    nu=0.1, dt=0.05, K=0, hidden=128, lr=1e-3, weight_decay=0.0,
@@ -257,7 +261,8 @@ def build_sim(wl: dict, seed: int, device):
         est = SbtmEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay,
                             divergence=cfg.divergence, rademacher=cfg.rademacher)
     else:
-        est = BlobEstimator(grid, float(wl["bandwidth"]))
+        bw = wl["bandwidth"]
+        est = BlobEstimator(grid, None if bw == "silverman" else float(bw))
     sim = Simulation(p, fields, grid, dt=cfg.dt, nu=cfg.nu, mode=cfg.mode, gamma=cfg.gamma,
                      estimator=est, max_rows=4)
     del torch

@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "pairs.cuh"
+#include "f32x2.cuh"
 
 namespace spic {
 
@@ -188,6 +189,127 @@ __global__ void __launch_bounds__(kLandauNT, 4)
   }
 }
 
+// Packed-FP32 blob sweep (dv = 3): 4 targets per thread as two f32x2 pairs, the j record
+// broadcast in the B/C operand slots; one MUFU.EX2 per pair. Same partial layout as above.
+template <bool MINIMG, bool UNIFORM_W>
+__global__ void __launch_bounds__(kLandauNT, 4)
+    k_blob_x2(const float4* __restrict__ xv, const float4* __restrict__ sw,
+              const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
+              const int32_t* __restrict__ tile_start, int M, int S, float L, float ie, float ie2,
+              float wie, float wie2, const float* __restrict__ h_cell, float h_fixed, int nsplit,
+              float* __restrict__ part, int64_t n) {
+  constexpr int RP = 2;
+  constexpr int TI = kLandauNT * 2 * RP;
+  __shared__ alignas(128) float4 s_xv[kLandauStages][kLandauTJ];
+  __shared__ alignas(128) float4 s_sw[UNIFORM_W ? 1 : kLandauStages][kLandauTJ];
+  __shared__ alignas(8) uint64_t s_bar[kLandauStages];
+  const int tile = blockIdx.x, split = blockIdx.y;
+  if (tile >= tile_start[M]) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kLandauStages; ++s) mbar_init(&s_bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  int lo = 0, hi = M;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(tile_start + mid) <= tile) lo = mid; else hi = mid;
+  }
+  const int c = lo;
+  const int cs = cell_start[c], ce = cell_start[c + 1];
+  const int t0 = cs + (tile - tile_start[c]) * TI;
+  const int t1 = min(t0 + TI, ce);
+  Window win = build_window(cell_start, sub_start, M, S, c, t0, t1, L);
+  int wlen = 0;
+  for (int s = 0; s < win.nseg; ++s) wlen += win.len[s];
+  const int jlo = (int)(((long long)wlen * split) / nsplit);
+  const int jhi = (int)(((long long)wlen * (split + 1)) / nsplit);
+  const int ntiles = window_tiles(win, jlo, jhi);
+  const float h = h_cell ? h_cell[c] : h_fixed;
+  const float kexp = -1.4426950408889634f * (0.5f / (h * h));  // exp(-q2/2h^2) = 2^(kexp q2)
+
+  f2 X[RP], V0[RP], V1[RP], V2[RP], DEN[RP], M0[RP], M1[RP], M2[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) {
+    float4 Ae = make_float4(1e30f, 0.f, 0.f, 0.f), Ao = Ae;
+    const int pe = t0 + threadIdx.x + (2 * r) * kLandauNT, po = pe + kLandauNT;
+    if (pe < t1) Ae = xv[pe];
+    if (po < t1) Ao = xv[po];
+    X[r] = mk2(Ae.x, Ao.x);
+    V0[r] = mk2(Ae.y, Ao.y); V1[r] = mk2(Ae.z, Ao.z); V2[r] = mk2(Ae.w, Ao.w);
+    DEN[r] = M0[r] = M1[r] = M2[r] = mk2(0.f, 0.f);
+  }
+  auto issue = [&](int q) {
+    TileDesc d = window_tile(win, jlo, jhi, q);
+    const int st = q % kLandauStages;
+    mbar_expect_tx(&s_bar[st], (uint32_t)((UNIFORM_W ? 1 : 2) * d.cnt * sizeof(float4)));
+    bulk_g2s(&s_xv[st][0], xv + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
+    if (!UNIFORM_W) bulk_g2s(&s_sw[st][0], sw + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
+  };
+  if (threadIdx.x == 0) {
+    fence_proxy_async();
+    for (int q = 0; q < min(ntiles, kLandauStages); ++q) issue(q);
+  }
+  const f2 W1c = UNIFORM_W ? mk2(wie, wie) : mk2(ie, ie);
+  const f2 nW2 = UNIFORM_W ? mk2(-wie2, -wie2) : mk2(-ie2, -ie2);
+  const f2 invL2 = mk2(1.0f / L, 1.0f / L), negL2 = mk2(-L, -L), kx2 = mk2(kexp, kexp);
+  for (int q = 0; q < ntiles; ++q) {
+    const int st = q % kLandauStages;
+    TileDesc d = window_tile(win, jlo, jhi, q);
+    f2 XA[RP];
+    const f2 sh = mk2(d.shift, d.shift);
+#pragma unroll
+    for (int r = 0; r < RP; ++r) XA[r] = sub2(X[r], sh);
+    mbar_wait(&s_bar[st], (uint32_t)((q / kLandauStages) & 1));
+    const float4* __restrict__ P = s_xv[st];
+    const float4* __restrict__ Q = s_sw[UNIFORM_W ? 0 : st];
+#pragma unroll 2
+    for (int jj = 0; jj < d.cnt; ++jj) {
+      const float4 A = P[jj];
+      const float wj = UNIFORM_W ? 1.f : Q[jj].w;
+      const f2 xj = mk2(A.x, A.x), vj0 = mk2(A.y, A.y), vj1 = mk2(A.z, A.z), vj2 = mk2(A.w, A.w);
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        f2 dx = sub2(XA[r], xj);
+        if (MINIMG) dx = fma2(rint2(mul2(dx, invL2)), negL2, dx);
+        float ce, co;
+        un2(fma2(abs2(dx), nW2, W1c), ce, co);
+        ce = fmaxf(ce, 0.f);
+        co = fmaxf(co, 0.f);
+        if (!UNIFORM_W) {
+          ce *= wj;
+          co *= wj;
+        }
+        const f2 z0 = sub2(V0[r], vj0), z1 = sub2(V1[r], vj1), z2 = sub2(V2[r], vj2);
+        float ee, eo;
+        un2(mul2(fma2(z2, z2, fma2(z1, z1, mul2(z0, z0))), kx2), ee, eo);
+        const f2 kw = mul2(mk2(ce, co), mk2(exp2f(ee), exp2f(eo)));
+        DEN[r] = add2(DEN[r], kw);
+        M0[r] = fma2(kw, vj0, M0[r]);
+        M1[r] = fma2(kw, vj1, M1[r]);
+        M2[r] = fma2(kw, vj2, M2[r]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && q + kLandauStages < ntiles) {
+      fence_proxy_async();
+      issue(q + kLandauStages);
+    }
+  }
+  float* out = part + (size_t)split * 4 * n;
+#pragma unroll
+  for (int r = 0; r < RP; ++r) {
+    float de, dn, m0e, m0o, m1e, m1o, m2e, m2o;
+    un2(DEN[r], de, dn);
+    un2(M0[r], m0e, m0o);
+    un2(M1[r], m1e, m1o);
+    un2(M2[r], m2e, m2o);
+    const int pe = t0 + threadIdx.x + (2 * r) * kLandauNT, po = pe + kLandauNT;
+    if (pe < t1) { out[pe] = de; out[n + pe] = m0e; out[2 * n + pe] = m1e; out[3 * n + pe] = m2e; }
+    if (po < t1) { out[po] = dn; out[n + po] = m0o; out[2 * n + po] = m1o; out[3 * n + po] = m2o; }
+  }
+}
+
 // fold splits (fixed order), form s, isolated-particle check
 __global__ void k_blob_fold(const float* __restrict__ part, int nsplit, int64_t n, int dv,
                             const float4* __restrict__ xv, float4* __restrict__ sw,
@@ -232,14 +354,8 @@ __global__ void k_blob_fold(const float* __restrict__ part, int nsplit, int64_t 
   }
 }
 
-static int blob_nsplit(int64_t n, int M) {
-  int64_t tiles = n / kLandauTI + (M + 1) / 2;
-  if (tiles < 1) tiles = 1;
-  int64_t want = (4 * kNumSMs + tiles - 1) / tiles;
-  int64_t window = 3 * n / std::max(M, 1);
-  int64_t cap = std::max<int64_t>(1, window / 512);
-  want = std::min<int64_t>(want, cap);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, 16));
+static int blob_nsplit(int64_t n, int M, int dv) {
+  return pair_nsplit(n, M, dv == 3 ? kLandauNT * 4 : kLandauTI);
 }
 
 }  // namespace spic
@@ -247,8 +363,7 @@ static int blob_nsplit(int64_t n, int M) {
 using namespace spic;
 
 extern "C" size_t spic_blob_scratch_bytes(int64_t n, int32_t M, int32_t dv) {
-  (void)dv;
-  int ns = blob_nsplit(n, M);
+  int ns = blob_nsplit(n, M, dv);
   return sizeof(float) * (size_t)ns * 4 * n + sizeof(double) * 3 * (size_t)M +
          sizeof(int32_t) * (M + 1) + 1024;
 }
@@ -264,7 +379,7 @@ extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_
   if (bandwidth <= 0 && !h_cell) return SPIC_ERR_ARG;
   if (n == 0) return SPIC_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const int ns = blob_nsplit(n, M);
+  const int ns = blob_nsplit(n, M, dv);
   float* part = (float*)scratch;
   uintptr_t pp = (uintptr_t)(part + (size_t)ns * 4 * n);
   pp = (pp + 255) & ~(uintptr_t)255;
@@ -278,13 +393,25 @@ extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_
     SPIC_CHECK_LAUNCH();
     hc = h_cell;
   }
-  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, kLandauTI, tile_start); spic::count_launch();
+  const bool packed = dv == 3;
+  const int TI = packed ? kLandauNT * 4 : kLandauTI;
+  k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start); spic::count_launch();
   const double L = (double)M * eta;
   const float ie = (float)(1.0 / eta), ie2 = (float)(1.0 / (eta * eta));
   const float wie = (float)((double)uniform_w / eta), wie2 = (float)((double)uniform_w / (eta * eta));
-  dim3 grid((unsigned)(n / kLandauTI + M + 1), (unsigned)ns);
+  dim3 grid((unsigned)(n / TI + M + 1), (unsigned)ns);
   const bool mi = M <= 2, uw = uniform_w > 0.f;
   const float hf = (float)bandwidth;
+  if (packed) {
+#define SPIC_BLOBX(MI_, UW_)                                                                   \
+  k_blob_x2<MI_, UW_><<<grid, kLandauNT, 0, st>>>(xv4, (const float4*)sw, cell_start, sub_start, \
+                                                  tile_start, M, S, (float)L, ie, ie2, wie, wie2, \
+                                                  hc, hf, ns, part, n)
+    if (mi) { if (uw) SPIC_BLOBX(true, true); else SPIC_BLOBX(true, false); }
+    else { if (uw) SPIC_BLOBX(false, true); else SPIC_BLOBX(false, false); }
+#undef SPIC_BLOBX
+    spic::count_launch();
+  } else {
 #define SPIC_BLOB(DV_, MI_, UW_)                                                             \
   do {                                                                                       \
     k_blob_pairs<DV_, MI_, UW_><<<grid, kLandauNT, 0, st>>>(                                 \
@@ -292,14 +419,10 @@ extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_
         wie, wie2, hc, hf, ns, part, n);                                                     \
     spic::count_launch();                                                                    \
   } while (0)
-  if (dv == 3) {
-    if (mi) { if (uw) SPIC_BLOB(3, true, true); else SPIC_BLOB(3, true, false); }
-    else { if (uw) SPIC_BLOB(3, false, true); else SPIC_BLOB(3, false, false); }
-  } else {
     if (mi) { if (uw) SPIC_BLOB(2, true, true); else SPIC_BLOB(2, true, false); }
     else { if (uw) SPIC_BLOB(2, false, true); else SPIC_BLOB(2, false, false); }
-  }
 #undef SPIC_BLOB
+  }
   SPIC_CHECK_LAUNCH();
   int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
   k_blob_fold<<<blocks, 256, 0, st>>>(part, ns, n, dv, xv4, (float4*)sw, perm, cell_start, M, hc,

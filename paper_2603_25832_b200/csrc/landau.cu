@@ -433,26 +433,7 @@ static void dispatch_g(int gm, bool uw, dim3 g, cudaStream_t st, const float4* x
 }
 
 static int auto_nsplit(int64_t n, int M, int dv) {
-  // choose the j-split so the (tile, split) CTA count fills whole waves of the resident
-  // CTA slots (4 per SM): wave quantisation, not the pair count, sets the tail
-  const bool packed = dv == 3;
-  const int TI = packed ? kLandauNT * 2 * 2 : kLandauTI;
-  const double tiles = std::max<double>(1.0, (double)(n / TI) + 0.5 * M);
-  const double slots = 4.0 * kNumSMs;
-  const int64_t window = 2 * n / std::max(M, 1);  // records in a culled j-window (approx.)
-  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(16, window / 1024));
-  int best = 1;
-  double best_eff = -1.0;
-  for (int ns = 1; ns <= cap; ++ns) {
-    const double waves = tiles * ns / slots;
-    double eff = waves < 1.0 ? waves : waves / std::ceil(waves);
-    eff -= 0.004 * (ns - 1);  // each split re-reads targets and writes a partial U
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = ns;
-    }
-  }
-  return best;
+  return pair_nsplit(n, M, dv == 3 ? kLandauNT * 2 * 2 : kLandauTI);
 }
 
 __global__ void k_fold_splits(const float* __restrict__ part, int nsplit, int dv, int64_t n,

@@ -188,4 +188,26 @@ static __global__ void k_landau_tiles(const int32_t* __restrict__ cell_start, in
   }
 }
 
+// j-split of a pair kernel: choose nsplit so the (tile, split) CTA count fills whole waves
+// of the resident CTA slots (4 per SM); wave quantisation, not the pair count, sets the tail
+static inline int pair_nsplit(int64_t n, int M, int TI) {
+  const double tiles = (double)(n / TI) + 0.5 * M > 1.0 ? (double)(n / TI) + 0.5 * M : 1.0;
+  const double slots = 4.0 * kNumSMs;
+  const int64_t window = 2 * n / (M > 1 ? M : 1);  // records in a culled j-window (approx.)
+  int cap = (int)(window / 1024);
+  cap = cap < 1 ? 1 : (cap > 16 ? 16 : cap);
+  int best = 1;
+  double best_eff = -1.0;
+  for (int ns = 1; ns <= cap; ++ns) {
+    const double waves = tiles * ns / slots;
+    double eff = waves < 1.0 ? waves : waves / ceil(waves);
+    eff -= 0.004 * (ns - 1);  // each split re-reads targets and writes a partial
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = ns;
+    }
+  }
+  return best;
+}
+
 }  // namespace spic

@@ -67,6 +67,11 @@ def main():
                                                           reset_lr=True, apply_step=False))
         out["mlp_forward_ms"] = timeit(lambda: sim.est.estimate_sorted(ci, n))
         out["sbtm_update_K_ms"] = timeit(lambda: tr.run(n, ci=ci, flags=sim.flags), reps=3)
+    else:
+        from paper_2603_25832_b200.score import blob_sorted
+
+        out["blob_ms"] = timeit(lambda: blob_sorted(ci, p, g, sim.est.bandwidth, sim.flags,
+                                                    sim.bad_pid, sim.h_cell), reps=5)
     out["landau_ms"] = timeit(lambda: landau_sorted(ci, p, g, sim.gamma, sim.U_sorted,
                                                     nsplit=sim.opt.landau_split), reps=5)
     out["step_ms"] = timeit(lambda: sim.step(1), reps=5)
