@@ -501,8 +501,8 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   const char* var = getenv("SPIC_LANDAU_VARIANT");
   const bool packed = dv == 3 && gm == 0 && !(var && var[0] == 's');
   // experiment knob: SPIC_LANDAU_VARIANT = s (scalar) | 1 (RP1) | 3 (RP3) | 4 (RP2, 4 CTA/SM)
-  const int cfg = (var && var[0] >= '1' && var[0] <= '7') ? var[0] - '0' : 2;
-  const int rp = cfg == 1 ? 1 : (cfg == 3 ? 3 : 2);
+  const int cfg = (var && var[0] >= '1' && var[0] <= '9') ? var[0] - '0' : 2;
+  const int rp = (cfg == 1 || cfg == 9) ? 1 : (cfg == 3 ? 3 : 2);
   const int TI = packed ? kLandauNT * 2 * rp : kLandauTI;
   k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start, c_lo, c_hi); spic::count_launch();
   SPIC_CHECK_LAUNCH();
@@ -538,6 +538,8 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
       case 5: SPIC_X2(2, 5); break;
       case 6: SPIC_X2U(2, 4, 4); break;
       case 7: SPIC_X2U(2, 4, 1); break;
+      case 8: SPIC_X2U(2, 5, 1); break;
+      case 9: SPIC_X2U(1, 8, 2); break;
       default: SPIC_X2(2, 4); break;
     }
 #undef SPIC_X2
