@@ -175,6 +175,35 @@ int spic_adamw_step(double* params64, const double* grads64, double* m, double* 
                     double* opt_state, double beta1, double beta2, double eps,
                     double weight_decay, float* params32, void* stream);
 
+/* ---- M1 extension: the BASELINE "2 x 128 SiLU" score network (no reference counterpart;
+ *      the reference's softsign net is score.py:38-71). Hidden GEMMs on tcgen05 tensor cores
+ *      in split-BF16 with float32 TMEM accumulation; H must be 128, dv = 3.
+ * Params (float32 working copy / float64 master): W1[H][4], b1[H], W2[H][H], b2[H], W3[3][H],
+ * b3[3]; u = [x * x_scale, v]. Inputs are cell-sorted records xv/sw (x' < 0 mapped back by
+ * +L = 1/x_scale; weight in sw.w). ---------------------------------------------------------- */
+int64_t spic_silu_num_params(int32_t H);
+size_t spic_silu_scratch_bytes(int64_t n);
+/* s into sw_out lanes 0..2 (lane 3 = the input weight); sw_out may alias sw. */
+int spic_silu_forward(const float* params32, int32_t H, const float* xv, const float* sw,
+                      int64_t n, float x_scale, float* sw_out, void* stream);
+/* Per-CTA float64 partials of [loss, grads] of sum_p w_p (|s_p|^2 + 2 div_p) with the exact
+ * divergence, reduced in fixed order into the row at spic_silu_row_offset(n). */
+int spic_silu_ism_partials(const float* params32, int32_t H, const float* xv, const float* sw,
+                           int64_t n, float x_scale, void* scratch, size_t scratch_bytes,
+                           void* stream);
+int64_t spic_silu_row_offset(int64_t n);
+/* AdamW with restore-and-halve recovery on the reduced row (same contract as
+ * spic_sbtm_finalize_ex with div_mode 0). */
+int spic_silu_finalize(void* scratch, int64_t n, int32_t H, double* params64, double* m,
+                       double* v2, double* opt_state, double beta1, double beta2, double eps,
+                       double weight_decay, int32_t reset_lr, int32_t apply_step,
+                       float* params32, double* grads_out, double* loss_out, int32_t* flags,
+                       void* stream);
+/* Tensor-core self-test: float32 [128][128] W, X, Y -> D1 = W X^T, D2 = W^T Y^T, D3 = Y^T X
+ * through the same split-BF16 tcgen05 GEMM views the SiLU kernel uses. */
+int spic_umma_selftest(const float* W, const float* X, const float* Y, float* D1, float* D2,
+                       float* D3, void* stream);
+
 /* ---- PIC (replaces interpolate_fields pic.py:61-74, lorentz_push pic.py:77-88,
  *      advance_positions pic.py:91-93 + wrap_position state.py:14-27, deposit
  *      pic.py:43-58, maxwell_step pic.py:96-110, vpl_field_step pic.py:113-115,

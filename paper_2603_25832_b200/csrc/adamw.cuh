@@ -1,0 +1,77 @@
+// adamw.cuh — the tail of every score-net training step: AdamW on the float64 master
+// parameters with the reference's restore-and-halve recovery (ref: score.py:371-386,
+// score.py:568-587). Called by all threads of a single-CTA finalize kernel; `grad` and `cand`
+// (candidate parameters, P doubles) may live in shared or global memory.
+#pragma once
+#include "common.cuh"
+
+namespace spic {
+
+// mse: pretraining semantics (a non-finite loss raises at once; the step is always applied)
+__device__ __forceinline__ void adamw_with_recovery(
+    double loss, const double* grad, int64_t P, bool mse, double* __restrict__ params,
+    double* __restrict__ m, double* __restrict__ v2, double* __restrict__ opt, double beta1,
+    double beta2, double eps, double wd, int reset_lr, int apply_step, float* __restrict__ params32,
+    double* __restrict__ grads_out, double* __restrict__ loss_out, double* cand, int32_t* flags) {
+  if (threadIdx.x == 0 && loss_out) *loss_out = loss;
+  if (grads_out)
+    for (int64_t k = threadIdx.x; k < P; k += blockDim.x) grads_out[k] = grad[k];
+  if (!apply_step) return;
+  double lr = reset_lr ? opt[2] : opt[1];
+  if (!isfinite(loss)) {
+    // ism_loss_and_grad raises before the optimizer step; sbtm_update restores (a no-op),
+    // halves lr and retries the same (non-finite) loss until lr < 1e-12 -> RuntimeError.
+    // The MSE path (pretraining) raises straight away (ref: score.py:348-349).
+    if (threadIdx.x == 0) {
+      int halvings = 0;
+      if (!mse)
+        do {
+          lr *= 0.5;
+          ++halvings;
+        } while (!(lr < 1e-12));
+      atomicAdd(flags + SPIC_FLAG_LR_HALVINGS, halvings);
+      atomicOr(flags + SPIC_FLAG_TRAIN_FATAL, 1);
+      opt[1] = lr;
+    }
+    return;
+  }
+  double t = opt[0];
+  for (;;) {
+    t += 1.0;
+    const double bc1 = 1.0 - pow(beta1, t), bc2 = 1.0 - pow(beta2, t);
+    int ok = 1;
+    for (int64_t k = threadIdx.x; k < P; k += blockDim.x) {
+      double p = params[k];
+      if (wd != 0.0) p -= lr * wd * p;
+      const double gk = grad[k];
+      const double mk = beta1 * m[k] + (1.0 - beta1) * gk;
+      const double vk = beta2 * v2[k] + (1.0 - beta2) * gk * gk;
+      m[k] = mk;
+      v2[k] = vk;
+      p -= lr * (mk / bc1) / (sqrt(vk / bc2) + eps);
+      cand[k] = p;
+      ok &= isfinite(p) ? 1 : 0;
+    }
+    ok = __syncthreads_and(ok);
+    if (ok || mse) {
+      for (int64_t k = threadIdx.x; k < P; k += blockDim.x) {
+        params[k] = cand[k];
+        params32[k] = (float)cand[k];
+      }
+      break;
+    }
+    // restore (params untouched), halve, retry with the same gradient (ref: score.py:578-585)
+    lr *= 0.5;
+    if (threadIdx.x == 0) atomicAdd(flags + SPIC_FLAG_LR_HALVINGS, 1);
+    if (lr < 1e-12) {
+      if (threadIdx.x == 0) atomicOr(flags + SPIC_FLAG_TRAIN_FATAL, 1);
+      break;
+    }
+  }
+  if (threadIdx.x == 0) {
+    opt[0] = t;
+    opt[1] = lr;
+  }
+}
+
+}  // namespace spic

@@ -16,6 +16,7 @@
 // master parameters). Deterministic for a given (n, grid).
 #include <algorithm>
 
+#include "adamw.cuh"
 #include "common.cuh"
 #include "f32x2.cuh"
 
@@ -396,66 +397,8 @@ __global__ void __launch_bounds__(1024) k_sbtm_finalize(
     }
   }
   __syncthreads();
-  const double loss = g[0];
-  if (threadIdx.x == 0 && loss_out) *loss_out = loss;
-  if (grads_out)
-    for (int64_t k = threadIdx.x; k < P; k += blockDim.x) grads_out[k] = grad[k];
-  if (!apply_step) return;
-  double lr = reset_lr ? opt[2] : opt[1];
-  if (!isfinite(loss)) {
-    // ism_loss_and_grad raises before the optimizer step; sbtm_update restores (a no-op),
-    // halves lr and retries the same (non-finite) loss until lr < 1e-12 -> RuntimeError.
-    // The MSE path (pretraining) raises straight away (ref: score.py:348-349).
-    if (threadIdx.x == 0) {
-      int halvings = 0;
-      if (div_mode != 3)
-        do {
-          lr *= 0.5;
-          ++halvings;
-        } while (!(lr < 1e-12));
-      atomicAdd(flags + SPIC_FLAG_LR_HALVINGS, halvings);
-      atomicOr(flags + SPIC_FLAG_TRAIN_FATAL, 1);
-      opt[1] = lr;
-    }
-    return;
-  }
-  double t = opt[0];
-  for (;;) {
-    t += 1.0;
-    const double bc1 = 1.0 - pow(beta1, t), bc2 = 1.0 - pow(beta2, t);
-    int ok = 1;
-    for (int64_t k = threadIdx.x; k < P; k += blockDim.x) {
-      double p = params[k];
-      if (wd != 0.0) p -= lr * wd * p;
-      const double gk = grad[k];
-      const double mk = beta1 * m[k] + (1.0 - beta1) * gk;
-      const double vk = beta2 * v2[k] + (1.0 - beta2) * gk * gk;
-      m[k] = mk;
-      v2[k] = vk;
-      p -= lr * (mk / bc1) / (sqrt(vk / bc2) + eps);
-      cand[k] = p;
-      ok &= isfinite(p) ? 1 : 0;
-    }
-    ok = __syncthreads_and(ok);
-    if (ok || div_mode == 3) {
-      for (int64_t k = threadIdx.x; k < P; k += blockDim.x) {
-        params[k] = cand[k];
-        params32[k] = (float)cand[k];
-      }
-      break;
-    }
-    // restore (params untouched), halve, retry with the same gradient (ref: score.py:578-585)
-    lr *= 0.5;
-    if (threadIdx.x == 0) atomicAdd(flags + SPIC_FLAG_LR_HALVINGS, 1);
-    if (lr < 1e-12) {
-      if (threadIdx.x == 0) atomicOr(flags + SPIC_FLAG_TRAIN_FATAL, 1);
-      break;
-    }
-  }
-  if (threadIdx.x == 0) {
-    opt[0] = t;
-    opt[1] = lr;
-  }
+  adamw_with_recovery(g[0], grad, P, div_mode == 3, params, m, v2, opt, beta1, beta2, eps, wd,
+                      reset_lr, apply_step, params32, grads_out, loss_out, cand, flags);
 }
 
 // Deterministic column sums of the [rows][width] block partials into one row, one warp per

@@ -1,0 +1,496 @@
+// silu.cu — the BASELINE "2 x 128 SiLU" score network (M1) with
+// its hidden-layer GEMMs on the 5th-generation tensor cores (tcgen05, accumulators in TMEM).
+//
+// Network (u = [x/L, v], float32 working copy of float64 master parameters, flat order
+//   W1[H][4], b1[H], W2[H][H], b2[H], W3[3][H], b3[3]):
+//   a1 = W1 u + b1, h1 = silu(a1); a2 = W2 h1 + b2, h2 = silu(a2); s = W3 h2 + b3.
+// The ISM loss sum_p w_p (|s_p|^2 + 2 div_p) (ref: score.py:303-338 applied to this network)
+// needs the exact Jacobian trace, carried as three forward tangents t1_k = silu'(a1) W1[:,1+k]
+// per particle, and then the reverse sweep. Per chunk of 32 particles the CTA runs three
+// 128 x 128 x 128 GEMMs, each as split-BF16 (hi*hi + hi*lo + lo*hi, ~2^-16 relative) on
+// tcgen05 with float32 TMEM accumulation:
+//   G1  [a2 - b2 | c2_k]      = W2   . [h1 | t1_k]        (columns: 4 per particle)
+//   G2  [dh1 | dt1_k]         = W2^T . [da2 | dc2_k]
+//   G3  dW2                  += [da2 | dc2_k] . [h1 | t1_k]^T   (TMEM-resident across chunks)
+// Everything elementwise (SiLU and its first two derivatives, the W1/W3 layers, the s / div
+// reductions over h, per-particle loss terms) runs on the FP32 pipes with one thread per
+// hidden unit (the TMEM lane) and two warpgroups splitting the chunk's particles.
+// One persistent CTA per SM (192 KB of operand tiles + 384 TMEM columns); per-CTA float64
+// partial rows are reduced in a fixed order and finalized by the shared AdamW kernel.
+#include <algorithm>
+
+#include "adamw.cuh"
+#include "common.cuh"
+#include "pairs.cuh"
+#include "umma.cuh"
+
+namespace spic {
+
+__global__ void k_ism_reduce_cols(const double* __restrict__ part, int rows, int64_t width,
+                                  double* __restrict__ out);  // sbtm.cu
+
+namespace {
+
+constexpr int kH = 128;       // hidden width of the tensor-core path
+constexpr int kCP = 32;       // particles per chunk (GEMM N = 4 * kCP = 128)
+constexpr int kNT = 256;      // two warpgroups; thread = (hidden unit h, particle half)
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColD1 = 0, kColD2 = 128, kColD3 = 256;
+
+__host__ __device__ constexpr int64_t silu_params(int H) { return (int64_t)H * H + 9 * H + 3; }
+
+struct SiluShared {
+  float4 u[kCP];
+  float w[kCP];
+  float4 gs[kCP];              // (2w s, 2w)
+  float red[4][4 * kCP];       // per-warp-quarter partial (s0, s1, s2, div) per particle
+  uint64_t bar;
+  uint32_t tmem;
+};
+constexpr size_t kSiluSmem = 6 * umma::kTileBytes + sizeof(SiluShared) + 1024;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+}
+
+__device__ __forceinline__ float sigmoid(float a) { return fast_rcp(1.f + __expf(-a)); }
+
+// lane l ends with the warp-wide sum of v[l] (31 shuffles for 32 values)
+__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return v[0];
+}
+
+// ISM = false: forward only (scores into sw_out lanes 0..2, weight lane kept).
+template <bool ISM>
+__global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ params,
+                                                 const float4* __restrict__ xv,
+                                                 const float4* __restrict__ sw, int64_t n,
+                                                 float x_scale, float L,
+                                                 float4* __restrict__ sw_out,
+                                                 double* __restrict__ part) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* W2h = base;
+  uint8_t* W2l = base + 1 * umma::kTileBytes;
+  uint8_t* Xh = base + 2 * umma::kTileBytes;
+  uint8_t* Xl = base + 3 * umma::kTileBytes;
+  uint8_t* Yh = base + 4 * umma::kTileBytes;
+  uint8_t* Yl = base + 5 * umma::kTileBytes;
+  SiluShared& S = *reinterpret_cast<SiluShared*>(base + 6 * umma::kTileBytes);
+
+  const int tid = threadIdx.x, h = tid & (kH - 1), wg = tid >> 7, lane = tid & 31;
+  const int quarter = (tid >> 5) & 3;
+  const float* W1 = params;
+  const float* b1 = W1 + 4 * kH;
+  const float* W2 = b1 + kH;
+  const float* b2 = W2 + kH * kH;
+  const float* W3 = b2 + kH;
+  const float* b3 = W3 + 3 * kH;
+
+  for (int e = tid; e < kH * kH; e += kNT) umma::store_split(W2h, W2l, e / kH, e % kH, W2[e]);
+  float w1[4], w3[3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w1[i] = W1[h * 4 + i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) w3[k] = W3[k * kH + h];
+  const float bb1 = b1[h], bb2 = b2[h];
+  if (tid < 32) umma::tmem_alloc(&S.tmem, kTmemCols);
+  if (tid == 32) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tm = S.tmem;
+  const uint32_t tl = tm + ((uint32_t)(quarter * 32) << 16);  // this warp's TMEM lanes
+  const uint32_t sW2h = smem_u32(W2h), sW2l = smem_u32(W2l), sXh = smem_u32(Xh),
+                 sXl = smem_u32(Xl), sYh = smem_u32(Yh), sYl = smem_u32(Yl);
+
+  double gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
+  double loss = 0, gb3[3] = {0, 0, 0};
+  uint32_t phase = 0;
+  bool first = true;
+  const int64_t nchunks = (n + kCP - 1) / kCP;
+  const int p0 = 16 * wg;  // this thread's particle half
+
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    if (tid < kCP) {
+      const int64_t p = c * kCP + tid;
+      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+      float wt = 0.f;
+      if (p < n) {
+        const float4 A = xv[p];
+        const float x = A.x < 0.f ? A.x + L : A.x;  // % M quirk records carry x - L
+        u = make_float4(x * x_scale, A.y, A.z, A.w);
+        wt = sw[p].w;
+      }
+      S.u[tid] = u;
+      S.w[tid] = wt;
+    }
+    __syncthreads();
+
+    // F1: layer 1 and its tangents -> X = [h1 | t1_0 | t1_1 | t1_2] (rows 4p + j, column h)
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const int p = p0 + i;
+      const float4 u = S.u[p];
+      const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
+      const float sg = sigmoid(a);
+      const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
+      umma::store_split(Xh, Xl, 4 * p, h, a * sg);
+      umma::store_split(Xh, Xl, 4 * p + 1, h, d1 * w1[1]);
+      umma::store_split(Xh, Xl, 4 * p + 2, h, d1 * w1[2]);
+      umma::store_split(Xh, Xl, 4 * p + 3, h, d1 * w1[3]);
+    }
+    fence_proxy_async();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    if (tid == 0) {
+      umma::gemm_split<false, false>(tm + kColD1, sW2h, sW2l, sXh, sXl, false);
+      umma::commit(&S.bar);
+    }
+    umma::wait_mma(&S.bar, phase);
+    phase ^= 1;
+    umma::fence_after();
+
+    // F2a: s and div partials over this thread's h, reduced across the warp
+#pragma unroll 1
+    for (int g = 0; g < 2; ++g) {
+      float v[32];
+      umma::tmem_ld32(tl + kColD1 + (uint32_t)(4 * (p0 + 8 * g)), v);
+      float val[32];
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp) {
+        const float a2 = v[4 * pp] + bb2;
+        const float sg = sigmoid(a2);
+        const float h2 = a2 * sg;
+        const float d2 = sg * fmaf(a2, 1.f - sg, 1.f);
+        val[4 * pp + 0] = w3[0] * h2;
+        val[4 * pp + 1] = w3[1] * h2;
+        val[4 * pp + 2] = w3[2] * h2;
+        val[4 * pp + 3] =
+            d2 * fmaf(w3[2], v[4 * pp + 3], fmaf(w3[1], v[4 * pp + 2], w3[0] * v[4 * pp + 1]));
+      }
+      S.red[quarter][4 * (p0 + 8 * g) + lane] = transpose_reduce32(val, lane);
+    }
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    if (tid < kCP) {
+      const int p = tid;
+      float s[3], dv = 0.f;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        s[k] = b3[k] + ((S.red[0][4 * p + k] + S.red[1][4 * p + k]) +
+                        (S.red[2][4 * p + k] + S.red[3][4 * p + k]));
+      dv = (S.red[0][4 * p + 3] + S.red[1][4 * p + 3]) + (S.red[2][4 * p + 3] + S.red[3][4 * p + 3]);
+      const int64_t q = c * kCP + p;
+      if (!ISM) {
+        if (q < n) sw_out[q] = make_float4(s[0], s[1], s[2], sw[q].w);
+      } else {
+        const float wt = S.w[p], tw = 2.f * wt;
+        S.gs[p] = make_float4(tw * s[0], tw * s[1], tw * s[2], tw);
+        loss += (double)(wt * (s[0] * s[0] + s[1] * s[1] + s[2] * s[2] + 2.f * dv));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) gb3[k] += (double)(tw * s[k]);
+      }
+    }
+    if (!ISM) {
+      umma::fence_before();
+      __syncthreads();
+      umma::fence_after();
+      continue;
+    }
+    __syncthreads();
+
+    // F2b: reverse through layer 2 -> Y = [da2 | dc2_0 | dc2_1 | dc2_2]; dW3, db2
+    float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
+#pragma unroll 1
+    for (int g = 0; g < 2; ++g) {
+      float v[32];
+      umma::tmem_ld32(tl + kColD1 + (uint32_t)(4 * (p0 + 8 * g)), v);
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp) {
+        const int p = p0 + 8 * g + pp;
+        const float4 G = S.gs[p];
+        const float a2 = v[4 * pp] + bb2;
+        const float sg = sigmoid(a2);
+        const float h2 = a2 * sg;
+        const float d2 = sg * fmaf(a2, 1.f - sg, 1.f);
+        const float e2 = sg * (1.f - sg) * fmaf(a2, 1.f - 2.f * sg, 2.f);
+        const float c0 = v[4 * pp + 1], c1 = v[4 * pp + 2], c2 = v[4 * pp + 3];
+        const float dh2 = fmaf(w3[2], G.z, fmaf(w3[1], G.y, w3[0] * G.x));
+        const float qv = fmaf(w3[2], c2, fmaf(w3[1], c1, w3[0] * c0));
+        const float da2 = fmaf(d2, dh2, G.w * e2 * qv);
+        const float twd2 = G.w * d2;
+        aw3[0] += fmaf(G.x, h2, twd2 * c0);
+        aw3[1] += fmaf(G.y, h2, twd2 * c1);
+        aw3[2] += fmaf(G.z, h2, twd2 * c2);
+        ab2 += da2;
+        umma::store_split(Yh, Yl, 4 * p, h, da2);
+        umma::store_split(Yh, Yl, 4 * p + 1, h, twd2 * w3[0]);
+        umma::store_split(Yh, Yl, 4 * p + 2, h, twd2 * w3[1]);
+        umma::store_split(Yh, Yl, 4 * p + 3, h, twd2 * w3[2]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gw3[k] += (double)aw3[k];
+    gb2 += (double)ab2;
+    fence_proxy_async();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    if (tid == 0) {
+      umma::gemm_split<true, false>(tm + kColD2, sW2h, sW2l, sYh, sYl, false);  // W2^T Y
+      umma::gemm_split<true, true>(tm + kColD3, sYh, sYl, sXh, sXl, !first);     // Y^T X
+      umma::commit(&S.bar);
+    }
+    first = false;
+    umma::wait_mma(&S.bar, phase);
+    phase ^= 1;
+    umma::fence_after();
+
+    // F3: reverse through layer 1 -> dW1, db1
+    float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
+#pragma unroll 1
+    for (int g = 0; g < 2; ++g) {
+      float v[32];
+      umma::tmem_ld32(tl + kColD2 + (uint32_t)(4 * (p0 + 8 * g)), v);
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp) {
+        const float4 u = S.u[p0 + 8 * g + pp];
+        const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
+        const float sg = sigmoid(a);
+        const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
+        const float e1 = sg * (1.f - sg) * fmaf(a, 1.f - 2.f * sg, 2.f);
+        const float dh1 = v[4 * pp], t0 = v[4 * pp + 1], t1 = v[4 * pp + 2], t2 = v[4 * pp + 3];
+        const float da1 = fmaf(d1, dh1, e1 * fmaf(w1[3], t2, fmaf(w1[2], t1, w1[1] * t0)));
+        ab1 += da1;
+        aw1[0] += da1 * u.x;
+        aw1[1] += fmaf(da1, u.y, d1 * t0);
+        aw1[2] += fmaf(da1, u.z, d1 * t1);
+        aw1[3] += fmaf(da1, u.w, d1 * t2);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) gw1[i] += (double)aw1[i];
+    gb1 += (double)ab1;
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  }
+
+  if (ISM) {
+    const int64_t width = 1 + silu_params(kH);
+    const int64_t oW1 = 1, ob1 = oW1 + 4 * kH, oW2 = ob1 + kH, ob2 = oW2 + kH * kH,
+                  oW3 = ob2 + kH, ob3 = oW3 + 3 * kH;
+    double* row = part + (size_t)blockIdx.x * width;
+    // dW2 from TMEM (row h, columns h'); the two warpgroups take two column halves each
+#pragma unroll 1
+    for (int g = 2 * wg; g < 2 * wg + 2; ++g) {
+      float v[32];
+      umma::tmem_ld32(tl + kColD3 + (uint32_t)(32 * g), v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) row[oW2 + h * kH + 32 * g + i] = first ? 0.0 : (double)v[i];
+    }
+    double* comb = reinterpret_cast<double*>(Xh);  // operand tiles are free now
+    if (wg == 1) {
+      comb[h * 9 + 0] = gw1[0]; comb[h * 9 + 1] = gw1[1]; comb[h * 9 + 2] = gw1[2];
+      comb[h * 9 + 3] = gw1[3]; comb[h * 9 + 4] = gb1; comb[h * 9 + 5] = gb2;
+      comb[h * 9 + 6] = gw3[0]; comb[h * 9 + 7] = gw3[1]; comb[h * 9 + 8] = gw3[2];
+    }
+    __syncthreads();
+    if (wg == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) row[oW1 + 4 * h + i] = gw1[i] + comb[h * 9 + i];
+      row[ob1 + h] = gb1 + comb[h * 9 + 4];
+      row[ob2 + h] = gb2 + comb[h * 9 + 5];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) row[oW3 + k * kH + h] = gw3[k] + comb[h * 9 + 6 + k];
+    }
+    if (tid < 32) {
+      loss = warp_sum(loss);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gb3[k] = warp_sum(gb3[k]);
+      if (tid == 0) {
+        row[0] = loss;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) row[ob3 + k] = gb3[k];
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (tid < 32) umma::tmem_free(tm, kTmemCols);
+}
+
+// One-CTA check of the three GEMM shapes (operand views) against a host reference.
+// W, X, Y: float32 [128][128] row-major; D1 = W X^T, D2 = W^T Y^T, D3 = Y^T X.
+__global__ void __launch_bounds__(128, 1) k_umma_selftest(const float* __restrict__ W,
+                                                          const float* __restrict__ X,
+                                                          const float* __restrict__ Y,
+                                                          float* __restrict__ D1,
+                                                          float* __restrict__ D2,
+                                                          float* __restrict__ D3) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* T[6];
+  for (int i = 0; i < 6; ++i) T[i] = base + i * umma::kTileBytes;
+  SiluShared& S = *reinterpret_cast<SiluShared*>(base + 6 * umma::kTileBytes);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kH * kH; e += 128) {
+    umma::store_split(T[0], T[1], e / kH, e % kH, W[e]);
+    umma::store_split(T[2], T[3], e / kH, e % kH, X[e]);
+    umma::store_split(T[4], T[5], e / kH, e % kH, Y[e]);
+  }
+  if (tid < 32) umma::tmem_alloc(&S.tmem, kTmemCols);
+  if (tid == 32) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tm = S.tmem;
+  uint32_t s[6];
+  for (int i = 0; i < 6; ++i) s[i] = smem_u32(T[i]);
+  if (tid == 0) {
+    umma::gemm_split<false, false>(tm + kColD1, s[0], s[1], s[2], s[3], false);
+    umma::gemm_split<true, false>(tm + kColD2, s[0], s[1], s[4], s[5], false);
+    umma::gemm_split<true, true>(tm + kColD3, s[4], s[5], s[2], s[3], false);
+    umma::commit(&S.bar);
+  }
+  umma::wait_mma(&S.bar, 0);
+  umma::fence_after();
+  const uint32_t tl = tm + ((uint32_t)((tid >> 5) * 32) << 16);
+  for (int g = 0; g < 4; ++g) {
+    float v[32];
+    umma::tmem_ld32(tl + kColD1 + 32 * g, v);
+    for (int i = 0; i < 32; ++i) D1[tid * kH + 32 * g + i] = v[i];
+    umma::tmem_ld32(tl + kColD2 + 32 * g, v);
+    for (int i = 0; i < 32; ++i) D2[tid * kH + 32 * g + i] = v[i];
+    umma::tmem_ld32(tl + kColD3 + 32 * g, v);
+    for (int i = 0; i < 32; ++i) D3[tid * kH + 32 * g + i] = v[i];
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (tid < 32) umma::tmem_free(tm, kTmemCols);
+}
+
+int silu_blocks(int64_t n) {
+  const int64_t chunks = (n + kCP - 1) / kCP;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, kNumSMs));
+}
+
+}  // namespace
+
+// single-CTA finalize: the reduced row [loss, grads] -> AdamW with recovery
+__global__ void __launch_bounds__(1024) k_silu_finalize(
+    const double* __restrict__ row, int64_t P, double* __restrict__ params, double* __restrict__ m,
+    double* __restrict__ v2, double* __restrict__ opt, double beta1, double beta2, double eps,
+    double wd, int reset_lr, int apply_step, float* __restrict__ params32,
+    double* __restrict__ grads_out, double* __restrict__ loss_out, double* cand, int32_t* flags) {
+  adamw_with_recovery(row[0], row + 1, P, false, params, m, v2, opt, beta1, beta2, eps, wd,
+                      reset_lr, apply_step, params32, grads_out, loss_out, cand, flags);
+}
+
+}  // namespace spic
+
+using namespace spic;
+
+extern "C" int64_t spic_silu_num_params(int32_t H) { return silu_params(H); }
+
+extern "C" size_t spic_silu_scratch_bytes(int64_t n) {
+  // [blocks][1 + P] partials, the reduced row, candidate parameters
+  const size_t width = 1 + (size_t)silu_params(kH);
+  return sizeof(double) * ((size_t)(silu_blocks(n) + 1) * width + (size_t)silu_params(kH)) + 64;
+}
+
+extern "C" int64_t spic_silu_row_offset(int64_t n) {
+  return (int64_t)(sizeof(double) * (size_t)silu_blocks(n) * (1 + (size_t)silu_params(kH)));
+}
+
+static int silu_launch(bool ism, const float* params32, int32_t H, const float* xv,
+                       const float* sw, int64_t n, float x_scale, float* sw_out, double* part,
+                       cudaStream_t st) {
+  if (H != kH) return SPIC_ERR_UNSUPPORTED;
+  if (n < 1 || !xv || !sw || !(x_scale > 0.f)) return SPIC_ERR_ARG;
+  const int blocks = silu_blocks(n);
+  const float L = 1.0f / x_scale;
+  if (ism) {
+    cudaFuncSetAttribute(k_silu<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiluSmem);
+    k_silu<true><<<blocks, kNT, kSiluSmem, st>>>(params32, (const float4*)xv, (const float4*)sw, n,
+                                                 x_scale, L, nullptr, part);
+  } else {
+    cudaFuncSetAttribute(k_silu<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiluSmem);
+    k_silu<false><<<blocks, kNT, kSiluSmem, st>>>(params32, (const float4*)xv, (const float4*)sw, n,
+                                                  x_scale, L, (float4*)sw_out, nullptr);
+  }
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
+
+extern "C" int spic_silu_forward(const float* params32, int32_t H, const float* xv,
+                                 const float* sw, int64_t n, float x_scale, float* sw_out,
+                                 void* stream) {
+  if (!sw_out) return SPIC_ERR_ARG;
+  return silu_launch(false, params32, H, xv, sw, n, x_scale, sw_out, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int spic_silu_ism_partials(const float* params32, int32_t H, const float* xv,
+                                      const float* sw, int64_t n, float x_scale, void* scratch,
+                                      size_t scratch_bytes, void* stream) {
+  if (n >= 1 && scratch_bytes < spic_silu_scratch_bytes(n)) return SPIC_ERR_SCRATCH;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = silu_launch(true, params32, H, xv, sw, n, x_scale, nullptr, (double*)scratch, st);
+  if (rc != SPIC_OK) return rc;
+  const int blocks = silu_blocks(n);
+  const int64_t width = 1 + silu_params(kH);
+  double* part = (double*)scratch;
+  k_ism_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(part, blocks, width,
+                                                                 part + (size_t)blocks * width);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
+
+extern "C" int spic_silu_finalize(void* scratch, int64_t n, int32_t H, double* params64,
+                                  double* m, double* v2, double* opt_state, double beta1,
+                                  double beta2, double eps, double weight_decay, int32_t reset_lr,
+                                  int32_t apply_step, float* params32, double* grads_out,
+                                  double* loss_out, int32_t* flags, void* stream) {
+  if (H != kH) return SPIC_ERR_UNSUPPORTED;
+  if (n < 1) return SPIC_ERR_ARG;
+  const int64_t P = silu_params(kH);
+  double* row = (double*)((char*)scratch + spic_silu_row_offset(n));
+  k_silu_finalize<<<1, 1024, 0, (cudaStream_t)stream>>>(
+      row, P, params64, m, v2, opt_state, beta1, beta2, eps, weight_decay, reset_lr, apply_step,
+      params32, grads_out, loss_out, row + 1 + P, flags);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}
+
+extern "C" int spic_umma_selftest(const float* W, const float* X, const float* Y, float* D1,
+                                  float* D2, float* D3, void* stream) {
+  cudaFuncSetAttribute(k_umma_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kSiluSmem);
+  k_umma_selftest<<<1, 128, kSiluSmem, (cudaStream_t)stream>>>(W, X, Y, D1, D2, D3);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
+}

@@ -1,0 +1,143 @@
+// umma.cuh — tcgen05 (5th-gen tensor core) helpers for the 128x128 split-BF16 GEMMs of the
+// SiLU score network (silu.cu).
+//
+// Operand tiles are 128 x 128 bf16 in shared memory, SWIZZLE_128B: two 64-column halves of
+// 16 KB, row r at r*128 B inside a half, 16-B chunk index XOR (r & 7). One physical tile is
+// read either K-major (rows = M/N index, cols = K) or MN-major (rows = K, cols = M/N), so a
+// single copy of an activation block serves as a K-major B operand in one GEMM and an
+// MN-major A/B operand in the transposed GEMMs (the backward pass and the weight gradient).
+// Accumulators are float32 in TMEM (lane = M row, column = N).
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace spic {
+namespace umma {
+
+constexpr uint32_t kTileBytes = 32768;  // 128 x 128 bf16
+
+// byte offset of element (r, c) inside a tile
+__device__ __forceinline__ uint32_t tile_off(int r, int c) {
+  return (uint32_t)((c >> 6) * 16384 + r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4) + (c & 7) * 2);
+}
+
+// shared-memory matrix descriptor: start, leading/stride byte offsets, version 1 (sm_100),
+// layout type 2 = SWIZZLE_128B
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+// K-major view; K-step ks covers columns 16ks..16ks+15 (32 B inside a 128-B swizzle row)
+__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int ks) {
+  return sdesc(tile + (uint32_t)((ks >> 2) * 16384 + (ks & 3) * 32), 16, 1024);
+}
+// MN-major view; K-step ks covers rows 16ks..16ks+15; MN groups of 64 are the two halves
+__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int ks) {
+  return sdesc(tile + (uint32_t)(ks * 2048), 16384, 1024);
+}
+
+// instruction descriptor: kind::f16, A/B bf16, D f32, M = N = 128, operand majors
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t a_mn, uint32_t b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((128u >> 3) << 17) |
+         ((128u >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// D (+)= A * B over K = 128 with split-BF16 operands: Ahi*Bhi + Ahi*Blo + Alo*Bhi
+// (~2^-16 relative per product; float32 accumulation in TMEM). Issued by one thread.
+template <bool A_MN, bool B_MN>
+__device__ __forceinline__ void gemm_split(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
+                                           uint32_t b_hi, uint32_t b_lo, bool accumulate) {
+  constexpr uint32_t id = idesc_bf16(A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const uint64_t ah = A_MN ? desc_mn(a_hi, ks) : desc_k(a_hi, ks);
+    const uint64_t al = A_MN ? desc_mn(a_lo, ks) : desc_k(a_lo, ks);
+    const uint64_t bh = B_MN ? desc_mn(b_hi, ks) : desc_k(b_hi, ks);
+    const uint64_t bl = B_MN ? desc_mn(b_lo, ks) : desc_k(b_lo, ks);
+    mma(d_tmem, ah, bh, id, (accumulate || ks > 0) ? 1u : 0u);
+    mma(d_tmem, ah, bl, id, 1u);
+    mma(d_tmem, al, bh, id, 1u);
+  }
+}
+
+// mbarrier parity wait that traps (instead of hanging the GPU) if the MMA never completes
+__device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (spin > (1u << 24)) __trap();
+  }
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// TMEM allocation (whole warp) / release
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_free(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+
+// 32 consecutive float32 columns of this thread's TMEM lane (warp w reads lanes 32(w%4)..)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&f)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
+}
+
+// split x into bf16 hi + lo (x ~= hi + lo to ~2^-17 relative) and store both tiles
+__device__ __forceinline__ void store_split(uint8_t* hi_tile, uint8_t* lo_tile, int r, int c,
+                                            float x) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+  const uint32_t o = tile_off(r, c);
+  *reinterpret_cast<__nv_bfloat16*>(hi_tile + o) = h;
+  *reinterpret_cast<__nv_bfloat16*>(lo_tile + o) = l;
+}
+
+}  // namespace umma
+}  // namespace spic

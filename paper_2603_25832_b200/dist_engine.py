@@ -24,7 +24,7 @@ from .collision import CellIndex, auto_sub_cells, build_cell_index, landau_sorte
 from .config import DeviceOptions
 from .parallel import CellPartition, Comm
 from .pic import FIELD_NONE, FIELD_VML, FIELD_VPL, Grid, deposit_from_index, raise_for_flags
-from .score import BlobEstimator, SbtmEstimator, SbtmTrainer, blob_sorted
+from .score import BlobEstimator, SbtmEstimator, blob_sorted
 from .state import DiagnosticsRecord, FieldState, ParticleEnsemble, new_flags
 
 DIAG_W = 9
@@ -97,9 +97,7 @@ class DistSimulation:
         self.diag = torch.zeros(max_rows, DIAG_W, dtype=torch.float64, device=dev)
         self.trainer = None
         if isinstance(estimator, SbtmEstimator):
-            self.trainer = SbtmTrainer(estimator.net, estimator.optimizer, estimator.K,
-                                       estimator.L, estimator.divergence, estimator.rademacher,
-                                       estimator.rng)
+            self.trainer = estimator.make_trainer()
         self._epi, self._epi_n = _lib.scratch("epilogue", 8 * 2 * 148 * 5 + 64)
         self.time_collision = False
         self.collision_events: list = []

@@ -26,7 +26,7 @@ from . import _lib
 from .collision import CellIndex, auto_sub_cells, build_cell_index, landau_sorted
 from .config import DeviceOptions
 from .pic import FIELD_VML, FIELD_VPL, Grid, deposit_from_index, raise_for_flags
-from .score import BlobEstimator, SbtmEstimator, SbtmTrainer, blob_sorted
+from .score import BlobEstimator, SbtmEstimator, blob_sorted
 from .state import DiagnosticsRecord, FieldState, ParticleEnsemble, new_flags
 
 DIAG_W = 9
@@ -55,9 +55,7 @@ class Simulation:
         self.diag = torch.zeros(max_rows, DIAG_W, dtype=torch.float64, device=dev)
         self.trainer = None
         if isinstance(estimator, SbtmEstimator):
-            self.trainer = SbtmTrainer(estimator.net, estimator.optimizer, estimator.K,
-                                       estimator.L, estimator.divergence, estimator.rademacher,
-                                       estimator.rng)
+            self.trainer = estimator.make_trainer()
         # optional CUDA-event brackets around the pair kernel (bench instrumentation)
         self.time_collision = False
         self.collision_events: list = []

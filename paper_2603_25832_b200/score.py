@@ -482,6 +482,11 @@ class SbtmEstimator:
         self.optimizer = AdamW(lr=lr, weight_decay=weight_decay, device=net.params64.device)
         self.warnings: list[str] = []
 
+    def make_trainer(self) -> SbtmTrainer:
+        """The device training loop the step engines drive."""
+        return SbtmTrainer(self.net, self.optimizer, self.K, self.L, self.divergence,
+                           self.rademacher, self.rng)
+
     def estimate(self, particles: ParticleEnsemble, cell_index=None) -> torch.Tensor:
         xn = (particles.x.double() / self.L).float()
         return mlp_forward(self.net, xn, particles.v)

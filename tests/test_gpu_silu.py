@@ -1,0 +1,199 @@
+"""GPU parity of the SiLU score network (extension M1, tcgen05 split-BF16 hidden GEMMs)
+against the float64 oracle (oracle/silu_oracle.py, itself pinned to torch autograd).
+
+Tolerances (stated; there is no reference implementation of this network): the split-BF16
+products are accurate to ~2^-16 relative with float32 accumulation, so
+  * raw GEMM self-test: max |err| <= 3e-5 * max |ref|;
+  * scores: relative L2 <= 1e-4 and per particle |err| <= 1e-4 * max |ref|;
+  * ISM loss <= 1e-4 relative, gradients <= 1e-4 relative L2 per parameter tensor;
+  * network outputs after K AdamW steps: relative L2 <= 1e-4.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import silu_oracle as so  # noqa: E402
+
+H = 128
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2603_25832_b200 import _lib
+
+    _lib.load()
+    return _lib
+
+
+def relL2(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _params(seed=0, bias=0.3):
+    rng = np.random.default_rng(seed)
+    p = so.glorot(H, rng)
+    p[4 * H:5 * H] = rng.normal(0, bias, H)
+    p[5 * H + H * H:6 * H + H * H] = rng.normal(0, bias, H)
+    p[-3:] = rng.normal(0, bias, 3)
+    return p.astype(np.float32).astype(np.float64)  # the kernels read the float32 copy
+
+
+def _ensemble(n, L, seed=1):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    v = rng.normal(0, 1.0, (n, 3)).astype(np.float32).astype(np.float64)
+    w = np.full(n, L / n, dtype=np.float32).astype(np.float64)
+    return x, v, w
+
+
+def _net(params):
+    from paper_2603_25832_b200.silu_net import SiluScoreNet
+
+    net = SiluScoreNet()
+    net.set_flat(params)
+    return net
+
+
+def test_umma_selftest_all_operand_views(lib):
+    rng = np.random.default_rng(0)
+    W, X, Y = (torch.tensor(rng.normal(size=(H, H)), dtype=torch.float32, device="cuda")
+               for _ in range(3))
+    D = [torch.empty(H, H, dtype=torch.float32, device="cuda") for _ in range(3)]
+    lib.call("spic_umma_selftest", *(lib.ptr(t) for t in (W, X, Y, *D)), lib.stream_handle())
+    torch.cuda.synchronize()
+    Wd, Xd, Yd = W.double(), X.double(), Y.double()
+    refs = [Wd @ Xd.T, Wd.T @ Yd.T, Yd.T @ Xd]
+    for name, got, ref in zip(("W X^T", "W^T Y^T", "Y^T X"), D, refs):
+        err = float((got.double() - ref).abs().max() / ref.abs().max())
+        assert err <= 3e-5, (name, err)
+
+
+@pytest.mark.parametrize("n", [1, 31, 1000, 148 * 32 * 2 + 7])
+def test_silu_forward_matches_oracle(lib, n):
+    from paper_2603_25832_b200.silu_net import silu_forward
+
+    L = 4 * math.pi
+    params = _params()
+    x, v, _ = _ensemble(n, L)
+    s = silu_forward(_net(params), x, v, L).cpu().numpy()
+    ref, _ = so.forward(params, so.inputs(x, v, L), H)
+    assert relL2(s, ref) <= 1e-4
+    assert np.max(np.abs(s - ref)) <= 1e-4 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("n", [5, 4099, 148 * 32 * 3 + 11])
+def test_silu_ism_loss_and_grad_matches_oracle(lib, n):
+    from paper_2603_25832_b200.silu_net import silu_ism_loss_and_grad
+
+    L = 4 * math.pi
+    params = _params(seed=n)
+    x, v, w = _ensemble(n, L, seed=n + 1)
+    net = _net(params)
+    loss, g = silu_ism_loss_and_grad(net, x, v, w, L)
+    g = g.cpu().numpy()
+    ref_loss, ref_g = so.ism_loss_and_grad(params, so.inputs(x, v, L), w, H)
+    assert abs(loss - ref_loss) <= 1e-4 * abs(ref_loss)
+    for (a, b, _), name in zip(net._slices(), ("W1", "b1", "W2", "b2", "W3", "b3")):
+        assert relL2(g[a:b], ref_g[a:b]) <= 1e-4, (name, relL2(g[a:b], ref_g[a:b]))
+
+
+def test_silu_sorted_records_quirk_and_weights(lib):
+    """Record inputs: x' = x - L (the %M quirk record) maps back to x; per-particle weights."""
+    from paper_2603_25832_b200 import _lib
+    from paper_2603_25832_b200.silu_net import _silu_finalize, _silu_partials, records
+    from paper_2603_25832_b200.score import AdamW
+
+    n, L = 700, 10 * math.pi
+    params = _params(seed=5)
+    x, v, _ = _ensemble(n, L, seed=6)
+    w = np.random.default_rng(7).uniform(0.2, 2.0, n).astype(np.float32).astype(np.float64)
+    net = _net(params)
+    xv, sw = records(x, v, w, L, torch.device("cuda"))
+    xv[::7, 0] -= L  # quirk records
+    buf = _silu_partials(net, xv, sw, n, L)
+    g = torch.empty(net.n_params, dtype=torch.float64, device="cuda")
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    _silu_finalize(net, buf, n, AdamW(device="cuda"), grads_out=g, loss_out=loss)
+    ref_loss, ref_g = so.ism_loss_and_grad(params, so.inputs(x, v, L), w, H)
+    assert abs(float(loss.item()) - ref_loss) <= 1e-4 * abs(ref_loss)
+    assert relL2(g.cpu().numpy(), ref_g) <= 1e-4
+    out = sw.clone()
+    _lib.call("spic_silu_forward", _lib.ptr(net.params32), H, _lib.ptr(xv), _lib.ptr(sw), n,
+              float(1 / L), _lib.ptr(out), _lib.stream_handle())
+    s_ref, _ = so.forward(params, so.inputs(x, v, L), H)
+    assert relL2(out[:, :3].cpu().numpy(), s_ref) <= 1e-4
+    np.testing.assert_array_equal(out[:, 3].cpu().numpy(), sw[:, 3].cpu().numpy())
+
+
+def test_silu_trainer_k_steps_matches_oracle_adamw(lib):
+    from paper_2603_25832_b200.score import AdamW
+    from paper_2603_25832_b200.silu_net import SiluTrainer, silu_forward
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    n, L, K, lr = 3000, 4 * math.pi, 4, 1e-3
+    params = _params(seed=9)
+    x, v, w = _ensemble(n, L, seed=10)
+    net = _net(params)
+    p = ParticleEnsemble.from_arrays(x, v, w)
+    tr = SiluTrainer(net, AdamW(lr=lr, weight_decay=0.0, device="cuda"), K, L)
+    tr.run(n, particles=p)
+    u = so.inputs(x, v, L)
+    P = params.copy()
+    m = np.zeros_like(P)
+    v2 = np.zeros_like(P)
+    losses = []
+    for t in range(1, K + 1):
+        loss, g = so.ism_loss_and_grad(P, u, w, H)
+        losses.append(loss)
+        P, m, v2 = so.adamw_step(P, g, m, v2, t, lr)
+    np.testing.assert_allclose(tr.losses[:K].cpu().numpy(), losses, rtol=1e-4)
+    s_dev = silu_forward(net, x, v, L).cpu().numpy()
+    s_ref, _ = so.forward(P, u, H)
+    assert relL2(s_dev, s_ref) <= 1e-4
+
+
+def test_engine_step_with_silu_estimator_and_graph(lib):
+    """Config-0-shaped engine steps with the SiLU estimator: collisions conserve momentum,
+    the captured CUDA graph reproduces the eager step bit for bit."""
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
+    from paper_2603_25832_b200.silu_net import SiluEstimator, SiluScoreNet
+    from paper_2603_25832_b200.state import FieldState, ParticleEnsemble
+
+    n, M, L = 20000, 32, 4 * math.pi
+    x, v, w = _ensemble(n, L, seed=12)
+    grid = Grid(M, L / M)
+
+    def make():
+        p = ParticleEnsemble.from_arrays(x, v, w)
+        rho, _ = deposit(p, grid)
+        rho_ion = float(rho.sum()) * grid.eta / L
+        f = FieldState.zeros(M, 3, rho_ion)
+        f.E1.copy_(poisson_solve(rho, rho_ion, grid))
+        r = np.random.default_rng(3)
+        net = SiluScoreNet.init_glorot(r)
+        est = SiluEstimator(net, L, 3, r, lr=1e-3, weight_decay=0.0)
+        return Simulation(p, f, grid, dt=0.05, nu=0.1, mode="VPL", gamma=-3.0, estimator=est,
+                          max_rows=8), p
+
+    a, pa = make()
+    b, pb = make()
+    for k in range(1, 4):
+        a.step(k)
+    b.step(1)
+    b.capture(2)
+    b.replay(2)
+    b.replay(3)
+    torch.cuda.synchronize()
+    assert torch.equal(pa.x, pb.x) and torch.equal(pa.vp, pb.vp)
+    d = a.diag.cpu().numpy()
+    assert np.all(np.isfinite(d[1:4]))
+    a.check()
