@@ -33,7 +33,9 @@ namespace {
 
 constexpr int kH = 128;       // hidden width of the tensor-core path
 constexpr int kCP = 32;       // particles per chunk (GEMM N = 4 * kCP = 128)
-constexpr int kNT = 256;      // two warpgroups; thread = (hidden unit h, particle half)
+constexpr int kNWG = 4;       // warpgroups per CTA; thread = (hidden unit h, particle slice)
+constexpr int kNT = 128 * kNWG;
+constexpr int kPPT = kCP / kNWG;  // particles per thread per chunk
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColD1 = 0, kColD2 = 128, kColD3 = 256;
 
@@ -44,7 +46,7 @@ struct SiluShared {
   float w[kCP];
   float4 gs[kCP];              // (2w s, 2w)
   float red[4][4 * kCP];       // per-warp-quarter partial (s0, s1, s2, div) per particle
-  uint64_t bar;
+  uint64_t bar[1];
   uint32_t tmem;
 };
 constexpr size_t kSiluSmem = 6 * umma::kTileBytes + sizeof(SiluShared) + 1024;
@@ -70,6 +72,25 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
   return v[0];
 }
 
+// Split-BF16 store of one value into a hi tile (at addr) and its lo tile (addr + 32 KB).
+// addr = the thread's column base for the row's (r & 7) swizzle phase + r * 128; with the
+// particle loops unrolled the row part is a constant that folds into the STS immediate.
+__device__ __forceinline__ void st_split(uint32_t addr, float x) {
+  asm volatile(
+      "{\n.reg .b16 h16, l16, z16;\n.reg .b32 hf;\n.reg .f32 r;\n"
+      "mov.b16 z16, 0;\n"
+      "cvt.rn.bf16.f32 h16, %1;\n"
+      "mov.b32 hf, {z16, h16};\n"
+      "sub.rn.f32 r, %1, hf;\n"
+      "cvt.rn.bf16.f32 l16, r;\n"
+      "st.shared.b16 [%0], h16;\n"
+      "st.shared.b16 [%0+32768], l16;\n}\n" ::"r"(addr),
+      "f"(x)
+      : "memory");
+}
+
+// One CTA per SM, four warpgroups. Thread (h, warpgroup g) owns hidden unit h (its TMEM lane)
+// for particles 8g..8g+7 of each 32-particle chunk; one thread issues the CTA's GEMMs.
 // ISM = false: forward only (scores into sw_out lanes 0..2, weight lane kept).
 template <bool ISM>
 __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ params,
@@ -87,6 +108,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   uint8_t* Yh = base + 4 * umma::kTileBytes;
   uint8_t* Yl = base + 5 * umma::kTileBytes;
   SiluShared& S = *reinterpret_cast<SiluShared*>(base + 6 * umma::kTileBytes);
+  constexpr int kY = 2 * (int)umma::kTileBytes;  // Y tiles sit 64 KB after the X tiles
 
   const int tid = threadIdx.x, h = tid & (kH - 1), wg = tid >> 7, lane = tid & 31;
   const int quarter = (tid >> 5) & 3;
@@ -106,9 +128,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const float bb1 = b1[h], bb2 = b2[h];
   if (tid < 32) umma::tmem_alloc(&S.tmem, kTmemCols);
   if (tid == 32) {
-    mbar_init(&S.bar, 1);
+    mbar_init(&S.bar[0], 1);
     fence_barrier_init();
   }
+  fence_proxy_async();
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
@@ -116,13 +139,22 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const uint32_t tl = tm + ((uint32_t)(quarter * 32) << 16);  // this warp's TMEM lanes
   const uint32_t sW2h = smem_u32(W2h), sW2l = smem_u32(W2l), sXh = smem_u32(Xh),
                  sXl = smem_u32(Xl), sYh = smem_u32(Yh), sYl = smem_u32(Yl);
+  // store bases for this thread's column h and its rows 32g + (0..31), one per (row & 7)
+  uint32_t rb[8];
+  {
+    const uint32_t col = sXh + (uint32_t)((h >> 6) * 16384 + (h & 7) * 2 + 4096 * wg);
+    const int hc = (h >> 3) & 7;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) rb[m] = col + (uint32_t)((hc ^ m) << 4);
+  }
 
   double gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
   double loss = 0, gb3[3] = {0, 0, 0};
   uint32_t phase = 0;
   bool first = true;
   const int64_t nchunks = (n + kCP - 1) / kCP;
-  const int p0 = 16 * wg;  // this thread's particle half
+  const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk
+  const uint32_t c0 = 4 * p0;  // ... and their first GEMM column
 
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     if (tid < kCP) {
@@ -141,17 +173,16 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     __syncthreads();
 
     // F1: layer 1 and its tangents -> X = [h1 | t1_0 | t1_1 | t1_2] (rows 4p + j, column h)
-#pragma unroll 4
-    for (int i = 0; i < 16; ++i) {
-      const int p = p0 + i;
-      const float4 u = S.u[p];
+#pragma unroll
+    for (int i = 0; i < kPPT; ++i) {
+      const float4 u = S.u[p0 + i];
       const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
       const float sg = sigmoid(a);
       const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
-      umma::store_split(Xh, Xl, 4 * p, h, a * sg);
-      umma::store_split(Xh, Xl, 4 * p + 1, h, d1 * w1[1]);
-      umma::store_split(Xh, Xl, 4 * p + 2, h, d1 * w1[2]);
-      umma::store_split(Xh, Xl, 4 * p + 3, h, d1 * w1[3]);
+      st_split(rb[(4 * i + 0) & 7] + ((4 * i + 0) * 128), a * sg);
+      st_split(rb[(4 * i + 1) & 7] + ((4 * i + 1) * 128), d1 * w1[1]);
+      st_split(rb[(4 * i + 2) & 7] + ((4 * i + 2) * 128), d1 * w1[2]);
+      st_split(rb[(4 * i + 3) & 7] + ((4 * i + 3) * 128), d1 * w1[3]);
     }
     fence_proxy_async();
     umma::fence_before();
@@ -159,20 +190,19 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     umma::fence_after();
     if (tid == 0) {
       umma::gemm_split<false, false>(tm + kColD1, sW2h, sW2l, sXh, sXl, false);
-      umma::commit(&S.bar);
+      umma::commit(&S.bar[0]);
     }
-    umma::wait_mma(&S.bar, phase);
+    umma::wait_mma(&S.bar[0], phase);
     phase ^= 1;
     umma::fence_after();
 
     // F2a: s and div partials over this thread's h, reduced across the warp
-#pragma unroll 1
-    for (int g = 0; g < 2; ++g) {
+    {
       float v[32];
-      umma::tmem_ld32(tl + kColD1 + (uint32_t)(4 * (p0 + 8 * g)), v);
+      umma::tmem_ld32(tl + kColD1 + c0, v);
       float val[32];
 #pragma unroll
-      for (int pp = 0; pp < 8; ++pp) {
+      for (int pp = 0; pp < kPPT; ++pp) {
         const float a2 = v[4 * pp] + bb2;
         const float sg = sigmoid(a2);
         const float h2 = a2 * sg;
@@ -183,7 +213,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         val[4 * pp + 3] =
             d2 * fmaf(w3[2], v[4 * pp + 3], fmaf(w3[1], v[4 * pp + 2], w3[0] * v[4 * pp + 1]));
       }
-      S.red[quarter][4 * (p0 + 8 * g) + lane] = transpose_reduce32(val, lane);
+      S.red[quarter][c0 + lane] = transpose_reduce32(val, lane);
     }
     umma::fence_before();
     __syncthreads();
@@ -216,38 +246,36 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     __syncthreads();
 
     // F2b: reverse through layer 2 -> Y = [da2 | dc2_0 | dc2_1 | dc2_2]; dW3, db2
-    float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
-#pragma unroll 1
-    for (int g = 0; g < 2; ++g) {
+    {
+      float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
       float v[32];
-      umma::tmem_ld32(tl + kColD1 + (uint32_t)(4 * (p0 + 8 * g)), v);
+      umma::tmem_ld32(tl + kColD1 + c0, v);
 #pragma unroll
-      for (int pp = 0; pp < 8; ++pp) {
-        const int p = p0 + 8 * g + pp;
-        const float4 G = S.gs[p];
+      for (int pp = 0; pp < kPPT; ++pp) {
+        const float4 G = S.gs[p0 + pp];
         const float a2 = v[4 * pp] + bb2;
         const float sg = sigmoid(a2);
         const float h2 = a2 * sg;
         const float d2 = sg * fmaf(a2, 1.f - sg, 1.f);
         const float e2 = sg * (1.f - sg) * fmaf(a2, 1.f - 2.f * sg, 2.f);
-        const float c0 = v[4 * pp + 1], c1 = v[4 * pp + 2], c2 = v[4 * pp + 3];
+        const float cc0 = v[4 * pp + 1], cc1 = v[4 * pp + 2], cc2 = v[4 * pp + 3];
         const float dh2 = fmaf(w3[2], G.z, fmaf(w3[1], G.y, w3[0] * G.x));
-        const float qv = fmaf(w3[2], c2, fmaf(w3[1], c1, w3[0] * c0));
+        const float qv = fmaf(w3[2], cc2, fmaf(w3[1], cc1, w3[0] * cc0));
         const float da2 = fmaf(d2, dh2, G.w * e2 * qv);
         const float twd2 = G.w * d2;
-        aw3[0] += fmaf(G.x, h2, twd2 * c0);
-        aw3[1] += fmaf(G.y, h2, twd2 * c1);
-        aw3[2] += fmaf(G.z, h2, twd2 * c2);
+        aw3[0] += fmaf(G.x, h2, twd2 * cc0);
+        aw3[1] += fmaf(G.y, h2, twd2 * cc1);
+        aw3[2] += fmaf(G.z, h2, twd2 * cc2);
         ab2 += da2;
-        umma::store_split(Yh, Yl, 4 * p, h, da2);
-        umma::store_split(Yh, Yl, 4 * p + 1, h, twd2 * w3[0]);
-        umma::store_split(Yh, Yl, 4 * p + 2, h, twd2 * w3[1]);
-        umma::store_split(Yh, Yl, 4 * p + 3, h, twd2 * w3[2]);
+        st_split(rb[(4 * pp + 0) & 7] + (kY + (4 * pp + 0) * 128), da2);
+        st_split(rb[(4 * pp + 1) & 7] + (kY + (4 * pp + 1) * 128), twd2 * w3[0]);
+        st_split(rb[(4 * pp + 2) & 7] + (kY + (4 * pp + 2) * 128), twd2 * w3[1]);
+        st_split(rb[(4 * pp + 3) & 7] + (kY + (4 * pp + 3) * 128), twd2 * w3[2]);
       }
-    }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) gw3[k] += (double)aw3[k];
-    gb2 += (double)ab2;
+      for (int k = 0; k < 3; ++k) gw3[k] += (double)aw3[k];
+      gb2 += (double)ab2;
+    }
     fence_proxy_async();
     umma::fence_before();
     __syncthreads();
@@ -255,22 +283,21 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     if (tid == 0) {
       umma::gemm_split<true, false>(tm + kColD2, sW2h, sW2l, sYh, sYl, false);  // W2^T Y
       umma::gemm_split<true, true>(tm + kColD3, sYh, sYl, sXh, sXl, !first);     // Y^T X
-      umma::commit(&S.bar);
+      umma::commit(&S.bar[0]);
     }
     first = false;
-    umma::wait_mma(&S.bar, phase);
+    umma::wait_mma(&S.bar[0], phase);
     phase ^= 1;
     umma::fence_after();
 
     // F3: reverse through layer 1 -> dW1, db1
-    float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
-#pragma unroll 1
-    for (int g = 0; g < 2; ++g) {
+    {
+      float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
       float v[32];
-      umma::tmem_ld32(tl + kColD2 + (uint32_t)(4 * (p0 + 8 * g)), v);
+      umma::tmem_ld32(tl + kColD2 + c0, v);
 #pragma unroll
-      for (int pp = 0; pp < 8; ++pp) {
-        const float4 u = S.u[p0 + 8 * g + pp];
+      for (int pp = 0; pp < kPPT; ++pp) {
+        const float4 u = S.u[p0 + pp];
         const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
         const float sg = sigmoid(a);
         const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
@@ -283,10 +310,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         aw1[2] += fmaf(da1, u.z, d1 * t1);
         aw1[3] += fmaf(da1, u.w, d1 * t2);
       }
-    }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) gw1[i] += (double)aw1[i];
-    gb1 += (double)ab1;
+      for (int i = 0; i < 4; ++i) gw1[i] += (double)aw1[i];
+      gb1 += (double)ab1;
+    }
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
@@ -297,28 +324,31 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     const int64_t oW1 = 1, ob1 = oW1 + 4 * kH, oW2 = ob1 + kH, ob2 = oW2 + kH * kH,
                   oW3 = ob2 + kH, ob3 = oW3 + 3 * kH;
     double* row = part + (size_t)blockIdx.x * width;
-    // dW2 from TMEM (row h, columns h'); the two warpgroups take two column halves each
-#pragma unroll 1
-    for (int g = 2 * wg; g < 2 * wg + 2; ++g) {
+    // dW2 from TMEM (row h, columns h'); warpgroup g takes columns 32g..32g+31
+    {
       float v[32];
-      umma::tmem_ld32(tl + kColD3 + (uint32_t)(32 * g), v);
+      umma::tmem_ld32(tl + kColD3 + (uint32_t)(32 * wg), v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) row[oW2 + h * kH + 32 * g + i] = first ? 0.0 : (double)v[i];
+      for (int i = 0; i < 32; ++i) row[oW2 + h * kH + 32 * wg + i] = first ? 0.0 : (double)v[i];
     }
-    double* comb = reinterpret_cast<double*>(Xh);  // operand tiles are free now
-    if (wg == 1) {
-      comb[h * 9 + 0] = gw1[0]; comb[h * 9 + 1] = gw1[1]; comb[h * 9 + 2] = gw1[2];
-      comb[h * 9 + 3] = gw1[3]; comb[h * 9 + 4] = gb1; comb[h * 9 + 5] = gb2;
-      comb[h * 9 + 6] = gw3[0]; comb[h * 9 + 7] = gw3[1]; comb[h * 9 + 8] = gw3[2];
-    }
+    // per-h sums over the four warpgroups in a fixed order (operand tiles are free now)
+    double* comb = reinterpret_cast<double*>(Xh);  // [4][kH][9]
+    double* mine = comb + (size_t)(wg * kH + h) * 9;
+    mine[0] = gw1[0]; mine[1] = gw1[1]; mine[2] = gw1[2]; mine[3] = gw1[3];
+    mine[4] = gb1; mine[5] = gb2; mine[6] = gw3[0]; mine[7] = gw3[1]; mine[8] = gw3[2];
     __syncthreads();
     if (wg == 0) {
+      double t[9];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) row[oW1 + 4 * h + i] = gw1[i] + comb[h * 9 + i];
-      row[ob1 + h] = gb1 + comb[h * 9 + 4];
-      row[ob2 + h] = gb2 + comb[h * 9 + 5];
+      for (int k = 0; k < 9; ++k)
+        t[k] = (comb[(0 * kH + h) * 9 + k] + comb[(1 * kH + h) * 9 + k]) +
+               (comb[(2 * kH + h) * 9 + k] + comb[(3 * kH + h) * 9 + k]);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) row[oW3 + k * kH + h] = gw3[k] + comb[h * 9 + 6 + k];
+      for (int i = 0; i < 4; ++i) row[oW1 + 4 * h + i] = t[i];
+      row[ob1 + h] = t[4];
+      row[ob2 + h] = t[5];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) row[oW3 + k * kH + h] = t[6 + k];
     }
     if (tid < 32) {
       loss = warp_sum(loss);
@@ -357,7 +387,7 @@ __global__ void __launch_bounds__(128, 1) k_umma_selftest(const float* __restric
   }
   if (tid < 32) umma::tmem_alloc(&S.tmem, kTmemCols);
   if (tid == 32) {
-    mbar_init(&S.bar, 1);
+    mbar_init(&S.bar[0], 1);
     fence_barrier_init();
   }
   fence_proxy_async();
@@ -371,9 +401,9 @@ __global__ void __launch_bounds__(128, 1) k_umma_selftest(const float* __restric
     umma::gemm_split<false, false>(tm + kColD1, s[0], s[1], s[2], s[3], false);
     umma::gemm_split<true, false>(tm + kColD2, s[0], s[1], s[4], s[5], false);
     umma::gemm_split<true, true>(tm + kColD3, s[4], s[5], s[2], s[3], false);
-    umma::commit(&S.bar);
+    umma::commit(&S.bar[0]);
   }
-  umma::wait_mma(&S.bar, 0);
+  umma::wait_mma(&S.bar[0], 0);
   umma::fence_after();
   const uint32_t tl = tm + ((uint32_t)((tid >> 5) * 32) << 16);
   for (int g = 0; g < 4; ++g) {
@@ -458,11 +488,11 @@ extern "C" int spic_silu_ism_partials(const float* params32, int32_t H, const fl
   cudaStream_t st = (cudaStream_t)stream;
   int rc = silu_launch(true, params32, H, xv, sw, n, x_scale, nullptr, (double*)scratch, st);
   if (rc != SPIC_OK) return rc;
-  const int blocks = silu_blocks(n);
+  const int rows = silu_blocks(n);
   const int64_t width = 1 + silu_params(kH);
   double* part = (double*)scratch;
-  k_ism_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(part, blocks, width,
-                                                                 part + (size_t)blocks * width);
+  k_ism_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(part, rows, width,
+                                                                 part + (size_t)rows * width);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;

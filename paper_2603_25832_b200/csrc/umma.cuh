@@ -36,9 +36,9 @@ __device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int ks) {
   return sdesc(tile + (uint32_t)(ks * 2048), 16384, 1024);
 }
 
-// instruction descriptor: kind::f16, A/B bf16, D f32, M = N = 128, operand majors
-__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t a_mn, uint32_t b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((128u >> 3) << 17) |
+// instruction descriptor: kind::f16, A/B bf16, D f32, M = 128, N, operand majors
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t a_mn, uint32_t b_mn, uint32_t N = 128) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) |
          ((128u >> 4) << 24);
 }
 
@@ -50,14 +50,15 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-// D (+)= A * B over K = 128 with split-BF16 operands: Ahi*Bhi + Ahi*Blo + Alo*Bhi
-// (~2^-16 relative per product; float32 accumulation in TMEM). Issued by one thread.
-template <bool A_MN, bool B_MN>
+// D[128 x N] (+)= A * B over K = 16 * KSTEPS with split-BF16 operands:
+// Ahi*Bhi + Ahi*Blo + Alo*Bhi (~2^-16 relative per product; float32 accumulation in TMEM).
+// Operand addresses are tile (sub-)block starts. Issued by one thread.
+template <bool A_MN, bool B_MN, int N = 128, int KSTEPS = 8>
 __device__ __forceinline__ void gemm_split(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
                                            uint32_t b_hi, uint32_t b_lo, bool accumulate) {
-  constexpr uint32_t id = idesc_bf16(A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+  constexpr uint32_t id = idesc_bf16(A_MN ? 1u : 0u, B_MN ? 1u : 0u, (uint32_t)N);
 #pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
+  for (int ks = 0; ks < KSTEPS; ++ks) {
     const uint64_t ah = A_MN ? desc_mn(a_hi, ks) : desc_k(a_hi, ks);
     const uint64_t al = A_MN ? desc_mn(a_lo, ks) : desc_k(a_lo, ks);
     const uint64_t bh = B_MN ? desc_mn(b_hi, ks) : desc_k(b_hi, ks);

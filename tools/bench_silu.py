@@ -29,12 +29,14 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--sizes", default="65536,1048576")
     args = ap.parse_args()
     _lib.load(build_if_missing=False)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     bf16_peak = float(peaks["bf16_tflops"])
     dev = torch.device("cuda", 0)
-    for n, L in ((65536, 4 * math.pi), (1 << 20, 10 * math.pi)):
+    for n in (int(a) for a in args.sizes.split(",")):
+        L = 4 * math.pi if n <= 65536 else 10 * math.pi
         rng = np.random.default_rng(0)
         net = SiluScoreNet.init_glorot(rng, device=dev)
         x = rng.uniform(0, L, n)
