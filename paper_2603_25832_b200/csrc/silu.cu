@@ -46,7 +46,7 @@ struct SiluShared {
   float w[kCP];
   float4 gs[kCP];              // (2w s, 2w)
   float red[4][4 * kCP];       // per-warp-quarter partial (s0, s1, s2, div) per particle
-  uint64_t bar[1];
+  uint64_t bar[2];  // [0]: G1 / G2 done, [1]: G3 done (X, Y free again)
   uint32_t tmem;
 };
 constexpr size_t kSiluSmem = 6 * umma::kTileBytes + sizeof(SiluShared) + 1024;
@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   if (tid < 32) umma::tmem_alloc(&S.tmem, kTmemCols);
   if (tid == 32) {
     mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
     fence_barrier_init();
   }
   fence_proxy_async();
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 
   double gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
   double loss = 0, gb3[3] = {0, 0, 0};
-  uint32_t phase = 0;
+  uint32_t phase = 0, phase3 = 0;
   bool first = true;
   const int64_t nchunks = (n + kCP - 1) / kCP;
   const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk
@@ -171,6 +172,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       S.w[tid] = wt;
     }
     __syncthreads();
+    if (ISM && !first) {  // the previous chunk's weight-gradient GEMM still reads X and Y
+      umma::wait_mma(&S.bar[1], phase3);
+      phase3 ^= 1;
+      umma::fence_after();
+    }
 
     // F1: layer 1 and its tangents -> X = [h1 | t1_0 | t1_1 | t1_2] (rows 4p + j, column h)
 #pragma unroll
@@ -282,8 +288,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     umma::fence_after();
     if (tid == 0) {
       umma::gemm_split<true, false>(tm + kColD2, sW2h, sW2l, sYh, sYl, false);  // W2^T Y
-      umma::gemm_split<true, true>(tm + kColD3, sYh, sYl, sXh, sXl, !first);     // Y^T X
       umma::commit(&S.bar[0]);
+      umma::gemm_split<true, true>(tm + kColD3, sYh, sYl, sXh, sXl, !first);     // Y^T X
+      umma::commit(&S.bar[1]);  // overlaps F3 and the next chunk's record loads
     }
     first = false;
     umma::wait_mma(&S.bar[0], phase);
@@ -320,6 +327,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   }
 
   if (ISM) {
+    if (!first) {
+      umma::wait_mma(&S.bar[1], phase3);
+      umma::fence_after();
+    }
     const int64_t width = 1 + silu_params(kH);
     const int64_t oW1 = 1, ob1 = oW1 + 4 * kH, oW2 = ob1 + kH, ob2 = oW2 + kH * kH,
                   oW3 = ob2 + kH, ob3 = oW3 + 3 * kH;
