@@ -51,8 +51,12 @@ struct SiluShared {
 };
 constexpr size_t kSiluSmem = 6 * umma::kTileBytes + sizeof(SiluShared) + 1024;
 
+// 1024-B aligned start inside the dynamic shared buffer (SWIZZLE_128B atoms). The offset is
+// applied to the __shared__ array itself so the compiler keeps shared-space (LDS/STS)
+// addressing for everything derived from it.
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  return p + ((1024u - (a & 1023u)) & 1023u);
 }
 
 __device__ __forceinline__ float sigmoid(float a) { return fast_rcp(1.f + __expf(-a)); }
