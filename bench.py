@@ -61,6 +61,13 @@ WORKLOADS = {
                    nu=0.1, dt=0.05, K=0, hidden=128, lr=1e-3, weight_decay=0.0,
                    divergence="exact", estimator="blob", bandwidth=0.025),
 }
+# BASELINE's own network for configs 0 and 2 ("2 x 128 SiLU", extension M1 with tcgen05
+# hidden GEMMs); the reference arm has only the softsign net, so these are extension lines.
+WORKLOADS["c2silu"] = dict(WORKLOADS["c2"], workload="config2_two_stream_sbtm_silu2x128",
+                           net="silu")
+WORKLOADS["c0silu"] = dict(WORKLOADS["c0"], workload="config0_landau_damping_sbtm_silu2x128",
+                           net="silu")
+SILU_GEMM_FLOP_PER_PARTICLE = 3 * 2 * 128 * 128 * 4  # G1, G2, G3 per ISM step (fp32-equivalent)
 
 
 def parse_args():
@@ -256,7 +263,12 @@ def build_sim(wl: dict, seed: int, device):
     p = ParticleEnsemble.from_arrays(x, v, w, device=device)
     rho, J = deposit(p, grid)
     fields = initial_fields(cfg, grid, rho, J)
-    if wl["estimator"] == "sbtm":
+    if wl["estimator"] == "sbtm" and wl.get("net") == "silu":
+        from paper_2603_25832_b200.silu_net import SiluEstimator, SiluScoreNet
+
+        net = SiluScoreNet.init_glorot(rng, device=device)
+        est = SiluEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay)
+    elif wl["estimator"] == "sbtm":
         net = MlpScoreNet.init_glorot(cfg.dv, cfg.hidden, rng, device=device)
         est = SbtmEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay,
                             divergence=cfg.divergence, rademacher=cfg.rademacher)
@@ -267,6 +279,51 @@ def build_sim(wl: dict, seed: int, device):
                      estimator=est, max_rows=4)
     del torch
     return sim
+
+
+def silu_extension(torch, device, wl: dict, seed: int, steps: int = 3) -> dict:
+    """Full steps of the same workload with BASELINE's 2 x 128 SiLU score net (extension M1):
+    graph-replayed steps timed with CUDA events (L2 flushed between steps), plus the K-step
+    ISM training loop timed alone for the tensor-core roofline of the hidden GEMMs."""
+    from paper_2603_25832_b200 import _lib
+
+    sw = dict(wl, workload=wl["workload"] + "_silu2x128", net="silu")
+    sim = build_sim(sw, seed, device)
+    n = sw["n"]
+    for _ in range(3):
+        sim.step(0)
+    torch.cuda.synchronize()
+    sim.check()
+    sim.capture(row=3)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    total = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sim.replay(1)
+        e1.record()
+        e1.synchronize()
+        total += e0.elapsed_time(e1)
+    sim.check()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sim.trainer.run(n, ci=sim.ci, flags=sim.flags)
+    e1.record()
+    e1.synchronize()
+    ism_ms = e0.elapsed_time(e1) / max(sw["K"], 1)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    bf16 = float(peaks["bf16_tflops"])
+    tc = 3 * SILU_GEMM_FLOP_PER_PARTICLE * n / (ism_ms * 1e-3) / 1e12
+    del _lib
+    return {"workload": sw["workload"], "value": n * steps / (total * 1e-3),
+            "unit": "particle-steps/s", "ms_per_step": total / steps, "ism_step_ms": ism_ms,
+            "tensor_roofline": {"bound": "tensor", "kernel": "spic_silu_ism_partials (k_silu)",
+                                "achieved": tc, "peak": bf16, "unit": "TFLOP/s",
+                                "frac": tc / bf16,
+                                "note": "bf16 tensor FLOP incl. the 3 split passes; ISM step "
+                                        "= partials + ordered reduce + AdamW finalize",
+                                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"}}
 
 
 def config1_microbench(torch, device, n: int = 131072, reps: int = 3) -> dict:
@@ -500,8 +557,10 @@ def main():
         "config": {"workload": wl["workload"], "n_per_gpu": n, "M": wl["M"], "L": wl["L"],
                    "mode": wl["mode"], "estimator": wl["estimator"], "K_ism": wl["K"],
                    "hidden": wl["hidden"],
-                   "net": "softsign 1x{} (reference arch; BASELINE's 2x128 SiLU is extension M1)"
-                   .format(wl["hidden"]),
+                   "net": ("SiLU 2x128 (BASELINE's MLP, extension M1, tcgen05 hidden GEMMs)"
+                           if wl.get("net") == "silu" else
+                           "softsign 1x{} (reference arch; BASELINE's 2x128 SiLU is extension "
+                           "M1, see silu_extension)".format(wl["hidden"])),
                    "divergence": wl["divergence"], "sub_cells": sim.S,
                    "l2": "flushed between timed steps (256 MiB write, outside timed windows)",
                    "parallelism": ("single GPU" if world == 1 else
@@ -526,6 +585,11 @@ def main():
             out["config1_microbench"] = mb
         except Exception as exc:  # noqa: BLE001
             out["config1_microbench"] = {"error": str(exc)}
+    if world == 1 and wl["estimator"] == "sbtm" and wl.get("net") != "silu":
+        try:
+            out["silu_extension"] = silu_extension(torch, device, wl, args.seed)
+        except Exception as exc:  # noqa: BLE001
+            out["silu_extension"] = {"error": str(exc)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line = cpu_baseline_line(wl, args.seed)
