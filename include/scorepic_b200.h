@@ -191,12 +191,19 @@ int spic_silu_forward(const float* params32, int32_t H, const float* xv, const f
 int spic_silu_ism_partials(const float* params32, int32_t H, const float* xv, const float* sw,
                            int64_t n, float x_scale, void* scratch, size_t scratch_bytes,
                            void* stream);
+/* Weighted MSE (pretraining, ref: score.py:254-300 / 402-445 with this network): partials of
+ * sum_p w_p inv_wsum |s_p - Z_p|^2 from pid-order planes x (scaled by x_scale), v[3][ldv],
+ * w, targets Z[3][ldz]; idx (nullable) maps kernel particle p to the source row. */
+int spic_silu_mse_partials(const float* params32, int32_t H, const float* x, const float* v,
+                           int64_t ldv, const float* w, int64_t n, float x_scale,
+                           const float* Z, int64_t ldz, const int32_t* idx, double inv_wsum,
+                           void* scratch, size_t scratch_bytes, void* stream);
 int64_t spic_silu_row_offset(int64_t n);
 /* AdamW with restore-and-halve recovery on the reduced row (same contract as
- * spic_sbtm_finalize_ex with div_mode 0). */
-int spic_silu_finalize(void* scratch, int64_t n, int32_t H, double* params64, double* m,
-                       double* v2, double* opt_state, double beta1, double beta2, double eps,
-                       double weight_decay, int32_t reset_lr, int32_t apply_step,
+ * spic_sbtm_finalize_ex; mse != 0 selects its div_mode 3 semantics). */
+int spic_silu_finalize(void* scratch, int64_t n, int32_t H, int32_t mse, double* params64,
+                       double* m, double* v2, double* opt_state, double beta1, double beta2,
+                       double eps, double weight_decay, int32_t reset_lr, int32_t apply_step,
                        float* params32, double* grads_out, double* loss_out, int32_t* flags,
                        void* stream);
 /* Tensor-core self-test: float32 [128][128] W, X, Y -> D1 = W X^T, D2 = W^T Y^T, D3 = Y^T X

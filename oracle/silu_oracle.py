@@ -118,6 +118,26 @@ def ism_loss_and_grad(params, u, w, H: int):
     return loss, grads
 
 
+def mse_loss_and_grad(params, u, w, target, H: int):
+    """(loss, grads[P]) of sum_p (w_p / sum w) |s_p - target_p|^2 (pretraining, ref:
+    score.py:254-300 / 340-350 restated for this network), float64."""
+    W1, b1, W2, b2, W3, b3 = split(params, H)
+    wi = np.asarray(w, dtype=np.float64) / float(np.sum(w))
+    a1 = u @ W1.T + b1
+    h1, d1, _ = _silu_terms(a1)
+    a2 = h1 @ W2.T + b2
+    h2, d2, _ = _silu_terms(a2)
+    r = h2 @ W3.T + b3 - np.asarray(target, dtype=np.float64)
+    loss = float(np.sum(wi * np.sum(r * r, axis=1)))
+    gs = 2.0 * wi[:, None] * r
+    gW3, gb3 = gs.T @ h2, gs.sum(axis=0)
+    da2 = d2 * (gs @ W3)
+    gW2, gb2 = da2.T @ h1, da2.sum(axis=0)
+    da1 = d1 * (da2 @ W2)
+    gW1, gb1 = da1.T @ u, da1.sum(axis=0)
+    return loss, np.concatenate([gW1.ravel(), gb1, gW2.ravel(), gb2, gW3.ravel(), gb3])
+
+
 def adamw_step(params, grads, m, v2, t: int, lr: float, betas=(0.9, 0.999), eps=1e-8,
                weight_decay=0.0):
     """One AdamW step (ref: score.py:371-386) on flat float64 arrays; returns new arrays."""

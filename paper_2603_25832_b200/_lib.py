@@ -75,8 +75,10 @@ SIGNATURES = {
     "spic_silu_forward": (ctypes.c_int, [_P, _I32, _P, _P, _I64, _F, _P, _P]),
     "spic_silu_ism_partials": (ctypes.c_int, [_P, _I32, _P, _P, _I64, _F, _P, ctypes.c_size_t, _P]),
     "spic_silu_row_offset": (_I64, [_I64]),
-    "spic_silu_finalize": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _D, _D, _D, _D, _I32,
-                                          _I32, _P, _P, _P, _P, _P]),
+    "spic_silu_mse_partials": (ctypes.c_int, [_P, _I32, _P, _P, _I64, _P, _I64, _F, _P, _I64, _P,
+                                              _D, _P, ctypes.c_size_t, _P]),
+    "spic_silu_finalize": (ctypes.c_int, [_P, _I64, _I32, _I32, _P, _P, _P, _P, _D, _D, _D, _D,
+                                          _I32, _I32, _P, _P, _P, _P, _P]),
     "spic_umma_selftest": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "spic_push": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _P, _P, _P, _I32, _D, _F, _P, _P]),
     "spic_interpolate": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _I32, _D, _P, _I64, _P, _I64,

@@ -44,7 +44,8 @@ __host__ __device__ constexpr int64_t silu_params(int H) { return (int64_t)H * H
 struct SiluShared {
   float4 u[kCP];
   float w[kCP];
-  float4 gs[kCP];              // (2w s, 2w)
+  float4 gs[kCP];              // ISM: (2w s, 2w); MSE: (2w' (s - t), 0)
+  float4 t[kCP];               // MSE target
   float red[4][4 * kCP];       // per-warp-quarter partial (s0, s1, s2, div) per particle
   uint64_t bar[2];  // [0]: G1 / G2 done, [1]: G3 done (X, Y free again)
   uint32_t tmem;
@@ -95,14 +96,33 @@ __device__ __forceinline__ void st_split(uint32_t addr, float x) {
 
 // One CTA per SM, four warpgroups. Thread (h, warpgroup g) owns hidden unit h (its TMEM lane)
 // for particles 8g..8g+7 of each 32-particle chunk; one thread issues the CTA's GEMMs.
-// ISM = false: forward only (scores into sw_out lanes 0..2, weight lane kept).
-template <bool ISM>
+// MODE 0: forward only (scores into sw_out lanes 0..2, weight lane kept); 1: ISM partials
+// (exact divergence); 2: weighted MSE partials to a target score (pretraining, ref:
+// score.py:254-300 applied to this network; no divergence, so the tangent columns are zero).
+// Inputs: cell-sorted records (xv != NULL) or pid-order planes x, v[3][ldv], w read through
+// idx (nullable) together with the target planes Z[3][ldz].
+struct SiluInputs {
+  const float4* xv;
+  const float4* sw;
+  const float* x;
+  const float* v;
+  int64_t ldv;
+  const float* w;
+  const float* Z;
+  int64_t ldz;
+  const int32_t* idx;
+  float inv_wsum;
+};
+
+template <int MODE>
 __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ params,
-                                                 const float4* __restrict__ xv,
-                                                 const float4* __restrict__ sw, int64_t n,
+                                                 const SiluInputs in, int64_t n,
                                                  float x_scale, float L,
                                                  float4* __restrict__ sw_out,
                                                  double* __restrict__ part) {
+  constexpr bool ISM = MODE != 0;  // training modes (loss + gradient partials)
+  const float4* __restrict__ xv = in.xv;
+  const float4* __restrict__ sw = in.sw;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
   uint8_t* W2h = base;
@@ -164,16 +184,24 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     if (tid < kCP) {
       const int64_t p = c * kCP + tid;
-      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 u = make_float4(0.f, 0.f, 0.f, 0.f), t = u;
       float wt = 0.f;
       if (p < n) {
-        const float4 A = xv[p];
-        const float x = A.x < 0.f ? A.x + L : A.x;  // % M quirk records carry x - L
-        u = make_float4(x * x_scale, A.y, A.z, A.w);
-        wt = sw[p].w;
+        if (xv) {
+          const float4 A = xv[p];
+          const float x = A.x < 0.f ? A.x + L : A.x;  // % M quirk records carry x - L
+          u = make_float4(x * x_scale, A.y, A.z, A.w);
+          wt = sw[p].w;
+        } else {
+          const int64_t r = in.idx ? (int64_t)in.idx[p] : p;
+          u = make_float4(in.x[r] * x_scale, in.v[r], in.v[in.ldv + r], in.v[2 * in.ldv + r]);
+          wt = in.w[r];
+          if (MODE == 2) t = make_float4(in.Z[r], in.Z[in.ldz + r], in.Z[2 * in.ldz + r], 0.f);
+        }
       }
       S.u[tid] = u;
       S.w[tid] = wt;
+      if (MODE == 2) S.t[tid] = t;
     }
     __syncthreads();
     if (ISM && !first) {  // the previous chunk's weight-gradient GEMM still reads X and Y
@@ -237,8 +265,17 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
                         (S.red[2][4 * p + k] + S.red[3][4 * p + k]));
       dv = (S.red[0][4 * p + 3] + S.red[1][4 * p + 3]) + (S.red[2][4 * p + 3] + S.red[3][4 * p + 3]);
       const int64_t q = c * kCP + p;
-      if (!ISM) {
+      if (MODE == 0) {
         if (q < n) sw_out[q] = make_float4(s[0], s[1], s[2], sw[q].w);
+      } else if (MODE == 2) {
+        const float wi = S.w[p] * in.inv_wsum;
+        const float4 t = S.t[p];
+        const float r0 = s[0] - t.x, r1 = s[1] - t.y, r2 = s[2] - t.z;
+        S.gs[p] = make_float4(2.f * wi * r0, 2.f * wi * r1, 2.f * wi * r2, 0.f);
+        loss += (double)(wi * (r0 * r0 + r1 * r1 + r2 * r2));
+        gb3[0] += (double)(2.f * wi * r0);
+        gb3[1] += (double)(2.f * wi * r1);
+        gb3[2] += (double)(2.f * wi * r2);
       } else {
         const float wt = S.w[p], tw = 2.f * wt;
         S.gs[p] = make_float4(tw * s[0], tw * s[1], tw * s[2], tw);
@@ -444,11 +481,12 @@ int silu_blocks(int64_t n) {
 
 // single-CTA finalize: the reduced row [loss, grads] -> AdamW with recovery
 __global__ void __launch_bounds__(1024) k_silu_finalize(
-    const double* __restrict__ row, int64_t P, double* __restrict__ params, double* __restrict__ m,
+    const double* __restrict__ row, int64_t P, bool mse, double* __restrict__ params,
+    double* __restrict__ m,
     double* __restrict__ v2, double* __restrict__ opt, double beta1, double beta2, double eps,
     double wd, int reset_lr, int apply_step, float* __restrict__ params32,
     double* __restrict__ grads_out, double* __restrict__ loss_out, double* cand, int32_t* flags) {
-  adamw_with_recovery(row[0], row + 1, P, false, params, m, v2, opt, beta1, beta2, eps, wd,
+  adamw_with_recovery(row[0], row + 1, P, mse, params, m, v2, opt, beta1, beta2, eps, wd,
                       reset_lr, apply_step, params32, grads_out, loss_out, cand, flags);
 }
 
@@ -468,41 +506,31 @@ extern "C" int64_t spic_silu_row_offset(int64_t n) {
   return (int64_t)(sizeof(double) * (size_t)silu_blocks(n) * (1 + (size_t)silu_params(kH)));
 }
 
-static int silu_launch(bool ism, const float* params32, int32_t H, const float* xv,
-                       const float* sw, int64_t n, float x_scale, float* sw_out, double* part,
-                       cudaStream_t st) {
+static int silu_launch(int mode, const float* params32, int32_t H, const SiluInputs& in,
+                       int64_t n, float x_scale, float* sw_out, double* part, cudaStream_t st) {
   if (H != kH) return SPIC_ERR_UNSUPPORTED;
-  if (n < 1 || !xv || !sw || !(x_scale > 0.f)) return SPIC_ERR_ARG;
+  if (n < 1 || !(x_scale > 0.f)) return SPIC_ERR_ARG;
+  if (in.xv ? !in.sw : (!in.x || !in.v || !in.w)) return SPIC_ERR_ARG;
+  if (mode == 2 && (in.xv || !in.Z)) return SPIC_ERR_ARG;
   const int blocks = silu_blocks(n);
   const float L = 1.0f / x_scale;
-  if (ism) {
-    cudaFuncSetAttribute(k_silu<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiluSmem);
-    k_silu<true><<<blocks, kNT, kSiluSmem, st>>>(params32, (const float4*)xv, (const float4*)sw, n,
-                                                 x_scale, L, nullptr, part);
-  } else {
-    cudaFuncSetAttribute(k_silu<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiluSmem);
-    k_silu<false><<<blocks, kNT, kSiluSmem, st>>>(params32, (const float4*)xv, (const float4*)sw, n,
-                                                  x_scale, L, (float4*)sw_out, nullptr);
-  }
+#define SPIC_SILU_LAUNCH(MD)                                                                   \
+  do {                                                                                         \
+    cudaFuncSetAttribute(k_silu<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                         (int)kSiluSmem);                                                      \
+    k_silu<MD><<<blocks, kNT, kSiluSmem, st>>>(params32, in, n, x_scale, L, (float4*)sw_out,   \
+                                               part);                                          \
+  } while (0)
+  if (mode == 0) SPIC_SILU_LAUNCH(0);
+  else if (mode == 1) SPIC_SILU_LAUNCH(1);
+  else SPIC_SILU_LAUNCH(2);
+#undef SPIC_SILU_LAUNCH
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
 }
 
-extern "C" int spic_silu_forward(const float* params32, int32_t H, const float* xv,
-                                 const float* sw, int64_t n, float x_scale, float* sw_out,
-                                 void* stream) {
-  if (!sw_out) return SPIC_ERR_ARG;
-  return silu_launch(false, params32, H, xv, sw, n, x_scale, sw_out, nullptr, (cudaStream_t)stream);
-}
-
-extern "C" int spic_silu_ism_partials(const float* params32, int32_t H, const float* xv,
-                                      const float* sw, int64_t n, float x_scale, void* scratch,
-                                      size_t scratch_bytes, void* stream) {
-  if (n >= 1 && scratch_bytes < spic_silu_scratch_bytes(n)) return SPIC_ERR_SCRATCH;
-  cudaStream_t st = (cudaStream_t)stream;
-  int rc = silu_launch(true, params32, H, xv, sw, n, x_scale, nullptr, (double*)scratch, st);
-  if (rc != SPIC_OK) return rc;
+static int silu_reduce(int64_t n, void* scratch, cudaStream_t st) {
   const int rows = silu_blocks(n);
   const int64_t width = 1 + silu_params(kH);
   double* part = (double*)scratch;
@@ -513,18 +541,52 @@ extern "C" int spic_silu_ism_partials(const float* params32, int32_t H, const fl
   return SPIC_OK;
 }
 
-extern "C" int spic_silu_finalize(void* scratch, int64_t n, int32_t H, double* params64,
-                                  double* m, double* v2, double* opt_state, double beta1,
-                                  double beta2, double eps, double weight_decay, int32_t reset_lr,
-                                  int32_t apply_step, float* params32, double* grads_out,
-                                  double* loss_out, int32_t* flags, void* stream) {
+extern "C" int spic_silu_forward(const float* params32, int32_t H, const float* xv,
+                                 const float* sw, int64_t n, float x_scale, float* sw_out,
+                                 void* stream) {
+  if (!sw_out || !xv) return SPIC_ERR_ARG;
+  SiluInputs in{(const float4*)xv, (const float4*)sw, nullptr, nullptr, 0, nullptr, nullptr, 0,
+                nullptr, 0.f};
+  return silu_launch(0, params32, H, in, n, x_scale, sw_out, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int spic_silu_ism_partials(const float* params32, int32_t H, const float* xv,
+                                      const float* sw, int64_t n, float x_scale, void* scratch,
+                                      size_t scratch_bytes, void* stream) {
+  if (n >= 1 && scratch_bytes < spic_silu_scratch_bytes(n)) return SPIC_ERR_SCRATCH;
+  if (!xv) return SPIC_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  SiluInputs in{(const float4*)xv, (const float4*)sw, nullptr, nullptr, 0, nullptr, nullptr, 0,
+                nullptr, 0.f};
+  int rc = silu_launch(1, params32, H, in, n, x_scale, nullptr, (double*)scratch, st);
+  return rc != SPIC_OK ? rc : silu_reduce(n, scratch, st);
+}
+
+extern "C" int spic_silu_mse_partials(const float* params32, int32_t H, const float* x,
+                                      const float* v, int64_t ldv, const float* w, int64_t n,
+                                      float x_scale, const float* Z, int64_t ldz,
+                                      const int32_t* idx, double inv_wsum, void* scratch,
+                                      size_t scratch_bytes, void* stream) {
+  if (n >= 1 && scratch_bytes < spic_silu_scratch_bytes(n)) return SPIC_ERR_SCRATCH;
+  cudaStream_t st = (cudaStream_t)stream;
+  SiluInputs in{nullptr, nullptr, x, v, ldv, w, Z, ldz, idx, (float)inv_wsum};
+  int rc = silu_launch(2, params32, H, in, n, x_scale, nullptr, (double*)scratch, st);
+  return rc != SPIC_OK ? rc : silu_reduce(n, scratch, st);
+}
+
+extern "C" int spic_silu_finalize(void* scratch, int64_t n, int32_t H, int32_t mse,
+                                  double* params64, double* m, double* v2, double* opt_state,
+                                  double beta1, double beta2, double eps, double weight_decay,
+                                  int32_t reset_lr, int32_t apply_step, float* params32,
+                                  double* grads_out, double* loss_out, int32_t* flags,
+                                  void* stream) {
   if (H != kH) return SPIC_ERR_UNSUPPORTED;
   if (n < 1) return SPIC_ERR_ARG;
   const int64_t P = silu_params(kH);
   double* row = (double*)((char*)scratch + spic_silu_row_offset(n));
   k_silu_finalize<<<1, 1024, 0, (cudaStream_t)stream>>>(
-      row, P, params64, m, v2, opt_state, beta1, beta2, eps, weight_decay, reset_lr, apply_step,
-      params32, grads_out, loss_out, row + 1 + P, flags);
+      row, P, mse != 0, params64, m, v2, opt_state, beta1, beta2, eps, weight_decay, reset_lr,
+      apply_step, params32, grads_out, loss_out, row + 1 + P, flags);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;

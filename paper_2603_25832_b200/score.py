@@ -344,7 +344,7 @@ class PretrainResult:
     tol: float
 
 
-def pretrain(net: MlpScoreNet, particles: ParticleEnsemble, analytic_score, *, L: float,
+def pretrain(net, particles: ParticleEnsemble, analytic_score, *, L: float,
              rng: np.random.Generator, budget: int = 10000, batch: int = 4096, lr: float = 1e-3,
              weight_decay: float = 1e-4, tol: float | None = None,
              eval_every: int = 100) -> PretrainResult:
@@ -361,15 +361,30 @@ def pretrain(net: MlpScoreNet, particles: ParticleEnsemble, analytic_score, *, L
     if tol is None:
         tol = 1e-3 * float((w64 * (T.double() ** 2).sum(0)).sum()) / wsum
     opt = AdamW(lr=lr, weight_decay=weight_decay, device=dev)
-    opt._ensure(net)
+    opt._ensure(net.n_params)
     flags = new_flags(dev)
     loss_buf = torch.empty(1, dtype=torch.float64, device=dev)
     idx_dev = torch.empty(n, dtype=torch.int32, device=dev)
+    if getattr(net, "arch", "softsign") == "silu":  # extension M1: same loop, SiLU kernels
+        from .silu_net import _silu_finalize, _silu_mse_partials
+
+        def mse_partials(nb, idx, inv):
+            return _silu_mse_partials(net, nb, x=xn, vp=particles.vp, w=particles.w, Z=T, ldz=n,
+                                      idx=idx, inv_wsum=inv, ldv=n)
+
+        def mse_finalize(buf, nb, **kw):
+            _silu_finalize(net, buf, nb, kw.pop("opt", None) or AdamW(device=dev), mse=True, **kw)
+    else:
+        def mse_partials(nb, idx, inv):
+            return _partials(net, DIV_MSE, n=nb, x_scale=1.0, x=xn, vp=particles.vp,
+                             w=particles.w, Z=T, ldz=n, idx=idx, inv_wsum=inv, ldv=n)
+
+        def mse_finalize(buf, nb, **kw):
+            _finalize(net, buf, nb, DIV_MSE, **kw)
 
     def full_mse() -> float:
-        buf = _partials(net, DIV_MSE, n=n, x_scale=1.0, x=xn, vp=particles.vp, w=particles.w,
-                        Z=T, ldz=n, inv_wsum=1.0 / wsum)
-        _finalize(net, buf, n, DIV_MSE, loss_out=loss_buf)
+        buf = mse_partials(n, None, 1.0 / wsum)
+        mse_finalize(buf, n, loss_out=loss_buf)
         return float(loss_buf.item())
 
     mse = full_mse()
@@ -387,9 +402,8 @@ def pretrain(net: MlpScoreNet, particles: ParticleEnsemble, analytic_score, *, L
             hi = min(lo + batch, n)
             nb = hi - lo
             inv = 1.0 / float(w_host[perm[lo:hi]].sum())
-            buf = _partials(net, DIV_MSE, n=nb, x_scale=1.0, x=xn, vp=particles.vp,
-                            w=particles.w, Z=T, ldz=n, idx=idx_dev[lo:hi], inv_wsum=inv, ldv=n)
-            _finalize(net, buf, nb, DIV_MSE, opt=opt, reset_lr=True, apply_step=True, flags=flags)
+            buf = mse_partials(nb, idx_dev[lo:hi], inv)
+            mse_finalize(buf, nb, opt=opt, reset_lr=True, apply_step=True, flags=flags)
             steps += 1
             if steps % eval_every == 0:
                 raise_for_flags(flags)

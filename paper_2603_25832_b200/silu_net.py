@@ -5,8 +5,9 @@ reference itself ships only the one-hidden-layer softsign net (ref: score.py:38-
 module adds the deeper network behind the same estimator plug-in surface (estimate / update /
 warnings, ref: score.py:591-623) and the same device training loop contract as SbtmTrainer,
 so the step engines and run() drive either network. Kernels: spic_silu_forward,
-spic_silu_ism_partials (tcgen05 split-BF16 hidden GEMMs), spic_silu_finalize (AdamW with the
-reference's restore-and-halve recovery). Only the exact divergence is supported.
+spic_silu_ism_partials (tcgen05 split-BF16 hidden GEMMs), spic_silu_mse_partials
+(pretraining), spic_silu_finalize (AdamW with the reference's restore-and-halve recovery).
+Only the exact divergence is supported.
 """
 
 from __future__ import annotations
@@ -110,10 +111,19 @@ def _silu_partials(net: SiluScoreNet, xv, sw, n: int, L: float):
     return buf
 
 
+def _silu_mse_partials(net: SiluScoreNet, n: int, *, x, vp, w, Z, ldz: int, idx=None,
+                       inv_wsum: float, ldv: int, x_scale: float = 1.0):
+    buf, nb = _lib.scratch("silu", _lib.query("spic_silu_scratch_bytes", n))
+    _lib.call("spic_silu_mse_partials", _lib.ptr(net.params32), net.hidden, _lib.ptr(x),
+              _lib.ptr(vp), ldv, _lib.ptr(w), n, float(x_scale), _lib.ptr(Z), ldz, _lib.ptr(idx),
+              float(inv_wsum), _lib.ptr(buf), nb, _lib.stream_handle())
+    return buf
+
+
 def _silu_finalize(net: SiluScoreNet, buf, n: int, opt: AdamW, *, reset_lr=False,
-                   apply_step=False, grads_out=None, loss_out=None, flags=None):
+                   apply_step=False, grads_out=None, loss_out=None, flags=None, mse=False):
     opt._ensure(net.n_params)
-    _lib.call("spic_silu_finalize", _lib.ptr(buf), n, net.hidden, _lib.ptr(net.params64),
+    _lib.call("spic_silu_finalize", _lib.ptr(buf), n, net.hidden, int(mse), _lib.ptr(net.params64),
               _lib.ptr(opt.m), _lib.ptr(opt.v), _lib.ptr(opt.state), float(opt.betas[0]),
               float(opt.betas[1]), float(opt.eps), float(opt.weight_decay), int(reset_lr),
               int(apply_step), _lib.ptr(net.params32), _lib.ptr(grads_out), _lib.ptr(loss_out),
@@ -202,5 +212,4 @@ class SiluEstimator(SbtmEstimator):
         if f[_lib.FLAG_TRAIN_FATAL]:
             raise RuntimeError("training divergence")
 
-    def pretrain(self, *args, **kwargs):
-        raise NotImplementedError("pretraining is implemented for the softsign network only")
+    # pretrain: inherited; score.pretrain dispatches to the SiLU MSE kernels for this net

@@ -78,3 +78,24 @@ def test_param_layout():
     assert W1.shape == (8, 4) and W2.shape == (8, 8) and W3.shape == (3, 8)
     assert not b1.any() and not b2.any() and not b3.any()
     assert np.abs(W2).max() <= np.sqrt(6.0 / 16)
+
+
+def test_mse_grad_matches_autograd():
+    params, u, w, H = _case()
+    target = np.random.default_rng(4).normal(size=(u.shape[0], 3))
+    loss, g = so.mse_loss_and_grad(params, u, w, target, H)
+    pt = torch.tensor(params, dtype=torch.float64, requires_grad=True)
+    o = 0
+    W1 = pt[o:o + 4 * H].reshape(H, 4); o += 4 * H
+    b1 = pt[o:o + H]; o += H
+    W2 = pt[o:o + H * H].reshape(H, H); o += H * H
+    b2 = pt[o:o + H]; o += H
+    W3 = pt[o:o + 3 * H].reshape(3, H); o += 3 * H
+    b3 = pt[o:o + 3]
+    silu = torch.nn.functional.silu
+    s = silu(silu(torch.tensor(u) @ W1.T + b1) @ W2.T + b2) @ W3.T + b3
+    wt = torch.tensor(w) / float(np.sum(w))
+    lt = (wt * ((s - torch.tensor(target)) ** 2).sum(1)).sum()
+    (gt,) = torch.autograd.grad(lt, pt)
+    assert loss == pytest.approx(float(lt.detach()), rel=1e-12)
+    np.testing.assert_allclose(g, gt.numpy(), rtol=1e-10, atol=1e-13)
