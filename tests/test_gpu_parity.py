@@ -376,7 +376,7 @@ def test_engine_steps_match_reference_run(spic, golden, tag):
 
 
 # ---------------------------------------------------------------------------- decomposed engine
-@pytest.mark.parametrize("estimator", ["sbtm", "blob"])
+@pytest.mark.parametrize("estimator", ["sbtm", "blob", "silu"])
 def test_dist_engine_single_rank_matches_engine(spic, estimator):
     """DistSimulation (the per-rank path of the cell-range decomposition) on one rank gives
     the same trajectory as the single-GPU engine."""
@@ -404,6 +404,11 @@ def test_dist_engine_single_rank_matches_engine(spic, estimator):
             r = np.random.default_rng(5)
             net = MlpScoreNet.init_glorot(3, 32, r)
             est = SbtmEstimator(net, L, 3, r, lr=1e-3, weight_decay=0.0, divergence="exact")
+        elif estimator == "silu":  # extension M1 (tcgen05 SiLU net) through the same engines
+            from paper_2603_25832_b200.silu_net import SiluEstimator, SiluScoreNet
+
+            r = np.random.default_rng(5)
+            est = SiluEstimator(SiluScoreNet.init_glorot(r), L, 3, r, lr=1e-3, weight_decay=0.0)
         else:
             est = BlobEstimator(grid, None)
         if kind == "single":
