@@ -77,6 +77,10 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
   return v[0];
 }
 
+__device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one warpgroup
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+}
+
 // Split-BF16 store of one value into a hi tile (at addr) and its lo tile (addr + 32 KB).
 // addr = the thread's column base for the row's (r & 7) swizzle phase + r * 128; with the
 // particle loops unrolled the row part is a constant that folds into the STS immediate.
@@ -181,9 +185,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk
   const uint32_t c0 = 4 * p0;  // ... and their first GEMM column
 
+  const int wtid = tid & 127;  // thread index inside the warpgroup
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    if (tid < kCP) {
-      const int64_t p = c * kCP + tid;
+    // each warpgroup loads, reduces and scores its own 8 particles: only the GEMM issue points
+    // need the whole CTA, everything else synchronises one warpgroup (named barrier)
+    if (wtid < kPPT) {
+      const int pl = p0 + wtid;
+      const int64_t p = c * kCP + pl;
       float4 u = make_float4(0.f, 0.f, 0.f, 0.f), t = u;
       float wt = 0.f;
       if (p < n) {
@@ -199,11 +207,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           if (MODE == 2) t = make_float4(in.Z[r], in.Z[in.ldz + r], in.Z[2 * in.ldz + r], 0.f);
         }
       }
-      S.u[tid] = u;
-      S.w[tid] = wt;
-      if (MODE == 2) S.t[tid] = t;
+      S.u[pl] = u;
+      S.w[pl] = wt;
+      if (MODE == 2) S.t[pl] = t;
     }
-    __syncthreads();
+    wg_sync(wg);
     if (ISM && !first) {  // the previous chunk's weight-gradient GEMM still reads X and Y
       umma::wait_mma(&S.bar[1], phase3);
       phase3 ^= 1;
@@ -253,11 +261,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       }
       S.red[quarter][c0 + lane] = transpose_reduce32(val, lane);
     }
-    umma::fence_before();
-    __syncthreads();
-    umma::fence_after();
-    if (tid < kCP) {
-      const int p = tid;
+    wg_sync(wg);
+    if (wtid < kPPT) {
+      const int p = p0 + wtid;
       float s[3], dv = 0.f;
 #pragma unroll
       for (int k = 0; k < 3; ++k)
@@ -284,13 +290,12 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         for (int k = 0; k < 3; ++k) gb3[k] += (double)(tw * s[k]);
       }
     }
-    if (!ISM) {
+    if (!ISM) {  // D1 is rewritten by the next chunk's G1 only after the next CTA barrier
       umma::fence_before();
-      __syncthreads();
-      umma::fence_after();
+      wg_sync(wg);
       continue;
     }
-    __syncthreads();
+    wg_sync(wg);
 
     // F2b: reverse through layer 2 -> Y = [da2 | dc2_0 | dc2_1 | dc2_2]; dW3, db2
     {
@@ -363,8 +368,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       gb1 += (double)ab1;
     }
     umma::fence_before();
-    __syncthreads();
-    umma::fence_after();
+    wg_sync(wg);
   }
 
   if (ISM) {
@@ -402,15 +406,23 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 #pragma unroll
       for (int k = 0; k < 3; ++k) row[oW3 + k * kH + h] = t[6 + k];
     }
-    if (tid < 32) {
+    double* lcomb = comb + 4 * kH * 9;  // [4 warpgroups][loss, gb3]
+    if (wtid < 32) {
       loss = warp_sum(loss);
 #pragma unroll
       for (int k = 0; k < 3; ++k) gb3[k] = warp_sum(gb3[k]);
-      if (tid == 0) {
-        row[0] = loss;
+      if (wtid == 0) {
+        lcomb[4 * wg] = loss;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) row[ob3 + k] = gb3[k];
+        for (int k = 0; k < 3; ++k) lcomb[4 * wg + 1 + k] = gb3[k];
       }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      row[0] = (lcomb[0] + lcomb[4]) + (lcomb[8] + lcomb[12]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        row[ob3 + k] = (lcomb[1 + k] + lcomb[5 + k]) + (lcomb[9 + k] + lcomb[13 + k]);
     }
   }
   umma::fence_before();
