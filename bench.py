@@ -42,16 +42,21 @@ FLOP_PER_PAIR = 38.0
 METRIC = "particle-steps/s (full VML step, SBTM)"
 
 WORKLOADS = {
+    # BASELINE configs as named, incl. their score MLP "(x,v) -> 2x128 SiLU -> R^3"
+    # (extension M1: tcgen05 hidden GEMMs). "...ss" = the same config with the reference's own
+    # softsign 1x128 network (the only network the reference has; like-for-like with its arm).
     "c2": dict(workload="config2_two_stream_sbtm", preset="two_stream", mode="VPL", n=1 << 20,
                M=128, L=10 * math.pi, alpha=0.001, k=0.2, c=2.4, nu=0.05, dt=0.05, K=10,
-               hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact", estimator="sbtm"),
+               hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact", estimator="sbtm",
+               net="silu"),
     "c0": dict(workload="config0_landau_damping_sbtm", preset="landau_damping", mode="VPL",
                n=65536, M=64, L=4 * math.pi, alpha=0.01, k=0.5, c=0.0, nu=0.1, dt=0.05, K=10,
-               hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact", estimator="sbtm"),
+               hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact", estimator="sbtm",
+               net="silu"),
     "c4": dict(workload="config4_landau_damping_sbtm_n2^24", preset="landau_damping", mode="VPL",
                n=1 << 24, M=1024, L=4 * math.pi, alpha=0.01, k=0.5, c=0.0, nu=0.1, dt=0.05,
                K=10, hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact",
-               estimator="sbtm"),
+               estimator="sbtm", net="silu"),
     "c2blob": dict(workload="config2_two_stream_blob", preset="two_stream", mode="VPL",
                    n=1 << 20, M=128, L=10 * math.pi, alpha=0.001, k=0.2, c=2.4, nu=0.05,
                    dt=0.05, K=0, hidden=128, lr=1e-3, weight_decay=0.0, divergence="exact",
@@ -61,12 +66,11 @@ WORKLOADS = {
                    nu=0.1, dt=0.05, K=0, hidden=128, lr=1e-3, weight_decay=0.0,
                    divergence="exact", estimator="blob", bandwidth=0.025),
 }
-# BASELINE's own network for configs 0 and 2 ("2 x 128 SiLU", extension M1 with tcgen05
-# hidden GEMMs); the reference arm has only the softsign net, so these are extension lines.
-WORKLOADS["c2silu"] = dict(WORKLOADS["c2"], workload="config2_two_stream_sbtm_silu2x128",
-                           net="silu")
-WORKLOADS["c0silu"] = dict(WORKLOADS["c0"], workload="config0_landau_damping_sbtm_silu2x128",
-                           net="silu")
+for _k in ("c0", "c2", "c4"):
+    WORKLOADS[_k + "ss"] = dict(WORKLOADS[_k], net="softsign",
+                                workload=WORKLOADS[_k]["workload"] + "_reference_softsign_net")
+NET_LABEL = {"silu": "SiLU 2x128 (BASELINE's MLP; extension M1, tcgen05 split-BF16 hidden GEMMs)",
+             "softsign": "softsign 1x128 (the reference's network)"}
 SILU_GEMM_FLOP_PER_PARTICLE = 3 * 2 * 128 * 128 * 4  # G1, G2, G3 per ISM step (fp32-equivalent)
 
 
@@ -117,7 +121,25 @@ def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_strid
     O.build_cell_index(x1, eta, M)
     t["push_deposit_field_bin"] = time.perf_counter() - t0
     rng = np.random.default_rng(seed)
-    if wl["estimator"] == "sbtm":
+    if wl["estimator"] == "sbtm" and wl.get("net") == "silu":
+        from oracle import silu_oracle as SO
+
+        params = SO.glorot(128, rng)
+        sub = rng.choice(n, size=max(1, n // (4 * ism_sub)), replace=False)
+        u = SO.inputs(x1[sub], v1[sub], L)
+        m, v2 = np.zeros_like(params), np.zeros_like(params)
+        t0 = time.perf_counter()
+        for k in range(wl["K"]):
+            _, g = SO.ism_loss_and_grad(params, u, w[sub], 128)
+            params, m, v2 = SO.adamw_step(params, g, m, v2, k + 1, wl["lr"],
+                                          weight_decay=wl["weight_decay"])
+        t["ism"] = (time.perf_counter() - t0) * (n / len(sub))
+        t0 = time.perf_counter()
+        fsub = np.arange(0, n, ism_sub)
+        s = np.zeros_like(v1)
+        s[fsub] = SO.forward(params, SO.inputs(x1[fsub], v1[fsub], L), 128, with_div=False)[0]
+        t["forward"] = (time.perf_counter() - t0) * (n / len(fsub))
+    elif wl["estimator"] == "sbtm":
         net = O.Net.glorot(v.shape[1], wl["hidden"], rng)
         sub = rng.choice(n, size=max(1, n // ism_sub), replace=False)
         opt = O.AdamW(lr=wl["lr"], weight_decay=wl["weight_decay"])
@@ -167,9 +189,14 @@ def cpu_baseline_line(wl: dict, seed: int, reps: int = 1, warm: int = 0):
     n = wl["n"]
     live = O.count_live_pairs(st["x"], wl["L"] / wl["M"], wl["M"]) if wl["n"] <= (1 << 21) else None
     return dict(value=n / T, unit="particle-steps/s", cores=O.num_threads(), kind="port",
-                sample=("oracle/ float64 C+OpenMP port; per step: push/deposit/field/bin and "
-                        "score forward on all n, K ISM steps on n/16 particles (x16), pair "
-                        "kernel on every 16th cell (x16)"),
+                sample=("oracle/ float64 C+OpenMP port; per step: push/deposit/field/bin on "
+                        "all n, the pair kernel on every 16th cell (x16), and "
+                        + ("the SiLU 2x128 score net as the float64 numpy restatement "
+                           "oracle/silu_oracle.py (the reference has no such network): K ISM "
+                           "steps on n/64 particles (x64), forward on every 16th particle (x16)"
+                           if wl.get("net") == "silu" else
+                           "the reference's softsign score net: K ISM steps on n/16 particles "
+                           "(x16), forward on all n")),
                 seconds_per_step=T, stage_seconds=parts,
                 pair_interactions_per_s=(live / parts["collision"]) if live else None)
 
@@ -246,6 +273,22 @@ def fp32_peak_tflops(torch, _lib) -> float:
     return best
 
 
+def make_estimator_for(wl: dict, cfg, rng, device, grid):
+    from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
+
+    if wl["estimator"] == "sbtm" and wl.get("net") == "silu":
+        from paper_2603_25832_b200.silu_net import SiluEstimator, SiluScoreNet
+
+        net = SiluScoreNet.init_glorot(rng, device=device)
+        return SiluEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay)
+    if wl["estimator"] == "sbtm":
+        net = MlpScoreNet.init_glorot(cfg.dv, cfg.hidden, rng, device=device)
+        return SbtmEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay,
+                             divergence=cfg.divergence, rademacher=cfg.rademacher)
+    bw = wl["bandwidth"]
+    return BlobEstimator(grid, None if bw == "silverman" else float(bw))
+
+
 def build_sim(wl: dict, seed: int, device):
     import torch
 
@@ -253,7 +296,6 @@ def build_sim(wl: dict, seed: int, device):
     from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
     from paper_2603_25832_b200.run import initial_fields
     from paper_2603_25832_b200.sampling import sample_arrays
-    from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
     from paper_2603_25832_b200.state import ParticleEnsemble
 
     cfg = make_config(wl, seed)
@@ -263,33 +305,18 @@ def build_sim(wl: dict, seed: int, device):
     p = ParticleEnsemble.from_arrays(x, v, w, device=device)
     rho, J = deposit(p, grid)
     fields = initial_fields(cfg, grid, rho, J)
-    if wl["estimator"] == "sbtm" and wl.get("net") == "silu":
-        from paper_2603_25832_b200.silu_net import SiluEstimator, SiluScoreNet
-
-        net = SiluScoreNet.init_glorot(rng, device=device)
-        est = SiluEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay)
-    elif wl["estimator"] == "sbtm":
-        net = MlpScoreNet.init_glorot(cfg.dv, cfg.hidden, rng, device=device)
-        est = SbtmEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay,
-                            divergence=cfg.divergence, rademacher=cfg.rademacher)
-    else:
-        bw = wl["bandwidth"]
-        est = BlobEstimator(grid, None if bw == "silverman" else float(bw))
+    est = make_estimator_for(wl, cfg, rng, device, grid)
     sim = Simulation(p, fields, grid, dt=cfg.dt, nu=cfg.nu, mode=cfg.mode, gamma=cfg.gamma,
                      estimator=est, max_rows=4)
     del torch
     return sim
 
 
-def silu_extension(torch, device, wl: dict, seed: int, steps: int = 3) -> dict:
-    """Full steps of the same workload with BASELINE's 2 x 128 SiLU score net (extension M1):
-    graph-replayed steps timed with CUDA events (L2 flushed between steps), plus the K-step
-    ISM training loop timed alone for the tensor-core roofline of the hidden GEMMs."""
-    from paper_2603_25832_b200 import _lib
-
-    sw = dict(wl, workload=wl["workload"] + "_silu2x128", net="silu")
-    sim = build_sim(sw, seed, device)
-    n = sw["n"]
+def variant_line(torch, device, wl: dict, seed: int, steps: int = 3) -> dict:
+    """Graph-replayed full steps of another network variant of the same workload (CUDA
+    events, L2 flushed between steps): particle-steps/s and ms per step."""
+    sim = build_sim(wl, seed, device)
+    n = wl["n"]
     for _ in range(3):
         sim.step(0)
     torch.cuda.synchronize()
@@ -306,24 +333,52 @@ def silu_extension(torch, device, wl: dict, seed: int, steps: int = 3) -> dict:
         e1.synchronize()
         total += e0.elapsed_time(e1)
     sim.check()
+    return {"workload": wl["workload"], "net": NET_LABEL[wl.get("net", "softsign")],
+            "value": n * steps / (total * 1e-3), "unit": "particle-steps/s",
+            "ms_per_step": total / steps}
+
+
+def silu_kernel_roofline(torch, device, sim, wl: dict, key: str, reps: int = 10) -> dict:
+    """The SiLU ISM kernel (spic_silu_ism_partials: k_silu + its fixed-order column reduce)
+    timed on the stream it runs on over `reps` launches on the step's own cell-sorted records.
+    achieved = algorithmic GEMM FLOP (3 GEMMs x 2*128*128*4 per particle) / launch time;
+    peak = the measured bf16 tensor peak / 3 (split-BF16 executes three bf16 products per
+    fp32-accurate product)."""
+    from paper_2603_25832_b200.silu_net import _silu_partials
+
+    net, n, L = sim.trainer.net, wl["n"], wl["L"]
+    if hasattr(sim, "ci"):  # the single-GPU engine's cell-sorted records of the last step
+        xv, sw = sim.ci.xv, sim.ci.sw
+    else:  # decomposed run: the same record count on this rank, seeded synthetic values
+        g = torch.Generator(device=device).manual_seed(7)
+        xv = torch.rand(n, 4, device=device, generator=g) * torch.tensor([L, 1, 1, 1], device=device)
+        sw = torch.full((n, 4), L / n, device=device)
+    _silu_partials(net, xv, sw, n, L)
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sim.trainer.run(n, ci=sim.ci, flags=sim.flags)
+    for _ in range(reps):
+        _silu_partials(net, xv, sw, n, L)
     e1.record()
     e1.synchronize()
-    ism_ms = e0.elapsed_time(e1) / max(sw["K"], 1)
+    ms = e0.elapsed_time(e1) / reps
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     bf16 = float(peaks["bf16_tflops"])
-    tc = 3 * SILU_GEMM_FLOP_PER_PARTICLE * n / (ism_ms * 1e-3) / 1e12
-    del _lib
-    return {"workload": sw["workload"], "value": n * steps / (total * 1e-3),
-            "unit": "particle-steps/s", "ms_per_step": total / steps, "ism_step_ms": ism_ms,
-            "tensor_roofline": {"bound": "tensor", "kernel": "spic_silu_ism_partials (k_silu)",
-                                "achieved": tc, "peak": bf16, "unit": "TFLOP/s",
-                                "frac": tc / bf16,
-                                "note": "bf16 tensor FLOP incl. the 3 split passes; ISM step "
-                                        "= partials + ordered reduce + AdamW finalize",
-                                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"}}
+    flop = SILU_GEMM_FLOP_PER_PARTICLE * n
+    achieved = flop / (ms * 1e-3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "silu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(key)
+        except Exception:  # noqa: BLE001
+            traffic = None
+    return {"bound": "tensor", "kernel": "spic_silu_ism_partials (k_silu, tcgen05)",
+            "achieved": achieved, "peak": bf16 / 3.0, "unit": "TFLOP/s",
+            "frac": achieved / (bf16 / 3.0), "traffic": traffic, "flop_per_launch": flop,
+            "launch_ms": ms, "launches_per_step": wl["K"],
+            "bf16_tflops_executed": 3.0 * achieved, "bf16_peak": bf16,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 3 split-BF16 passes"}
 
 
 def config1_microbench(torch, device, n: int = 131072, reps: int = 3) -> dict:
@@ -376,7 +431,6 @@ def build_dist_sim(wl: dict, seed: int, device, world: int):
     from paper_2603_25832_b200.pic import Grid, deposit
     from paper_2603_25832_b200.run import initial_fields
     from paper_2603_25832_b200.sampling import sample_arrays
-    from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
     from paper_2603_25832_b200.state import ParticleEnsemble
 
     wl = dict(wl, n=wl["n"] * world, M=wl["M"] * world, L=wl["L"] * world)
@@ -395,12 +449,7 @@ def build_dist_sim(wl: dict, seed: int, device, world: int):
     rho, J = deposit(pfull, grid)
     fields = initial_fields(cfg, grid, rho, J)
     del pfull
-    if wl["estimator"] == "sbtm":
-        net = MlpScoreNet.init_glorot(cfg.dv, cfg.hidden, rng, device=device)
-        est = SbtmEstimator(net, cfg.L, cfg.K, rng, lr=cfg.lr, weight_decay=cfg.weight_decay,
-                            divergence=cfg.divergence, rademacher=cfg.rademacher)
-    else:
-        est = BlobEstimator(grid, float(wl["bandwidth"]))
+    est = make_estimator_for(wl, cfg, rng, device, grid)
     sim = DistSimulation(x[own], v[own], w[own], own, fields, grid, dt=cfg.dt, nu=cfg.nu,
                          mode=cfg.mode, gamma=cfg.gamma, estimator=est, comm=comm, partition=part,
                          n_global=cfg.n, max_rows=4)
@@ -427,7 +476,7 @@ def main():
                "ms_per_step": 1e3 * line["seconds_per_step"], "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": {"workload": wl["workload"], "n": wl["n"], "M": wl["M"], "K": wl["K"],
-                          "hidden": wl["hidden"]},
+                          "hidden": wl["hidden"], "net": NET_LABEL[wl.get("net", "softsign")]},
                "cpu_baseline": {"value": line["value"], "unit": "particle-steps/s",
                                 "cores": line["cores"], "kind": "port", "sample": line["sample"]},
                "e2e": {"value": line["value"], "unit": "particle-steps/s",
@@ -542,6 +591,13 @@ def main():
         sim.check()
 
     achieved = FLOP_PER_PAIR * live / (coll_avg_ms * 1e-3) / 1e12
+    silu_rf = None
+    if wl["estimator"] == "sbtm" and wl.get("net") == "silu":
+        silu_rf = silu_kernel_roofline(torch, device, sim, wl, args.workload)
+        t = torch.tensor([silu_rf["launch_ms"]], dtype=torch.float64, device=device)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        silu_rf["launch_ms"] = float(t[0])
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "landau_traffic.json")
     if os.path.exists(tfile):
@@ -556,11 +612,7 @@ def main():
         "data": "synthetic (seeded reference sampler; random-init score net, no pretraining)",
         "config": {"workload": wl["workload"], "n_per_gpu": n, "M": wl["M"], "L": wl["L"],
                    "mode": wl["mode"], "estimator": wl["estimator"], "K_ism": wl["K"],
-                   "hidden": wl["hidden"],
-                   "net": ("SiLU 2x128 (BASELINE's MLP, extension M1, tcgen05 hidden GEMMs)"
-                           if wl.get("net") == "silu" else
-                           "softsign 1x{} (reference arch; BASELINE's 2x128 SiLU is extension "
-                           "M1, see silu_extension)".format(wl["hidden"])),
+                   "hidden": wl["hidden"], "net": NET_LABEL[wl.get("net", "softsign")],
                    "divergence": wl["divergence"], "sub_cells": sim.S,
                    "l2": "flushed between timed steps (256 MiB write, outside timed windows)",
                    "parallelism": ("single GPU" if world == 1 else
@@ -569,15 +621,24 @@ def main():
         "pair_interactions_per_s": world * live / (coll_avg_ms * 1e-3),
         "live_pairs_per_step": live,
         "collision_ms": coll_avg_ms,
-        "roofline": {"bound": "fp32", "kernel": "spic_landau (k_landau)", "achieved": achieved,
-                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic,
-                     "flop_per_launch": FLOP_PER_PAIR * live,
-                     "peak_source": "measured in-run: spic_fp32_probe (FFMA2 chains, 592 CTAs)"},
+        "roofline_pair": {"bound": "fp32", "kernel": "spic_landau (k_landau_x2)",
+                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                          "frac": achieved / peak, "traffic": traffic,
+                          "flop_per_launch": FLOP_PER_PAIR * live, "launch_ms": coll_avg_ms,
+                          "launches_per_step": 1,
+                          "peak_source": "measured in-run: spic_fp32_probe (FFMA2 chains, "
+                                         "592 CTAs)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    # `roofline` = the kernel with the largest share of the step: with the SiLU net the K = 10
+    # ISM launches (tensor cores) edge out the pair kernel; otherwise the pair kernel
+    out["roofline"] = out["roofline_pair"]
+    if silu_rf is not None:
+        out["roofline_silu"] = silu_rf
+        if silu_rf["launch_ms"] * silu_rf["launches_per_step"] > coll_avg_ms:
+            out["roofline"] = silu_rf
     if world == 1:
         try:
             mb = config1_microbench(torch, device)
@@ -585,11 +646,14 @@ def main():
             out["config1_microbench"] = mb
         except Exception as exc:  # noqa: BLE001
             out["config1_microbench"] = {"error": str(exc)}
-    if world == 1 and wl["estimator"] == "sbtm" and wl.get("net") != "silu":
+    if world == 1 and args.workload + "ss" in WORKLOADS:
+        # the same config with the reference's own softsign network (like-for-like with the
+        # reference arm, which has no SiLU network)
         try:
-            out["silu_extension"] = silu_extension(torch, device, wl, args.seed)
+            out["reference_net_variant"] = variant_line(torch, device,
+                                                        WORKLOADS[args.workload + "ss"], args.seed)
         except Exception as exc:  # noqa: BLE001
-            out["silu_extension"] = {"error": str(exc)}
+            out["reference_net_variant"] = {"error": str(exc)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line = cpu_baseline_line(wl, args.seed)

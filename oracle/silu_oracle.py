@@ -67,14 +67,16 @@ def inputs(x, v, L: float) -> np.ndarray:
     return np.concatenate([(x / L)[:, None], v], axis=1)
 
 
-def forward(params, u, H: int):
-    """s [n][3] and the divergence div [n]."""
+def forward(params, u, H: int, with_div: bool = True):
+    """s [n][3] and the divergence div [n] (None unless with_div)."""
     W1, b1, W2, b2, W3, b3 = split(params, H)
     a1 = u @ W1.T + b1
     h1, d1, _ = _silu_terms(a1)
     a2 = h1 @ W2.T + b2
     h2, d2, _ = _silu_terms(a2)
     s = h2 @ W3.T + b3
+    if not with_div:
+        return s, None
     div = np.zeros(u.shape[0])
     for k in range(3):
         c2 = (d1 * W1[:, 1 + k]) @ W2.T

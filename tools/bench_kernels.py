@@ -53,7 +53,14 @@ def main():
     out["bin_ms"] = timeit(lambda: build_cell_index(p, g, sim.S, out=ci))
     out["deposit_field_ms"] = timeit(lambda: deposit_from_index(
         ci, p, g, fields=sim.f, field_mode=FIELD_VPL, dt=0.0, diag_out=sim.diag[3, 0:3], flags=sim.flags))
-    if sim.trainer is not None:
+    if sim.trainer is not None and getattr(sim.trainer.net, "arch", "") == "silu":
+        from paper_2603_25832_b200.silu_net import _silu_partials
+
+        tr = sim.trainer
+        out["ism_partials_ms"] = timeit(lambda: _silu_partials(tr.net, ci.xv, ci.sw, n, tr.L))
+        out["forward_ms"] = timeit(lambda: sim.est.estimate_sorted(ci, n))
+        out["sbtm_update_K_ms"] = timeit(lambda: tr.run(n, ci=ci, flags=sim.flags), reps=3)
+    elif sim.trainer is not None:
         from paper_2603_25832_b200.score import DIV_EXACT, _finalize, _partials
 
         net, tr = sim.trainer.net, sim.trainer
