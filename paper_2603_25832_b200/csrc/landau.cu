@@ -498,52 +498,27 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   const bool minimg = M <= 2;
   const bool uw = uniform_w > 0.f;
   // packed f32x2 kernel for the dominant case (dv = 3, M >= 3, Coulomb gamma = -3)
+  // SPIC_LANDAU_VARIANT=s forces the scalar kernel (A/B checks); the packed configuration
+  // (2 packed pairs per thread, 4 CTAs/SM, 2-way j unroll) won a sweep of RP 1..3, 2..8
+  // CTAs/SM and unroll 1/2/4 on config 2
   const char* var = getenv("SPIC_LANDAU_VARIANT");
   const bool packed = dv == 3 && gm == 0 && !(var && var[0] == 's');
-  // experiment knob: SPIC_LANDAU_VARIANT = s (scalar) | 1 (RP1) | 3 (RP3) | 4 (RP2, 4 CTA/SM)
-  const int cfg = (var && var[0] >= '1' && var[0] <= '9') ? var[0] - '0' : 2;
-  const int rp = (cfg == 1 || cfg == 9) ? 1 : (cfg == 3 ? 3 : 2);
+  constexpr int rp = kLandauRP;
   const int TI = packed ? kLandauNT * 2 * rp : kLandauTI;
   k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start, c_lo, c_hi); spic::count_launch();
   SPIC_CHECK_LAUNCH();
   dim3 grid((unsigned)(n / TI + M + 1), (unsigned)nsplit);
   if (packed) {
-#define SPIC_X2(RP_, MB_) SPIC_X2U(RP_, MB_, 2)
-#define SPIC_X2U(RP_, MB_, U_)                                                               \
-  do {                                                                                        \
-    if (minimg) {                                                                             \
-      if (uw)                                                                                 \
-        k_landau_x2<RP_, MB_, true, true, U_><<<grid, kLandauNT, 0, st>>>(                    \
-            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
-            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
-      else                                                                                    \
-        k_landau_x2<RP_, MB_, false, true, U_><<<grid, kLandauNT, 0, st>>>(                   \
-            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
-            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
-    } else {                                                                                  \
-      if (uw)                                                                                 \
-        k_landau_x2<RP_, MB_, true, false, U_><<<grid, kLandauNT, 0, st>>>(                   \
-            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
-            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
-      else                                                                                    \
-        k_landau_x2<RP_, MB_, false, false, U_><<<grid, kLandauNT, 0, st>>>(                  \
-            (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S,    \
-            (float)L, ie, ie2, wie, wie2, nsplit, Upart, n);                                  \
-    }                                                                                         \
-  } while (0)
-    switch (cfg) {
-      case 1: SPIC_X2(1, 6); break;
-      case 3: SPIC_X2(3, 2); break;
-      case 4: SPIC_X2(2, 3); break;
-      case 5: SPIC_X2(2, 5); break;
-      case 6: SPIC_X2U(2, 4, 4); break;
-      case 7: SPIC_X2U(2, 4, 1); break;
-      case 8: SPIC_X2U(2, 5, 1); break;
-      case 9: SPIC_X2U(1, 8, 2); break;
-      default: SPIC_X2(2, 4); break;
+#define SPIC_X2(MINIMG_, UW_)                                                                 \
+  k_landau_x2<kLandauRP, 4, UW_, MINIMG_, 2><<<grid, kLandauNT, 0, st>>>(                     \
+      (const float4*)xv, (const float4*)sw, cell_start, sub_start, tile_start, M, S, (float)L, \
+      ie, ie2, wie, wie2, nsplit, Upart, n)
+    if (minimg) {
+      if (uw) SPIC_X2(true, true); else SPIC_X2(true, false);
+    } else {
+      if (uw) SPIC_X2(false, true); else SPIC_X2(false, false);
     }
 #undef SPIC_X2
-#undef SPIC_X2U
     spic::count_launch();
   } else if (dv == 3) {
     if (minimg)
