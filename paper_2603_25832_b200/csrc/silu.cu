@@ -50,7 +50,13 @@ struct SiluShared {
   uint64_t bar[2];  // [0]: G1 / G2 done, [1]: G3 done (X, Y free again)
   uint32_t tmem;
 };
-constexpr size_t kSiluSmem = 6 * umma::kTileBytes + sizeof(SiluShared) + 1024;
+// W2 and B = W2 (.) C as 128-row operand tiles (hi, lo); X and Y as 64-row tiles (hi, lo):
+// rows 0..31 = the chunk's primal columns, rows 32..63 = its divergence columns
+constexpr uint32_t kXHalf = 2 * kCP * 128;        // 64-row tile half (8 KB)
+constexpr uint32_t kXTile = 2 * kXHalf;           // 16 KB
+constexpr size_t kSiluTiles = 4 * umma::kTileBytes + 4 * kXTile;
+constexpr size_t kSiluSmem = kSiluTiles + sizeof(SiluShared) + 1024;
+static_assert(6 * umma::kTileBytes <= kSiluTiles, "self-test tiles fit");
 
 // 1024-B aligned start inside the dynamic shared buffer (SWIZZLE_128B atoms). The offset is
 // applied to the __shared__ array itself so the compiler keeps shared-space (LDS/STS)
@@ -81,7 +87,7 @@ __device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one warpg
   asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
 }
 
-// Split-BF16 store of one value into a hi tile (at addr) and its lo tile (addr + 32 KB).
+// Split-BF16 store of one value into a 64-row X / Y tile: hi at addr, lo at addr + kXTile.
 // addr = the thread's column base for the row's (r & 7) swizzle phase + r * 128; with the
 // particle loops unrolled the row part is a constant that folds into the STS immediate.
 __device__ __forceinline__ void st_split(uint32_t addr, float x) {
@@ -93,16 +99,26 @@ __device__ __forceinline__ void st_split(uint32_t addr, float x) {
       "sub.rn.f32 r, %1, hf;\n"
       "cvt.rn.bf16.f32 l16, r;\n"
       "st.shared.b16 [%0], h16;\n"
-      "st.shared.b16 [%0+32768], l16;\n}\n" ::"r"(addr),
-      "f"(x)
+      "st.shared.b16 [%0+%2], l16;\n}\n" ::"r"(addr),
+      "f"(x), "n"(kXTile)
       : "memory");
 }
 
 // One CTA per SM, four warpgroups. Thread (h, warpgroup g) owns hidden unit h (its TMEM lane)
 // for particles 8g..8g+7 of each 32-particle chunk; one thread issues the CTA's GEMMs.
+//
+// The exact divergence is carried by one extra column per particle instead of three forward
+// tangents: with C[h][h'] = sum_k W3[k][h] W1[h'][1+k] and B = W2 (.) C (elementwise),
+//   div = d2 . (B d1),  d1 = silu'(a1), d2 = silu'(a2)
+// so per chunk (columns: 32 primal + 32 divergence)
+//   G1  [a2 - b2 | e]     = [W2 h1 | B d1]
+//   G2  [dh1 | f]         = [W2^T da2 | B^T y2],   y2 = 2w d2 (the dL/de column)
+//   G3  dW2 += da2 h1^T,   M += y2 d1^T             (TMEM-resident over the CTA's chunks)
+// and at the end of the kernel dW2 += C (.) M, dW3[k][h] += sum_h' W1[h'][1+k] (W2 (.) M)[h][h'],
+// dW1[h'][1+k] += sum_h W3[k][h] (W2 (.) M)[h][h'] (the tangent terms, once per CTA).
 // MODE 0: forward only (scores into sw_out lanes 0..2, weight lane kept); 1: ISM partials
 // (exact divergence); 2: weighted MSE partials to a target score (pretraining, ref:
-// score.py:254-300 applied to this network; no divergence, so the tangent columns are zero).
+// score.py:254-300 applied to this network; no divergence columns).
 // Inputs: cell-sorted records (xv != NULL) or pid-order planes x, v[3][ldv], w read through
 // idx (nullable) together with the target planes Z[3][ldz].
 struct SiluInputs {
@@ -125,21 +141,22 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
                                                  float4* __restrict__ sw_out,
                                                  double* __restrict__ part) {
   constexpr bool ISM = MODE != 0;  // training modes (loss + gradient partials)
+  constexpr bool DIV = MODE == 1;  // divergence columns
   const float4* __restrict__ xv = in.xv;
   const float4* __restrict__ sw = in.sw;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
   uint8_t* W2h = base;
   uint8_t* W2l = base + 1 * umma::kTileBytes;
-  uint8_t* Xh = base + 2 * umma::kTileBytes;
-  uint8_t* Xl = base + 3 * umma::kTileBytes;
-  uint8_t* Yh = base + 4 * umma::kTileBytes;
-  uint8_t* Yl = base + 5 * umma::kTileBytes;
-  SiluShared& S = *reinterpret_cast<SiluShared*>(base + 6 * umma::kTileBytes);
-  constexpr int kY = 2 * (int)umma::kTileBytes;  // Y tiles sit 64 KB after the X tiles
+  uint8_t* Bh = base + 2 * umma::kTileBytes;
+  uint8_t* Bl = base + 3 * umma::kTileBytes;
+  uint8_t* Xh = base + 4 * umma::kTileBytes;  // lo at + kXTile, Y hi at + 2 kXTile
+  SiluShared& S = *reinterpret_cast<SiluShared*>(base + kSiluTiles);
+  constexpr uint32_t kY = 2 * kXTile;
+  constexpr uint32_t kDivRows = kCP * 128;  // byte offset of the divergence rows
 
   const int tid = threadIdx.x, h = tid & (kH - 1), wg = tid >> 7, lane = tid & 31;
-  const int quarter = (tid >> 5) & 3;
+  const int quarter = (tid >> 5) & 3, wtid = tid & 127;
   const float* W1 = params;
   const float* b1 = W1 + 4 * kH;
   const float* W2 = b1 + kH;
@@ -147,7 +164,15 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const float* W3 = b2 + kH;
   const float* b3 = W3 + 3 * kH;
 
-  for (int e = tid; e < kH * kH; e += kNT) umma::store_split(W2h, W2l, e / kH, e % kH, W2[e]);
+  for (int e = tid; e < kH * kH; e += kNT) {
+    const int r = e / kH, cc = e % kH;  // W2[r][cc]
+    umma::store_split(W2h, W2l, r, cc, W2[e]);
+    if (DIV) {
+      const float Crc = fmaf(W3[2 * kH + r], W1[cc * 4 + 3],
+                             fmaf(W3[kH + r], W1[cc * 4 + 2], W3[r] * W1[cc * 4 + 1]));
+      umma::store_split(Bh, Bl, r, cc, W2[e] * Crc);
+    }
+  }
   float w1[4], w3[3];
 #pragma unroll
   for (int i = 0; i < 4; ++i) w1[i] = W1[h * 4 + i];
@@ -166,12 +191,15 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   umma::fence_after();
   const uint32_t tm = S.tmem;
   const uint32_t tl = tm + ((uint32_t)(quarter * 32) << 16);  // this warp's TMEM lanes
-  const uint32_t sW2h = smem_u32(W2h), sW2l = smem_u32(W2l), sXh = smem_u32(Xh),
-                 sXl = smem_u32(Xl), sYh = smem_u32(Yh), sYl = smem_u32(Yl);
-  // store bases for this thread's column h and its rows 32g + (0..31), one per (row & 7)
+  const uint32_t sW2h = smem_u32(W2h), sW2l = smem_u32(W2l), sBh = smem_u32(Bh),
+                 sBl = smem_u32(Bl), sXh = smem_u32(Xh), sXl = sXh + kXTile,
+                 sYh = sXh + kY, sYl = sYh + kXTile;
+  // TMEM columns: D1 = [a2 - b2 (32) | e (32)], D2 = [dh1 (32) | f (32)], D3 = dW2, D4 = M
+  constexpr uint32_t cD1 = 0, cD2 = 64, cD3 = 128, cD4 = 256;
+  // store bases for this thread's column h and its rows 8g + (0..7), one per (row & 7)
   uint32_t rb[8];
   {
-    const uint32_t col = sXh + (uint32_t)((h >> 6) * 16384 + (h & 7) * 2 + 4096 * wg);
+    const uint32_t col = sXh + (uint32_t)((h >> 6) * kXHalf + (h & 7) * 2 + 1024 * wg);
     const int hc = (h >> 3) & 7;
 #pragma unroll
     for (int m = 0; m < 8; ++m) rb[m] = col + (uint32_t)((hc ^ m) << 4);
@@ -182,10 +210,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   uint32_t phase = 0, phase3 = 0;
   bool first = true;
   const int64_t nchunks = (n + kCP - 1) / kCP;
-  const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk
-  const uint32_t c0 = 4 * p0;  // ... and their first GEMM column
+  const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk (= GEMM columns)
 
-  const int wtid = tid & 127;  // thread index inside the warpgroup
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     // each warpgroup loads, reduces and scores its own 8 particles: only the GEMM issue points
     // need the whole CTA, everything else synchronises one warpgroup (named barrier)
@@ -212,30 +238,31 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       if (MODE == 2) S.t[pl] = t;
     }
     wg_sync(wg);
-    if (ISM && !first) {  // the previous chunk's weight-gradient GEMM still reads X and Y
+    if (ISM && !first) {  // the previous chunk's weight-gradient GEMMs still read X and Y
       umma::wait_mma(&S.bar[1], phase3);
       phase3 ^= 1;
       umma::fence_after();
     }
 
-    // F1: layer 1 and its tangents -> X = [h1 | t1_0 | t1_1 | t1_2] (rows 4p + j, column h)
+    // F1: layer 1 -> X rows p (h1) and 32 + p (d1 = silu'(a1)), column h
 #pragma unroll
     for (int i = 0; i < kPPT; ++i) {
       const float4 u = S.u[p0 + i];
       const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
       const float sg = sigmoid(a);
-      const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
-      st_split(rb[(4 * i + 0) & 7] + ((4 * i + 0) * 128), a * sg);
-      st_split(rb[(4 * i + 1) & 7] + ((4 * i + 1) * 128), d1 * w1[1]);
-      st_split(rb[(4 * i + 2) & 7] + ((4 * i + 2) * 128), d1 * w1[2]);
-      st_split(rb[(4 * i + 3) & 7] + ((4 * i + 3) * 128), d1 * w1[3]);
+      st_split(rb[i] + i * 128, a * sg);
+      if (DIV) st_split(rb[i] + kDivRows + i * 128, sg * fmaf(a, 1.f - sg, 1.f));
     }
     fence_proxy_async();
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
     if (tid == 0) {
-      umma::gemm_split<false, false>(tm + kColD1, sW2h, sW2l, sXh, sXl, false);
+      umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
+                                                            false);
+      if (DIV)
+        umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(
+            tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);
       umma::commit(&S.bar[0]);
     }
     umma::wait_mma(&S.bar[0], phase);
@@ -244,22 +271,21 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 
     // F2a: s and div partials over this thread's h, reduced across the warp
     {
-      float v[32];
-      umma::tmem_ld32(tl + kColD1 + c0, v);
+      float va[8], ve[8];
+      umma::tmem_ld8(tl + cD1 + p0, va);
+      if (DIV) umma::tmem_ld8(tl + cD1 + kCP + p0, ve);
       float val[32];
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
-        const float a2 = v[4 * pp] + bb2;
+        const float a2 = va[pp] + bb2;
         const float sg = sigmoid(a2);
         const float h2 = a2 * sg;
-        const float d2 = sg * fmaf(a2, 1.f - sg, 1.f);
         val[4 * pp + 0] = w3[0] * h2;
         val[4 * pp + 1] = w3[1] * h2;
         val[4 * pp + 2] = w3[2] * h2;
-        val[4 * pp + 3] =
-            d2 * fmaf(w3[2], v[4 * pp + 3], fmaf(w3[1], v[4 * pp + 2], w3[0] * v[4 * pp + 1]));
+        val[4 * pp + 3] = DIV ? sg * fmaf(a2, 1.f - sg, 1.f) * ve[pp] : 0.f;
       }
-      S.red[quarter][c0 + lane] = transpose_reduce32(val, lane);
+      S.red[quarter][4 * p0 + lane] = transpose_reduce32(val, lane);
     }
     wg_sync(wg);
     if (wtid < kPPT) {
@@ -297,32 +323,31 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     }
     wg_sync(wg);
 
-    // F2b: reverse through layer 2 -> Y = [da2 | dc2_0 | dc2_1 | dc2_2]; dW3, db2
+    // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
     {
       float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
-      float v[32];
-      umma::tmem_ld32(tl + kColD1 + c0, v);
+      float va[8], ve[8];
+      umma::tmem_ld8(tl + cD1 + p0, va);
+      if (DIV) umma::tmem_ld8(tl + cD1 + kCP + p0, ve);
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
         const float4 G = S.gs[p0 + pp];
-        const float a2 = v[4 * pp] + bb2;
+        const float a2 = va[pp] + bb2;
         const float sg = sigmoid(a2);
         const float h2 = a2 * sg;
         const float d2 = sg * fmaf(a2, 1.f - sg, 1.f);
-        const float e2 = sg * (1.f - sg) * fmaf(a2, 1.f - 2.f * sg, 2.f);
-        const float cc0 = v[4 * pp + 1], cc1 = v[4 * pp + 2], cc2 = v[4 * pp + 3];
         const float dh2 = fmaf(w3[2], G.z, fmaf(w3[1], G.y, w3[0] * G.x));
-        const float qv = fmaf(w3[2], cc2, fmaf(w3[1], cc1, w3[0] * cc0));
-        const float da2 = fmaf(d2, dh2, G.w * e2 * qv);
-        const float twd2 = G.w * d2;
-        aw3[0] += fmaf(G.x, h2, twd2 * cc0);
-        aw3[1] += fmaf(G.y, h2, twd2 * cc1);
-        aw3[2] += fmaf(G.z, h2, twd2 * cc2);
+        float da2 = d2 * dh2;
+        if (DIV) {
+          const float e2 = sg * (1.f - sg) * fmaf(a2, 1.f - 2.f * sg, 2.f);
+          da2 = fmaf(e2, G.w * ve[pp], da2);
+        }
+        aw3[0] = fmaf(G.x, h2, aw3[0]);
+        aw3[1] = fmaf(G.y, h2, aw3[1]);
+        aw3[2] = fmaf(G.z, h2, aw3[2]);
         ab2 += da2;
-        st_split(rb[(4 * pp + 0) & 7] + (kY + (4 * pp + 0) * 128), da2);
-        st_split(rb[(4 * pp + 1) & 7] + (kY + (4 * pp + 1) * 128), twd2 * w3[0]);
-        st_split(rb[(4 * pp + 2) & 7] + (kY + (4 * pp + 2) * 128), twd2 * w3[1]);
-        st_split(rb[(4 * pp + 3) & 7] + (kY + (4 * pp + 3) * 128), twd2 * w3[2]);
+        st_split(rb[pp] + kY + pp * 128, da2);
+        if (DIV) st_split(rb[pp] + kY + kDivRows + pp * 128, G.w * d2);
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) gw3[k] += (double)aw3[k];
@@ -333,9 +358,18 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     __syncthreads();
     umma::fence_after();
     if (tid == 0) {
-      umma::gemm_split<true, false>(tm + kColD2, sW2h, sW2l, sYh, sYl, false);  // W2^T Y
+      umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(tm + cD2, sW2h, sW2l, sYh, sYl,
+                                                           false);  // W2^T da2
+      if (DIV)
+        umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(
+            tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
       umma::commit(&S.bar[0]);
-      umma::gemm_split<true, true>(tm + kColD3, sYh, sYl, sXh, sXl, !first);     // Y^T X
+      umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(tm + cD3, sYh, sYl, sXh, sXl,
+                                                                  !first);  // da2 h1^T
+      if (DIV)
+        umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(
+            tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
+            !first);  // y2 d1^T
       umma::commit(&S.bar[1]);  // overlaps F3 and the next chunk's record loads
     }
     first = false;
@@ -343,25 +377,25 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     phase ^= 1;
     umma::fence_after();
 
-    // F3: reverse through layer 1 -> dW1, db1
+    // F3: reverse through layer 1 -> dW1 (input part), db1
     {
       float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
-      float v[32];
-      umma::tmem_ld32(tl + kColD2 + c0, v);
+      float vd[8], vf[8];
+      umma::tmem_ld8(tl + cD2 + p0, vd);
+      if (DIV) umma::tmem_ld8(tl + cD2 + kCP + p0, vf);
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
         const float4 u = S.u[p0 + pp];
         const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
         const float sg = sigmoid(a);
         const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
-        const float e1 = sg * (1.f - sg) * fmaf(a, 1.f - 2.f * sg, 2.f);
-        const float dh1 = v[4 * pp], t0 = v[4 * pp + 1], t1 = v[4 * pp + 2], t2 = v[4 * pp + 3];
-        const float da1 = fmaf(d1, dh1, e1 * fmaf(w1[3], t2, fmaf(w1[2], t1, w1[1] * t0)));
+        float da1 = d1 * vd[pp];
+        if (DIV) da1 = fmaf(sg * (1.f - sg) * fmaf(a, 1.f - 2.f * sg, 2.f), vf[pp], da1);
         ab1 += da1;
-        aw1[0] += da1 * u.x;
-        aw1[1] += fmaf(da1, u.y, d1 * t0);
-        aw1[2] += fmaf(da1, u.z, d1 * t1);
-        aw1[3] += fmaf(da1, u.w, d1 * t2);
+        aw1[0] = fmaf(da1, u.x, aw1[0]);
+        aw1[1] = fmaf(da1, u.y, aw1[1]);
+        aw1[2] = fmaf(da1, u.z, aw1[2]);
+        aw1[3] = fmaf(da1, u.w, aw1[3]);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) gw1[i] += (double)aw1[i];
@@ -376,37 +410,45 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       umma::wait_mma(&S.bar[1], phase3);
       umma::fence_after();
     }
+    __syncthreads();  // every warpgroup is done with the X / Y tiles before they are reused
     const int64_t width = 1 + silu_params(kH);
     const int64_t oW1 = 1, ob1 = oW1 + 4 * kH, oW2 = ob1 + kH, ob2 = oW2 + kH * kH,
                   oW3 = ob2 + kH, ob3 = oW3 + 3 * kH;
     double* row = part + (size_t)blockIdx.x * width;
-    // dW2 from TMEM (row h, columns h'); warpgroup g takes columns 32g..32g+31
+    // dW2 = D3 + C (.) M (row h, columns h'); warpgroup g takes columns 32g..32g+31. The
+    // tangent terms of dW3 (row sums of (W2 (.) M) W1[:,1+k]) and dW1 (column sums of
+    // W3[k] (W2 (.) M)) go through shared memory: WM = W2 (.) M as float [h][h'].
+    float* WM = reinterpret_cast<float*>(Xh);  // 64 KB: the X and Y tiles are free now
+    float tw3[3] = {0.f, 0.f, 0.f};
     {
-      float v[32];
-      umma::tmem_ld32(tl + kColD3 + (uint32_t)(32 * wg), v);
+      float v[32], m[32];
+      umma::tmem_ld32(tl + cD3 + (uint32_t)(32 * wg), v);
+      if (DIV) umma::tmem_ld32(tl + cD4 + (uint32_t)(32 * wg), m);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) row[oW2 + h * kH + 32 * wg + i] = first ? 0.0 : (double)v[i];
+      for (int i = 0; i < 32; ++i) {
+        const int hp = 32 * wg + i;
+        double g = first ? 0.0 : (double)v[i];
+        if (DIV && !first) {
+          const float Chh = fmaf(w3[2], W1[hp * 4 + 3], fmaf(w3[1], W1[hp * 4 + 2], w3[0] * W1[hp * 4 + 1]));
+          const float wm = W2[h * kH + hp] * m[i];
+          g += (double)(Chh * m[i]);
+          WM[h * kH + hp] = wm;
+          tw3[0] = fmaf(W1[hp * 4 + 1], wm, tw3[0]);
+          tw3[1] = fmaf(W1[hp * 4 + 2], wm, tw3[1]);
+          tw3[2] = fmaf(W1[hp * 4 + 3], wm, tw3[2]);
+        } else if (DIV) {
+          WM[h * kH + hp] = 0.f;
+        }
+        row[oW2 + h * kH + hp] = g;
+      }
     }
-    // per-h sums over the four warpgroups in a fixed order (operand tiles are free now)
-    double* comb = reinterpret_cast<double*>(Xh);  // [4][kH][9]
-    double* mine = comb + (size_t)(wg * kH + h) * 9;
+    // per-h sums over the four warpgroups in a fixed order (in the free W2 tiles)
+    double* comb = reinterpret_cast<double*>(W2h);  // [4][kH][12] + [4][4]
+    double* mine = comb + (size_t)(wg * kH + h) * 12;
     mine[0] = gw1[0]; mine[1] = gw1[1]; mine[2] = gw1[2]; mine[3] = gw1[3];
     mine[4] = gb1; mine[5] = gb2; mine[6] = gw3[0]; mine[7] = gw3[1]; mine[8] = gw3[2];
-    __syncthreads();
-    if (wg == 0) {
-      double t[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k)
-        t[k] = (comb[(0 * kH + h) * 9 + k] + comb[(1 * kH + h) * 9 + k]) +
-               (comb[(2 * kH + h) * 9 + k] + comb[(3 * kH + h) * 9 + k]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) row[oW1 + 4 * h + i] = t[i];
-      row[ob1 + h] = t[4];
-      row[ob2 + h] = t[5];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) row[oW3 + k * kH + h] = t[6 + k];
-    }
-    double* lcomb = comb + 4 * kH * 9;  // [4 warpgroups][loss, gb3]
+    mine[9] = tw3[0]; mine[10] = tw3[1]; mine[11] = tw3[2];
+    double* lcomb = comb + 4 * kH * 12;  // [4 warpgroups][loss, gb3]
     if (wtid < 32) {
       loss = warp_sum(loss);
 #pragma unroll
@@ -418,6 +460,29 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       }
     }
     __syncthreads();
+    if (wg == 0) {
+      double t[12];
+#pragma unroll
+      for (int k = 0; k < 12; ++k)
+        t[k] = (comb[(0 * kH + h) * 12 + k] + comb[(1 * kH + h) * 12 + k]) +
+               (comb[(2 * kH + h) * 12 + k] + comb[(3 * kH + h) * 12 + k]);
+      row[oW1 + 4 * h + 0] = t[0];
+      row[ob1 + h] = t[4];
+      row[ob2 + h] = t[5];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) row[oW3 + k * kH + h] = t[6 + k] + t[9 + k];
+      // dW1[h][1+k]: input part + sum over rows h'' of W3[k][h''] WM[h''][h] (column h)
+      float cw[3] = {0.f, 0.f, 0.f};
+      if (DIV)
+        for (int r = 0; r < kH; ++r) {
+          const float wm = WM[r * kH + h];
+          cw[0] = fmaf(W3[r], wm, cw[0]);
+          cw[1] = fmaf(W3[kH + r], wm, cw[1]);
+          cw[2] = fmaf(W3[2 * kH + r], wm, cw[2]);
+        }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) row[oW1 + 4 * h + 1 + k] = t[1 + k] + (double)cw[k];
+    }
     if (tid == 0) {
       row[0] = (lcomb[0] + lcomb[4]) + (lcomb[8] + lcomb[12]);
 #pragma unroll

@@ -27,13 +27,21 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
 }
-// K-major view; K-step ks covers columns 16ks..16ks+15 (32 B inside a 128-B swizzle row)
-__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int ks) {
-  return sdesc(tile + (uint32_t)((ks >> 2) * 16384 + (ks & 3) * 32), 16, 1024);
+// A tile of R rows x 128 bf16 columns is two 64-column halves of R * 128 B ("half" below;
+// 16 KB for R = 128). K-major view; K-step ks covers columns 16ks..16ks+15 (32 B inside a
+// 128-B swizzle row)
+__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int ks, uint32_t half = 16384) {
+  return sdesc(tile + (uint32_t)(ks >> 2) * half + (uint32_t)((ks & 3) * 32), 16, 1024);
 }
 // MN-major view; K-step ks covers rows 16ks..16ks+15; MN groups of 64 are the two halves
-__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int ks) {
-  return sdesc(tile + (uint32_t)(ks * 2048), 16384, 1024);
+__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int ks, uint32_t half = 16384) {
+  return sdesc(tile + (uint32_t)(ks * 2048), half, 1024);
+}
+
+// byte offset of element (r, c) inside an R-row tile (half = R * 128)
+__device__ __forceinline__ uint32_t tile_off_h(int r, int c, uint32_t half) {
+  return (uint32_t)(c >> 6) * half +
+         (uint32_t)(r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4) + (c & 7) * 2);
 }
 
 // instruction descriptor: kind::f16, A/B bf16, D f32, M = 128, N, operand majors
@@ -53,16 +61,17 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
 // D[128 x N] (+)= A * B over K = 16 * KSTEPS with split-BF16 operands:
 // Ahi*Bhi + Ahi*Blo + Alo*Bhi (~2^-16 relative per product; float32 accumulation in TMEM).
 // Operand addresses are tile (sub-)block starts. Issued by one thread.
-template <bool A_MN, bool B_MN, int N = 128, int KSTEPS = 8>
+template <bool A_MN, bool B_MN, int N = 128, int KSTEPS = 8, uint32_t AH = 16384,
+          uint32_t BH = 16384>
 __device__ __forceinline__ void gemm_split(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
                                            uint32_t b_hi, uint32_t b_lo, bool accumulate) {
   constexpr uint32_t id = idesc_bf16(A_MN ? 1u : 0u, B_MN ? 1u : 0u, (uint32_t)N);
 #pragma unroll
   for (int ks = 0; ks < KSTEPS; ++ks) {
-    const uint64_t ah = A_MN ? desc_mn(a_hi, ks) : desc_k(a_hi, ks);
-    const uint64_t al = A_MN ? desc_mn(a_lo, ks) : desc_k(a_lo, ks);
-    const uint64_t bh = B_MN ? desc_mn(b_hi, ks) : desc_k(b_hi, ks);
-    const uint64_t bl = B_MN ? desc_mn(b_lo, ks) : desc_k(b_lo, ks);
+    const uint64_t ah = A_MN ? desc_mn(a_hi, ks, AH) : desc_k(a_hi, ks, AH);
+    const uint64_t al = A_MN ? desc_mn(a_lo, ks, AH) : desc_k(a_lo, ks, AH);
+    const uint64_t bh = B_MN ? desc_mn(b_hi, ks, BH) : desc_k(b_hi, ks, BH);
+    const uint64_t bl = B_MN ? desc_mn(b_lo, ks, BH) : desc_k(b_lo, ks, BH);
     mma(d_tmem, ah, bh, id, (accumulate || ks > 0) ? 1u : 0u);
     mma(d_tmem, ah, bl, id, 1u);
     mma(d_tmem, al, bh, id, 1u);
@@ -128,6 +137,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&f)[32]) {
       : "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
+}
+
+// 8 consecutive float32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&f)[8]) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]);
 }
 
 // split x into bf16 hi + lo (x ~= hi + lo to ~2^-17 relative) and store both tiles
