@@ -71,7 +71,8 @@ for _k in ("c0", "c2", "c4"):
                                 workload=WORKLOADS[_k]["workload"] + "_reference_softsign_net")
 NET_LABEL = {"silu": "SiLU 2x128 (BASELINE's MLP; extension M1, tcgen05 split-BF16 hidden GEMMs)",
              "softsign": "softsign 1x128 (the reference's network)"}
-SILU_GEMM_FLOP_PER_PARTICLE = 3 * 2 * 128 * 128 * 4  # G1, G2, G3 per ISM step (fp32-equivalent)
+# per particle per ISM step: G1 [W2 h1 | B d1], G2 [W2^T da2 | B^T y2], G3 [da2 h1^T, y2 d1^T]
+SILU_GEMM_FLOP_PER_PARTICLE = 3 * 2 * (2 * 128 * 128)
 
 
 def parse_args():
@@ -341,7 +342,7 @@ def variant_line(torch, device, wl: dict, seed: int, steps: int = 3) -> dict:
 def silu_kernel_roofline(torch, device, sim, wl: dict, key: str, reps: int = 10) -> dict:
     """The SiLU ISM kernel (spic_silu_ism_partials: k_silu + its fixed-order column reduce)
     timed on the stream it runs on over `reps` launches on the step's own cell-sorted records.
-    achieved = algorithmic GEMM FLOP (3 GEMMs x 2*128*128*4 per particle) / launch time;
+    achieved = algorithmic GEMM FLOP (3 x 2 x 2*128*128 per particle) / launch time;
     peak = the measured bf16 tensor peak / 3 (split-BF16 executes three bf16 products per
     fp32-accurate product)."""
     from paper_2603_25832_b200.silu_net import _silu_partials

@@ -32,7 +32,7 @@ __global__ void k_ism_reduce_cols(const double* __restrict__ part, int rows, int
 namespace {
 
 constexpr int kH = 128;       // hidden width of the tensor-core path
-constexpr int kCP = 32;       // particles per chunk (GEMM N = 4 * kCP = 128)
+constexpr int kCP = 48;       // particles per chunk (GEMM N of the layer GEMMs)
 constexpr int kNWG = 4;       // warpgroups per CTA; thread = (hidden unit h, particle slice)
 constexpr int kNT = 128 * kNWG;
 constexpr int kPPT = kCP / kNWG;  // particles per thread per chunk
@@ -45,15 +45,17 @@ struct SiluShared {
   float4 u[kCP];
   float w[kCP];
   float4 gs[kCP];              // ISM: (2w s, 2w); MSE: (2w' (s - t), 0)
-  float4 t[kCP];               // MSE target
-  float red[4][4 * kCP];       // per-warp-quarter partial (s0, s1, s2, div) per particle
   uint64_t bar[2];  // [0]: G1 / G2 done, [1]: G3 done (X, Y free again)
   uint32_t tmem;
 };
 // W2 and B = W2 (.) C as 128-row operand tiles (hi, lo); X and Y as 64-row tiles (hi, lo):
 // rows 0..31 = the chunk's primal columns, rows 32..63 = its divergence columns
-constexpr uint32_t kXHalf = 2 * kCP * 128;        // 64-row tile half (8 KB)
-constexpr uint32_t kXTile = 2 * kXHalf;           // 16 KB
+constexpr uint32_t kXHalf = 2 * kCP * 128;        // 96-row tile half (12 KB)
+constexpr uint32_t kXTile = 2 * kXHalf;           // 24 KB
+// per-warp-quarter partials (s0, s1, s2, div) per particle and the MSE targets live in the Y
+// tile while it is free (after the previous chunk's G2 / G3, before this chunk's F2b)
+constexpr uint32_t kRedBytes = 4 * 4 * kCP * sizeof(float);
+static_assert(kRedBytes + kCP * sizeof(float4) <= kXTile, "scratch fits the Y tile");
 constexpr size_t kSiluTiles = 4 * umma::kTileBytes + 4 * kXTile;
 constexpr size_t kSiluSmem = kSiluTiles + sizeof(SiluShared) + 1024;
 static_assert(6 * umma::kTileBytes <= kSiluTiles, "self-test tiles fit");
@@ -72,6 +74,23 @@ __device__ __forceinline__ float sigmoid(float a) { return fast_rcp(1.f + __expf
 __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 #pragma unroll
   for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return v[0];
+}
+
+// lanes l and l ^ 16 end with the warp-wide sum of v[l & 15] (31 shuffles for 16 values)
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {
     const bool up = (lane & w) != 0;
 #pragma unroll
     for (int i = 0; i < w; ++i) {
@@ -194,16 +213,19 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const uint32_t sW2h = smem_u32(W2h), sW2l = smem_u32(W2l), sBh = smem_u32(Bh),
                  sBl = smem_u32(Bl), sXh = smem_u32(Xh), sXl = sXh + kXTile,
                  sYh = sXh + kY, sYl = sYh + kXTile;
-  // TMEM columns: D1 = [a2 - b2 (32) | e (32)], D2 = [dh1 (32) | f (32)], D3 = dW2, D4 = M
-  constexpr uint32_t cD1 = 0, cD2 = 64, cD3 = 128, cD4 = 256;
-  // store bases for this thread's column h and its rows 8g + (0..7), one per (row & 7)
+  // TMEM columns: D1 = [a2 - b2 | e], D2 = [dh1 | f] (kCP each), D3 = dW2, D4 = M
+  constexpr uint32_t cD1 = 0, cD2 = 128, cD3 = 256, cD4 = 384;
+  // store bases for this thread's column h and its rows kPPT g + i: rb[i & 7] + i * 128
   uint32_t rb[8];
   {
-    const uint32_t col = sXh + (uint32_t)((h >> 6) * kXHalf + (h & 7) * 2 + 1024 * wg);
+    const int r0 = kPPT * wg;
+    const uint32_t col = sXh + (uint32_t)((h >> 6) * kXHalf + (h & 7) * 2 + 128 * r0);
     const int hc = (h >> 3) & 7;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) rb[m] = col + (uint32_t)((hc ^ m) << 4);
+    for (int m = 0; m < 8; ++m) rb[m] = col + (uint32_t)((hc ^ ((r0 + m) & 7)) << 4);
   }
+  float (*red)[4 * kCP] = reinterpret_cast<float (*)[4 * kCP]>(Xh + kY);
+  float4* tgt = reinterpret_cast<float4*>(Xh + kY + kRedBytes);
 
   double gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
   double loss = 0, gb3[3] = {0, 0, 0};
@@ -215,6 +237,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     // each warpgroup loads, reduces and scores its own 8 particles: only the GEMM issue points
     // need the whole CTA, everything else synchronises one warpgroup (named barrier)
+    if (ISM && !first) {  // the previous chunk's weight-gradient GEMMs still read X and Y
+      umma::wait_mma(&S.bar[1], phase3);
+      phase3 ^= 1;
+      umma::fence_after();
+    }
     if (wtid < kPPT) {
       const int pl = p0 + wtid;
       const int64_t p = c * kCP + pl;
@@ -235,14 +262,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       }
       S.u[pl] = u;
       S.w[pl] = wt;
-      if (MODE == 2) S.t[pl] = t;
+      if (MODE == 2) tgt[pl] = t;
     }
     wg_sync(wg);
-    if (ISM && !first) {  // the previous chunk's weight-gradient GEMMs still read X and Y
-      umma::wait_mma(&S.bar[1], phase3);
-      phase3 ^= 1;
-      umma::fence_after();
-    }
 
     // F1: layer 1 -> X rows p (h1) and 32 + p (d1 = silu'(a1)), column h
 #pragma unroll
@@ -250,8 +272,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       const float4 u = S.u[p0 + i];
       const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
       const float sg = sigmoid(a);
-      st_split(rb[i] + i * 128, a * sg);
-      if (DIV) st_split(rb[i] + kDivRows + i * 128, sg * fmaf(a, 1.f - sg, 1.f));
+      st_split(rb[i & 7] + i * 128, a * sg);
+      if (DIV) st_split(rb[i & 7] + kDivRows + i * 128, sg * fmaf(a, 1.f - sg, 1.f));
     }
     fence_proxy_async();
     umma::fence_before();
@@ -269,23 +291,28 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     phase ^= 1;
     umma::fence_after();
 
-    // F2a: s and div partials over this thread's h, reduced across the warp
+    // F2a: s and div partials over this thread's h, reduced across the warp (particles
+    // 0..7 of the warpgroup by a 32-value, 8..11 by a 16-value transpose-reduce)
     {
-      float va[8], ve[8];
-      umma::tmem_ld8(tl + cD1 + p0, va);
-      if (DIV) umma::tmem_ld8(tl + cD1 + kCP + p0, ve);
-      float val[32];
+      float va[16], ve[16];
+      umma::tmem_ld12(tl + cD1 + p0, va);
+      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
+      float v32[32], v16[16];
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
         const float a2 = va[pp] + bb2;
         const float sg = sigmoid(a2);
         const float h2 = a2 * sg;
-        val[4 * pp + 0] = w3[0] * h2;
-        val[4 * pp + 1] = w3[1] * h2;
-        val[4 * pp + 2] = w3[2] * h2;
-        val[4 * pp + 3] = DIV ? sg * fmaf(a2, 1.f - sg, 1.f) * ve[pp] : 0.f;
+        float* dst = pp < 8 ? &v32[4 * pp] : &v16[4 * (pp - 8)];
+        dst[0] = w3[0] * h2;
+        dst[1] = w3[1] * h2;
+        dst[2] = w3[2] * h2;
+        dst[3] = DIV ? sg * fmaf(a2, 1.f - sg, 1.f) * ve[pp] : 0.f;
       }
-      S.red[quarter][4 * p0 + lane] = transpose_reduce32(val, lane);
+      const float r32 = transpose_reduce32(v32, lane);
+      const float r16 = transpose_reduce16(v16, lane);
+      red[quarter][4 * p0 + lane] = r32;
+      if (lane < 16) red[quarter][4 * (p0 + 8) + lane] = r16;
     }
     wg_sync(wg);
     if (wtid < kPPT) {
@@ -293,15 +320,15 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       float s[3], dv = 0.f;
 #pragma unroll
       for (int k = 0; k < 3; ++k)
-        s[k] = b3[k] + ((S.red[0][4 * p + k] + S.red[1][4 * p + k]) +
-                        (S.red[2][4 * p + k] + S.red[3][4 * p + k]));
-      dv = (S.red[0][4 * p + 3] + S.red[1][4 * p + 3]) + (S.red[2][4 * p + 3] + S.red[3][4 * p + 3]);
+        s[k] = b3[k] + ((red[0][4 * p + k] + red[1][4 * p + k]) +
+                        (red[2][4 * p + k] + red[3][4 * p + k]));
+      dv = (red[0][4 * p + 3] + red[1][4 * p + 3]) + (red[2][4 * p + 3] + red[3][4 * p + 3]);
       const int64_t q = c * kCP + p;
       if (MODE == 0) {
         if (q < n) sw_out[q] = make_float4(s[0], s[1], s[2], sw[q].w);
       } else if (MODE == 2) {
         const float wi = S.w[p] * in.inv_wsum;
-        const float4 t = S.t[p];
+        const float4 t = tgt[p];
         const float r0 = s[0] - t.x, r1 = s[1] - t.y, r2 = s[2] - t.z;
         S.gs[p] = make_float4(2.f * wi * r0, 2.f * wi * r1, 2.f * wi * r2, 0.f);
         loss += (double)(wi * (r0 * r0 + r1 * r1 + r2 * r2));
@@ -321,14 +348,14 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       wg_sync(wg);
       continue;
     }
-    wg_sync(wg);
+    __syncthreads();  // F2b overwrites the Y tile that holds every warpgroup's partials
 
     // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
     {
       float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
-      float va[8], ve[8];
-      umma::tmem_ld8(tl + cD1 + p0, va);
-      if (DIV) umma::tmem_ld8(tl + cD1 + kCP + p0, ve);
+      float va[16], ve[16];
+      umma::tmem_ld12(tl + cD1 + p0, va);
+      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
         const float4 G = S.gs[p0 + pp];
@@ -346,8 +373,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         aw3[1] = fmaf(G.y, h2, aw3[1]);
         aw3[2] = fmaf(G.z, h2, aw3[2]);
         ab2 += da2;
-        st_split(rb[pp] + kY + pp * 128, da2);
-        if (DIV) st_split(rb[pp] + kY + kDivRows + pp * 128, G.w * d2);
+        st_split(rb[pp & 7] + kY + pp * 128, da2);
+        if (DIV) st_split(rb[pp & 7] + kY + kDivRows + pp * 128, G.w * d2);
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) gw3[k] += (double)aw3[k];
@@ -380,9 +407,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     // F3: reverse through layer 1 -> dW1 (input part), db1
     {
       float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
-      float vd[8], vf[8];
-      umma::tmem_ld8(tl + cD2 + p0, vd);
-      if (DIV) umma::tmem_ld8(tl + cD2 + kCP + p0, vf);
+      float vd[16], vf[16];
+      umma::tmem_ld12(tl + cD2 + p0, vd);
+      if (DIV) umma::tmem_ld12(tl + cD2 + kCP + p0, vf);
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
         const float4 u = S.u[p0 + pp];

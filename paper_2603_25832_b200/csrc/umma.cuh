@@ -153,6 +153,40 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&f)[8]) {
   for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]);
 }
 
+// 16 consecutive float32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&f)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]);
+}
+
+// 12 consecutive float32 columns (three x4 loads, 4-column aligned) of this thread's lane
+__device__ __forceinline__ void tmem_ld12(uint32_t taddr, float (&f)[16]) {
+  uint32_t r[12];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%12];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [%13];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8,%9,%10,%11}, [%14];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+      : "r"(taddr), "r"(taddr + 4), "r"(taddr + 8)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 12; ++i) f[i] = __uint_as_float(r[i]);
+#pragma unroll
+  for (int i = 12; i < 16; ++i) f[i] = 0.f;
+}
+
 // split x into bf16 hi + lo (x ~= hi + lo to ~2^-17 relative) and store both tiles
 __device__ __forceinline__ void store_split(uint8_t* hi_tile, uint8_t* lo_tile, int r, int c,
                                             float x) {

@@ -13,8 +13,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-# per particle per ISM step: 3 GEMMs (G1, G2, G3) x 2 FLOP x 128 x 128 x 4 columns
-GEMM_FLOP_PER_PARTICLE = 3 * 2 * 128 * 128 * 4
+# per particle per ISM step: G1, G2, G3 with two 128 x 128 products each (primal + divergence)
+GEMM_FLOP_PER_PARTICLE = 3 * 2 * (2 * 128 * 128)
 SPLIT_PASSES = 3  # hi*hi + hi*lo + lo*hi
 
 
