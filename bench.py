@@ -66,7 +66,14 @@ WORKLOADS = {
                    nu=0.1, dt=0.05, K=0, hidden=128, lr=1e-3, weight_decay=0.0,
                    divergence="exact", estimator="blob", bandwidth=0.025),
 }
-for _k in ("c0", "c2", "c4"):
+# BASELINE config 3: Weibel, full Maxwell (VML), anisotropic Maxwellian T = (0.01, 0.04, 0.04),
+# seeded B_z noise of amplitude 1e-4 (extension samplers)
+WORKLOADS["c3"] = dict(workload="config3_weibel_vml_sbtm", preset="weibel", mode="VML",
+                       n=1 << 22, M=256, L=2 * math.pi / 1.25, alpha=0.0, k=1.25, c=0.0,
+                       beta=0.01, alpha_B=0.0, nu=0.01, dt=0.02, K=10, hidden=128, lr=1e-3,
+                       weight_decay=0.0, divergence="exact", estimator="sbtm", net="silu",
+                       sampler="anisotropic", temps=(0.01, 0.04, 0.04), b3_noise=1e-4)
+for _k in ("c0", "c2", "c3", "c4"):
     WORKLOADS[_k + "ss"] = dict(WORKLOADS[_k], net="softsign",
                                 workload=WORKLOADS[_k]["workload"] + "_reference_softsign_net")
 NET_LABEL = {"silu": "SiLU 2x128 (BASELINE's MLP; extension M1, tcgen05 split-BF16 hidden GEMMs)",
@@ -160,12 +167,24 @@ def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_strid
     return sum(t.values()), t
 
 
+def sample_workload(wl: dict, cfg, rng):
+    """Initial particles of a workload: the reference's preset sampler, or BASELINE config 3's
+    anisotropic Maxwellian; plus the seeded B3 noise (None unless the workload has one)."""
+    from paper_2603_25832_b200.sampling import anisotropic_ensemble, sample_arrays, seeded_b3_noise
+
+    if wl.get("sampler") == "anisotropic":
+        x, v, w = anisotropic_ensemble(cfg.n, cfg.L, wl["temps"], rng)
+    else:
+        x, v, w = sample_arrays(cfg, rng)
+    b3 = seeded_b3_noise(cfg.M, wl["b3_noise"], rng) if wl.get("b3_noise") else None
+    return x, v, w, b3
+
+
 def host_initial_state(wl: dict, seed: int):
-    from paper_2603_25832_b200.sampling import sample_arrays
     from oracle import oracle as O
 
     cfg = make_config(wl, seed)
-    x, v, w = sample_arrays(cfg, np.random.default_rng(seed))
+    x, v, w, b3 = sample_workload(wl, cfg, np.random.default_rng(seed))
     x = x.astype(np.float32).astype(np.float64)
     v = v.astype(np.float32).astype(np.float64)
     M, L = wl["M"], wl["L"]
@@ -173,7 +192,7 @@ def host_initial_state(wl: dict, seed: int):
     rho, _ = O.deposit(x, v, w, eta, M)
     rho_ion = float(rho.sum() * eta / L)
     E1 = O.poisson_solve(rho, rho_ion, eta) if wl["mode"] == "VPL" else np.zeros(M)
-    return dict(x=x, v=v, w=w, E1=E1, E2=np.zeros(M), B3=np.zeros(M))
+    return dict(x=x, v=v, w=w, E1=E1, E2=np.zeros(M), B3=b3 if b3 is not None else np.zeros(M))
 
 
 def cpu_baseline_line(wl: dict, seed: int, reps: int = 1, warm: int = 0):
@@ -296,16 +315,17 @@ def build_sim(wl: dict, seed: int, device):
     from paper_2603_25832_b200.engine import Simulation
     from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
     from paper_2603_25832_b200.run import initial_fields
-    from paper_2603_25832_b200.sampling import sample_arrays
     from paper_2603_25832_b200.state import ParticleEnsemble
 
     cfg = make_config(wl, seed)
     rng = np.random.default_rng(seed)
-    x, v, w = sample_arrays(cfg, rng)
+    x, v, w, b3 = sample_workload(wl, cfg, rng)
     grid = Grid(cfg.M, cfg.eta)
     p = ParticleEnsemble.from_arrays(x, v, w, device=device)
     rho, J = deposit(p, grid)
     fields = initial_fields(cfg, grid, rho, J)
+    if b3 is not None:
+        fields.B3.copy_(torch.as_tensor(b3, dtype=fields.B3.dtype, device=fields.B3.device))
     est = make_estimator_for(wl, cfg, rng, device, grid)
     sim = Simulation(p, fields, grid, dt=cfg.dt, nu=cfg.nu, mode=cfg.mode, gamma=cfg.gamma,
                      estimator=est, max_rows=4)
@@ -431,13 +451,12 @@ def build_dist_sim(wl: dict, seed: int, device, world: int):
     from paper_2603_25832_b200.parallel import CellPartition, Comm
     from paper_2603_25832_b200.pic import Grid, deposit
     from paper_2603_25832_b200.run import initial_fields
-    from paper_2603_25832_b200.sampling import sample_arrays
     from paper_2603_25832_b200.state import ParticleEnsemble
 
     wl = dict(wl, n=wl["n"] * world, M=wl["M"] * world, L=wl["L"] * world)
     cfg = make_config(wl, seed)
     rng = np.random.default_rng(seed)
-    x, v, w = sample_arrays(cfg, rng)
+    x, v, w, b3 = sample_workload(wl, cfg, rng)
     grid = Grid(cfg.M, cfg.eta)
     comm = Comm()
     part = CellPartition.equal(cfg.M, world)
@@ -449,6 +468,10 @@ def build_dist_sim(wl: dict, seed: int, device, world: int):
     pfull = ParticleEnsemble.from_arrays(x, v, w, device=device)
     rho, J = deposit(pfull, grid)
     fields = initial_fields(cfg, grid, rho, J)
+    if b3 is not None:
+        import torch
+
+        fields.B3.copy_(torch.as_tensor(b3, dtype=fields.B3.dtype, device=fields.B3.device))
     del pfull
     est = make_estimator_for(wl, cfg, rng, device, grid)
     sim = DistSimulation(x[own], v[own], w[own], own, fields, grid, dt=cfg.dt, nu=cfg.nu,
