@@ -293,10 +293,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 
     // F2a: s and div partials over this thread's h, reduced across the warp (particles
     // 0..7 of the warpgroup by a 32-value, 8..11 by a 16-value transpose-reduce)
+    // (the D1 columns stay in registers for F2b: one TMEM round trip per chunk saved)
+    float va[16], ve[16];
+    umma::tmem_ld12(tl + cD1 + p0, va);
+    if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
     {
-      float va[16], ve[16];
-      umma::tmem_ld12(tl + cD1 + p0, va);
-      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
       float v32[32], v16[16];
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
@@ -353,9 +354,6 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
     {
       float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
-      float va[16], ve[16];
-      umma::tmem_ld12(tl + cD1 + p0, va);
-      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
         const float4 G = S.gs[p0 + pp];

@@ -89,8 +89,10 @@ def test_silu_forward_matches_oracle(lib, n):
     assert np.max(np.abs(s - ref)) <= 1e-4 * np.max(np.abs(ref))
 
 
-@pytest.mark.parametrize("n", [5, 4099, 148 * 32 * 3 + 11])
+@pytest.mark.parametrize("n", [5, 4099, 148 * 32 * 3 + 11, 250007])
 def test_silu_ism_loss_and_grad_matches_oracle(lib, n):
+    """250 007 particles = ~35 chunks per CTA: float32 TMEM accumulation of dW2 and M over a
+    long chunk sequence still meets the tolerance."""
     from paper_2603_25832_b200.silu_net import silu_ism_loss_and_grad
 
     L = 4 * math.pi
