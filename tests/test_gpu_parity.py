@@ -171,6 +171,35 @@ def test_homogeneous_config1_parity_and_conservation(spic, n):
     assert mom <= 1e-5 and en <= 1e-5, (mom, en)
 
 
+@pytest.mark.parametrize("tag", ["config2", "config3"])
+def test_full_size_collision_conservation(spic, tag):
+    """BASELINE full sizes (config 2: n = 2^20, M = 128; config 3: n = 2^22, M = 256) through
+    size-independent properties: the binned Landau operator conserves momentum and energy
+    (sum w U = 0, sum w v.U = 0) for any scores; sub-cell culling on (the engine default)."""
+    from paper_2603_25832_b200.collision import auto_sub_cells, build_cell_index, collision_force
+    from paper_2603_25832_b200.pic import Grid
+
+    n, M, L = ((1 << 20, 128, 10 * math.pi) if tag == "config2" else
+               (1 << 22, 256, 2 * math.pi / 1.25))
+    rng = np.random.default_rng(11)
+    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    x[x >= L] = 0.0
+    v = (rng.normal(size=(n, 3)) * (1.0 if tag == "config2" else 0.2)).astype(np.float32)
+    v = v.astype(np.float64)
+    s = (-v + 0.5 * rng.normal(size=(n, 3))).astype(np.float32).astype(np.float64)
+    p = ens(x, v, np.full(n, L / n))
+    grid = Grid(M, L / M)
+    ci = build_cell_index(p, grid, auto_sub_cells(n, M))
+    U = collision_force(p, s, ci, grid, -3.0).double().cpu().numpy()
+    w64 = p.w.double().cpu().numpy()
+    wU = w64[:, None] * U
+    mom = float(np.max(np.abs(wU.sum(0))) / np.sum(np.abs(wU)))
+    en = abs(float(np.sum(w64 * np.einsum("ij,ij->i", v, U))))
+    en /= float(np.sum(w64 * np.linalg.norm(v, axis=1) * np.linalg.norm(U, axis=1)))
+    assert np.all(np.isfinite(U))
+    assert mom <= 1e-5 and en <= 1e-5, (mom, en)
+
+
 def test_collision_config0_shapes_with_subcell_culling(spic):
     """Config-0 shapes (n = 65536, M = 64, L = 4 pi), random scores: S = 1 and S > 1 agree
     with the oracle (culling only drops pairs with |dx| >= eta)."""
