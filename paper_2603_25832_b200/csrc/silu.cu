@@ -5,18 +5,15 @@
 //   W1[H][4], b1[H], W2[H][H], b2[H], W3[3][H], b3[3]):
 //   a1 = W1 u + b1, h1 = silu(a1); a2 = W2 h1 + b2, h2 = silu(a2); s = W3 h2 + b3.
 // The ISM loss sum_p w_p (|s_p|^2 + 2 div_p) (ref: score.py:303-338 applied to this network)
-// needs the exact Jacobian trace, carried as three forward tangents t1_k = silu'(a1) W1[:,1+k]
-// per particle, and then the reverse sweep. Per chunk of 32 particles the CTA runs three
-// 128 x 128 x 128 GEMMs, each as split-BF16 (hi*hi + hi*lo + lo*hi, ~2^-16 relative) on
-// tcgen05 with float32 TMEM accumulation:
-//   G1  [a2 - b2 | c2_k]      = W2   . [h1 | t1_k]        (columns: 4 per particle)
-//   G2  [dh1 | dt1_k]         = W2^T . [da2 | dc2_k]
-//   G3  dW2                  += [da2 | dc2_k] . [h1 | t1_k]^T   (TMEM-resident across chunks)
-// Everything elementwise (SiLU and its first two derivatives, the W1/W3 layers, the s / div
-// reductions over h, per-particle loss terms) runs on the FP32 pipes with one thread per
-// hidden unit (the TMEM lane) and two warpgroups splitting the chunk's particles.
-// One persistent CTA per SM (192 KB of operand tiles + 384 TMEM columns); per-CTA float64
-// partial rows are reduced in a fixed order and finalized by the shared AdamW kernel.
+// needs the exact Jacobian trace; it is carried by one divergence column per particle,
+// div = d2 . (B d1) with B = W2 (.) C, C[h][h'] = sum_k W3[k][h] W1[h'][1+k] (see k_silu).
+// Per chunk of 48 particles the CTA runs the layer GEMMs as split-BF16 (hi*hi + hi*lo + lo*hi,
+// ~2^-16 relative) on tcgen05 with float32 TMEM accumulation; everything elementwise (SiLU
+// and its first two derivatives, the W1/W3 layers, the s / div reductions over h, the loss
+// terms) runs on the FP32 pipes with one thread per hidden unit (the TMEM lane) and four
+// warpgroups splitting the chunk's particles. One persistent CTA per SM (224 KB of operand
+// tiles, 512 TMEM columns); per-CTA float64 partial rows are reduced in a fixed order and
+// finalized by the shared AdamW kernel (adamw.cuh).
 #include <algorithm>
 
 #include "adamw.cuh"
@@ -37,7 +34,7 @@ constexpr int kNWG = 4;       // warpgroups per CTA; thread = (hidden unit h, pa
 constexpr int kNT = 128 * kNWG;
 constexpr int kPPT = kCP / kNWG;  // particles per thread per chunk
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColD1 = 0, kColD2 = 128, kColD3 = 256;
+constexpr uint32_t kColD1 = 0, kColD2 = 128, kColD3 = 256;  // self-test accumulators
 
 __host__ __device__ constexpr int64_t silu_params(int H) { return (int64_t)H * H + 9 * H + 3; }
 
@@ -48,8 +45,8 @@ struct SiluShared {
   uint64_t bar[2];  // [0]: G1 / G2 done, [1]: G3 done (X, Y free again)
   uint32_t tmem;
 };
-// W2 and B = W2 (.) C as 128-row operand tiles (hi, lo); X and Y as 64-row tiles (hi, lo):
-// rows 0..31 = the chunk's primal columns, rows 32..63 = its divergence columns
+// W2 and B = W2 (.) C as 128-row operand tiles (hi, lo); X and Y as 96-row tiles (hi, lo):
+// rows 0..47 = the chunk's primal columns, rows 48..95 = its divergence columns
 constexpr uint32_t kXHalf = 2 * kCP * 128;        // 96-row tile half (12 KB)
 constexpr uint32_t kXTile = 2 * kXHalf;           // 24 KB
 // per-warp-quarter partials (s0, s1, s2, div) per particle and the MSE targets live in the Y
