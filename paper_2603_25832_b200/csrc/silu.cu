@@ -440,7 +440,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     // dW2 = D3 + C (.) M (row h, columns h'); warpgroup g takes columns 32g..32g+31. The
     // tangent terms of dW3 (row sums of (W2 (.) M) W1[:,1+k]) and dW1 (column sums of
     // W3[k] (W2 (.) M)) go through shared memory: WM = W2 (.) M as float [h][h'].
-    float* WM = reinterpret_cast<float*>(Xh);  // 64 KB: the X and Y tiles are free now
+    constexpr int kWMs = kH + 1;  // padded row stride: row writes by lane h hit distinct banks
+    static_assert(sizeof(float) * kH * kWMs <= 4 * kXTile, "WM fits the X / Y tiles");
+    float* WM = reinterpret_cast<float*>(Xh);  // the X and Y tiles are free now
     float tw3[3] = {0.f, 0.f, 0.f};
     {
       float v[32], m[32];
@@ -454,12 +456,12 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           const float Chh = fmaf(w3[2], W1[hp * 4 + 3], fmaf(w3[1], W1[hp * 4 + 2], w3[0] * W1[hp * 4 + 1]));
           const float wm = W2[h * kH + hp] * m[i];
           g += (double)(Chh * m[i]);
-          WM[h * kH + hp] = wm;
+          WM[h * kWMs + hp] = wm;
           tw3[0] = fmaf(W1[hp * 4 + 1], wm, tw3[0]);
           tw3[1] = fmaf(W1[hp * 4 + 2], wm, tw3[1]);
           tw3[2] = fmaf(W1[hp * 4 + 3], wm, tw3[2]);
         } else if (DIV) {
-          WM[h * kH + hp] = 0.f;
+          WM[h * kWMs + hp] = 0.f;
         }
         row[oW2 + h * kH + hp] = g;
       }
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       float cw[3] = {0.f, 0.f, 0.f};
       if (DIV)
         for (int r = 0; r < kH; ++r) {
-          const float wm = WM[r * kH + h];
+          const float wm = WM[r * kWMs + h];
           cw[0] = fmaf(W3[r], wm, cw[0]);
           cw[1] = fmaf(W3[kH + r], wm, cw[1]);
           cw[2] = fmaf(W3[2 * kH + r], wm, cw[2]);
