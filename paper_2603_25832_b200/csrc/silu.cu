@@ -484,6 +484,21 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       }
     }
     __syncthreads();
+    // dW1[h][1+k] tangent part: sum over rows r of W3[k][r] WM[r][h] (column h); warpgroup g
+    // sums rows 32g..32g+31, the four partials are added in a fixed order below
+    float* cwp = reinterpret_cast<float*>(lcomb + 16);  // [4][kH][3]
+    if (DIV) {
+      float cw[3] = {0.f, 0.f, 0.f};
+      for (int r = 32 * wg; r < 32 * wg + 32; ++r) {
+        const float wm = WM[r * kWMs + h];
+        cw[0] = fmaf(W3[r], wm, cw[0]);
+        cw[1] = fmaf(W3[kH + r], wm, cw[1]);
+        cw[2] = fmaf(W3[2 * kH + r], wm, cw[2]);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cwp[(wg * kH + h) * 3 + k] = cw[k];
+    }
+    __syncthreads();
     if (wg == 0) {
       double t[12];
 #pragma unroll
@@ -495,17 +510,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       row[ob2 + h] = t[5];
 #pragma unroll
       for (int k = 0; k < 3; ++k) row[oW3 + k * kH + h] = t[6 + k] + t[9 + k];
-      // dW1[h][1+k]: input part + sum over rows h'' of W3[k][h''] WM[h''][h] (column h)
-      float cw[3] = {0.f, 0.f, 0.f};
-      if (DIV)
-        for (int r = 0; r < kH; ++r) {
-          const float wm = WM[r * kWMs + h];
-          cw[0] = fmaf(W3[r], wm, cw[0]);
-          cw[1] = fmaf(W3[kH + r], wm, cw[1]);
-          cw[2] = fmaf(W3[2 * kH + r], wm, cw[2]);
-        }
 #pragma unroll
-      for (int k = 0; k < 3; ++k) row[oW1 + 4 * h + 1 + k] = t[1 + k] + (double)cw[k];
+      for (int k = 0; k < 3; ++k) {
+        const float cw = DIV ? (cwp[(0 * kH + h) * 3 + k] + cwp[(1 * kH + h) * 3 + k]) +
+                                   (cwp[(2 * kH + h) * 3 + k] + cwp[(3 * kH + h) * 3 + k])
+                             : 0.f;
+        row[oW1 + 4 * h + 1 + k] = t[1 + k] + (double)cw;
+      }
     }
     if (tid == 0) {
       row[0] = (lcomb[0] + lcomb[4]) + (lcomb[8] + lcomb[12]);
