@@ -36,6 +36,18 @@ constexpr int kPPT = kCP / kNWG;  // particles per thread per chunk
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColD1 = 0, kColD2 = 128, kColD3 = 256;  // self-test accumulators
 
+#ifdef SPIC_SILU_TRACE  // tools/silu_trace.cu: per-phase clock64 stamps of CTA 0, thread 0
+__device__ long long g_silu_trace[64 * 16];
+#define SILU_TRACE(k)                                                                  \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && it < 64) g_silu_trace[it * 16 + (k)] = clock64(); \
+  } while (0)
+#else
+#define SILU_TRACE(k) \
+  do {                \
+  } while (0)
+#endif
+
 __host__ __device__ constexpr int64_t silu_params(int H) { return (int64_t)H * H + 9 * H + 3; }
 
 struct SiluShared {
@@ -197,8 +209,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const float bb1 = b1[h], bb2 = b2[h];
   if (tid < 32) umma::tmem_alloc(&S.tmem, kTmemCols);
   if (tid == 32) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
+    // with divergence columns, the primal and the divergence GEMM of each phase are issued
+    // by two threads of different warps (tid 0 and 32), each committing once
+    mbar_init(&S.bar[0], DIV ? 2 : 1);
+    mbar_init(&S.bar[1], DIV ? 2 : 1);
     fence_barrier_init();
   }
   fence_proxy_async();
@@ -231,7 +245,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const int64_t nchunks = (n + kCP - 1) / kCP;
   const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk (= GEMM columns)
 
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    SILU_TRACE(0);
     // each warpgroup loads, reduces and scores its own 8 particles: only the GEMM issue points
     // need the whole CTA, everything else synchronises one warpgroup (named barrier)
     if (ISM && !first) {  // the previous chunk's weight-gradient GEMMs still read X and Y
@@ -262,6 +278,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       if (MODE == 2) tgt[pl] = t;
     }
     wg_sync(wg);
+    SILU_TRACE(1);
 
     // F1: layer 1 -> X rows p (h1) and 32 + p (d1 = silu'(a1)), column h
 #pragma unroll
@@ -276,17 +293,20 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
+    SILU_TRACE(2);
     if (tid == 0) {
       umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
                                                             false);
-      if (DIV)
-        umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(
-            tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);
+      umma::commit(&S.bar[0]);
+    } else if (DIV && tid == 32) {
+      umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(
+          tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);
       umma::commit(&S.bar[0]);
     }
     umma::wait_mma(&S.bar[0], phase);
     phase ^= 1;
     umma::fence_after();
+    SILU_TRACE(3);
 
     // F2a: s and div partials over this thread's h, reduced across the warp (particles
     // 0..7 of the warpgroup by a 32-value, 8..11 by a 16-value transpose-reduce)
@@ -313,6 +333,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       if (lane < 16) red[quarter][4 * (p0 + 8) + lane] = r16;
     }
     wg_sync(wg);
+    SILU_TRACE(4);
     if (wtid < kPPT) {
       const int p = p0 + wtid;
       float s[3], dv = 0.f;
@@ -347,6 +368,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       continue;
     }
     __syncthreads();  // F2b overwrites the Y tile that holds every warpgroup's partials
+    SILU_TRACE(5);
 
     // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
     {
@@ -379,25 +401,30 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
+    SILU_TRACE(6);
+    // two issuing threads in two warps: tid 0 the primal G2 then G3 halves, tid 32 the
+    // divergence halves, so both G2 halves reach the tensor pipe ahead of G3
     if (tid == 0) {
       umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(tm + cD2, sW2h, sW2l, sYh, sYl,
                                                            false);  // W2^T da2
-      if (DIV)
-        umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(
-            tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
       umma::commit(&S.bar[0]);
       umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(tm + cD3, sYh, sYl, sXh, sXl,
                                                                   !first);  // da2 h1^T
-      if (DIV)
-        umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(
-            tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
-            !first);  // y2 d1^T
       umma::commit(&S.bar[1]);  // overlaps F3 and the next chunk's record loads
+    } else if (DIV && tid == 32) {
+      umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(
+          tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
+      umma::commit(&S.bar[0]);
+      umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(
+          tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
+          !first);  // y2 d1^T
+      umma::commit(&S.bar[1]);
     }
     first = false;
     umma::wait_mma(&S.bar[0], phase);
     phase ^= 1;
     umma::fence_after();
+    SILU_TRACE(7);
 
     // F3: reverse through layer 1 -> dW1 (input part), db1
     {
@@ -425,6 +452,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     }
     umma::fence_before();
     wg_sync(wg);
+    SILU_TRACE(8);
   }
 
   if (ISM) {

@@ -60,21 +60,27 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
 
 // D[128 x N] (+)= A * B over K = 16 * KSTEPS with split-BF16 operands:
 // Ahi*Bhi + Ahi*Blo + Alo*Bhi (~2^-16 relative per product; float32 accumulation in TMEM).
-// Operand addresses are tile (sub-)block starts. Issued by one thread.
+// Operand addresses are tile (sub-)block starts. Issued by one thread. The four base
+// descriptors are built once; every K-step only adds a constant to their start-address
+// field (addresses stay below 2^18, so the 14-bit field never carries).
 template <bool A_MN, bool B_MN, int N = 128, int KSTEPS = 8, uint32_t AH = 16384,
           uint32_t BH = 16384>
 __device__ __forceinline__ void gemm_split(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
                                            uint32_t b_hi, uint32_t b_lo, bool accumulate) {
   constexpr uint32_t id = idesc_bf16(A_MN ? 1u : 0u, B_MN ? 1u : 0u, (uint32_t)N);
+  const uint64_t ah0 = A_MN ? desc_mn(a_hi, 0, AH) : desc_k(a_hi, 0, AH);
+  const uint64_t al0 = A_MN ? desc_mn(a_lo, 0, AH) : desc_k(a_lo, 0, AH);
+  const uint64_t bh0 = B_MN ? desc_mn(b_hi, 0, BH) : desc_k(b_hi, 0, BH);
+  const uint64_t bl0 = B_MN ? desc_mn(b_lo, 0, BH) : desc_k(b_lo, 0, BH);
 #pragma unroll
   for (int ks = 0; ks < KSTEPS; ++ks) {
-    const uint64_t ah = A_MN ? desc_mn(a_hi, ks, AH) : desc_k(a_hi, ks, AH);
-    const uint64_t al = A_MN ? desc_mn(a_lo, ks, AH) : desc_k(a_lo, ks, AH);
-    const uint64_t bh = B_MN ? desc_mn(b_hi, ks, BH) : desc_k(b_hi, ks, BH);
-    const uint64_t bl = B_MN ? desc_mn(b_lo, ks, BH) : desc_k(b_lo, ks, BH);
-    mma(d_tmem, ah, bh, id, (accumulate || ks > 0) ? 1u : 0u);
-    mma(d_tmem, ah, bl, id, 1u);
-    mma(d_tmem, al, bh, id, 1u);
+    const uint64_t ao = A_MN ? (uint64_t)(ks * 2048 >> 4)
+                             : (uint64_t)(((ks >> 2) * AH + (ks & 3) * 32) >> 4);
+    const uint64_t bo = B_MN ? (uint64_t)(ks * 2048 >> 4)
+                             : (uint64_t)(((ks >> 2) * BH + (ks & 3) * 32) >> 4);
+    mma(d_tmem, ah0 + ao, bh0 + bo, id, (accumulate || ks > 0) ? 1u : 0u);
+    mma(d_tmem, ah0 + ao, bl0 + bo, id, 1u);
+    mma(d_tmem, al0 + ao, bh0 + bo, id, 1u);
   }
 }
 
