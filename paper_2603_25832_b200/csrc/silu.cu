@@ -54,7 +54,7 @@ struct SiluShared {
   float4 u[kCP];
   float w[kCP];
   float4 gs[kCP];              // ISM: (2w s, 2w); MSE: (2w' (s - t), 0)
-  uint64_t bar[2];  // [0]: G1 / G2 done, [1]: G3 done (X, Y free again)
+  uint64_t bar[3];  // [0] G1 done, [1] G3 done (X, Y free again), [2] G2 done
   uint32_t tmem;
 };
 // W2 and B = W2 (.) C as 128-row operand tiles (hi, lo); X and Y as 96-row tiles (hi, lo):
@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     // by two threads of different warps (tid 0 and 32), each committing once
     mbar_init(&S.bar[0], DIV ? 2 : 1);
     mbar_init(&S.bar[1], DIV ? 2 : 1);
+    mbar_init(&S.bar[2], DIV ? 2 : 1);
     fence_barrier_init();
   }
   fence_proxy_async();
@@ -240,11 +241,55 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 
   double gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
   double loss = 0, gb3[3] = {0, 0, 0};
-  uint32_t phase = 0, phase3 = 0;
+  uint32_t phase = 0, phase2 = 0, phase3 = 0;
   bool first = true;
   const int64_t nchunks = (n + kCP - 1) / kCP;
   const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk (= GEMM columns)
 
+  // F3: reverse through layer 1 -> dW1 (input part), db1, for chunk cc whose G2 result is in
+  // D2. The ISM runs it one chunk late, while the tensor cores compute the next chunk's G1
+  // (re-reading that chunk's records, an L2 hit); MSE runs it in order from S.u.
+  auto layer1_reverse = [&](int64_t cc) {
+    float4 uu[kPPT];
+#pragma unroll
+    for (int pp = 0; pp < kPPT; ++pp) {
+      if (MODE == 1) {
+        const int64_t p = cc * kCP + p0 + pp;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (p < n) A = xv[p];
+        const float x = A.x < 0.f ? A.x + L : A.x;
+        uu[pp] = make_float4(x * x_scale, A.y, A.z, A.w);
+      } else {
+        uu[pp] = S.u[p0 + pp];
+      }
+    }
+    umma::wait_mma(&S.bar[2], phase2);
+    phase2 ^= 1;
+    umma::fence_after();
+    float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
+    float vd[16], vf[16];
+    umma::tmem_ld12(tl + cD2 + p0, vd);
+    if (DIV) umma::tmem_ld12(tl + cD2 + kCP + p0, vf);
+#pragma unroll
+    for (int pp = 0; pp < kPPT; ++pp) {
+      const float4 u = uu[pp];
+      const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
+      const float sg = sigmoid(a);
+      const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
+      float da1 = d1 * vd[pp];
+      if (DIV) da1 = fmaf(sg * (1.f - sg) * fmaf(a, 1.f - 2.f * sg, 2.f), vf[pp], da1);
+      ab1 += da1;
+      aw1[0] = fmaf(da1, u.x, aw1[0]);
+      aw1[1] = fmaf(da1, u.y, aw1[1]);
+      aw1[2] = fmaf(da1, u.z, aw1[2]);
+      aw1[3] = fmaf(da1, u.w, aw1[3]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) gw1[i] += (double)aw1[i];
+    gb1 += (double)ab1;
+  };
+
+  int64_t prev = -1;  // chunk whose layer-1 reverse sweep is still pending (ISM)
   int it = 0;
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
     SILU_TRACE(0);
@@ -303,10 +348,12 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);
       umma::commit(&S.bar[0]);
     }
+    if (MODE == 1 && prev >= 0) layer1_reverse(prev);  // overlaps this chunk's G1
+    SILU_TRACE(3);
     umma::wait_mma(&S.bar[0], phase);
     phase ^= 1;
     umma::fence_after();
-    SILU_TRACE(3);
+    SILU_TRACE(4);
 
     // F2a: s and div partials over this thread's h, reduced across the warp (particles
     // 0..7 of the warpgroup by a 32-value, 8..11 by a 16-value transpose-reduce)
@@ -333,7 +380,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       if (lane < 16) red[quarter][4 * (p0 + 8) + lane] = r16;
     }
     wg_sync(wg);
-    SILU_TRACE(4);
+    SILU_TRACE(5);
     if (wtid < kPPT) {
       const int p = p0 + wtid;
       float s[3], dv = 0.f;
@@ -368,7 +415,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       continue;
     }
     __syncthreads();  // F2b overwrites the Y tile that holds every warpgroup's partials
-    SILU_TRACE(5);
+    SILU_TRACE(6);
 
     // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
     {
@@ -401,59 +448,36 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    SILU_TRACE(6);
+    SILU_TRACE(7);
     // two issuing threads in two warps: tid 0 the primal G2 then G3 halves, tid 32 the
     // divergence halves, so both G2 halves reach the tensor pipe ahead of G3
     if (tid == 0) {
       umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(tm + cD2, sW2h, sW2l, sYh, sYl,
                                                            false);  // W2^T da2
-      umma::commit(&S.bar[0]);
+      umma::commit(&S.bar[2]);
       umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(tm + cD3, sYh, sYl, sXh, sXl,
                                                                   !first);  // da2 h1^T
       umma::commit(&S.bar[1]);  // overlaps F3 and the next chunk's record loads
     } else if (DIV && tid == 32) {
       umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(
           tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
-      umma::commit(&S.bar[0]);
+      umma::commit(&S.bar[2]);
       umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(
           tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
           !first);  // y2 d1^T
       umma::commit(&S.bar[1]);
     }
     first = false;
-    umma::wait_mma(&S.bar[0], phase);
-    phase ^= 1;
-    umma::fence_after();
-    SILU_TRACE(7);
-
-    // F3: reverse through layer 1 -> dW1 (input part), db1
-    {
-      float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
-      float vd[16], vf[16];
-      umma::tmem_ld12(tl + cD2 + p0, vd);
-      if (DIV) umma::tmem_ld12(tl + cD2 + kCP + p0, vf);
-#pragma unroll
-      for (int pp = 0; pp < kPPT; ++pp) {
-        const float4 u = S.u[p0 + pp];
-        const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
-        const float sg = sigmoid(a);
-        const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
-        float da1 = d1 * vd[pp];
-        if (DIV) da1 = fmaf(sg * (1.f - sg) * fmaf(a, 1.f - 2.f * sg, 2.f), vf[pp], da1);
-        ab1 += da1;
-        aw1[0] = fmaf(da1, u.x, aw1[0]);
-        aw1[1] = fmaf(da1, u.y, aw1[1]);
-        aw1[2] = fmaf(da1, u.z, aw1[2]);
-        aw1[3] = fmaf(da1, u.w, aw1[3]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) gw1[i] += (double)aw1[i];
-      gb1 += (double)ab1;
+    if (MODE == 1) {
+      prev = c;
+    } else {
+      layer1_reverse(c);
     }
     umma::fence_before();
     wg_sync(wg);
     SILU_TRACE(8);
   }
+  if (MODE == 1 && prev >= 0) layer1_reverse(prev);
 
   if (ISM) {
     if (!first) {

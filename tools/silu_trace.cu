@@ -1,8 +1,8 @@
 // Per-phase cycle stamps of the SiLU ISM kernel (CTA 0, thread 0, first 64 chunks).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DSPIC_SILU_TRACE \
 //        -o tools/silu_trace tools/silu_trace.cu
-// Phases: 0 top, 1 records loaded, 2 F1 done (G1 issue), 3 G1 done, 4 F2a done,
-// 5 per-particle done, 6 F2b done (G2/G3 issue), 7 G2 done, 8 F3 done.
+// Phases: 0 top, 1 records loaded, 2 F1 done (G1 issue), 3 previous chunk's F3 done,
+// 4 G1 done, 5 F2a done, 6 per-particle done, 7 F2b done, 8 G2/G3 issued.
 #include <cstdio>
 #include <vector>
 #include <random>
@@ -50,8 +50,8 @@ int main() {
     sum[0] += (double)(h[(it + 1) * 16] - h[it * 16 + 8]);
     ++cnt;
   }
-  const char* names[9] = {"loop-tail", "wait G3 + records", "F1", "G1 wait", "F2a",
-                          "per-particle", "F2b", "G2 wait", "F3"};
+  const char* names[9] = {"loop-tail", "wait G3 + records", "F1", "F3(prev) under G1",
+                          "G1 wait", "F2a", "per-particle", "F2b", "G2/G3 issue"};
   double tot = 0;
   for (int k = 0; k <= 8; ++k) tot += sum[k];
   for (int k = 0; k <= 8; ++k)
