@@ -30,8 +30,9 @@ namespace {
 
 constexpr int kH = 128;       // hidden width of the tensor-core path
 constexpr int kCP = 48;       // particles per chunk (GEMM N of the layer GEMMs)
-constexpr int kNWG = 4;       // warpgroups per CTA; thread = (hidden unit h, particle slice)
-constexpr int kNT = 128 * kNWG;
+constexpr int kNWG = 4;       // compute warpgroups; thread = (hidden unit h, particle slice)
+constexpr int kNCW = 128 * kNWG;  // compute threads
+constexpr int kNT = kNCW + 32;    // + one MMA-issuer warp
 constexpr int kPPT = kCP / kNWG;  // particles per thread per chunk
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColD1 = 0, kColD2 = 128, kColD3 = 256;  // self-test accumulators
@@ -51,7 +52,7 @@ __device__ long long g_silu_trace[64 * 16];
 __host__ __device__ constexpr int64_t silu_params(int H) { return (int64_t)H * H + 9 * H + 3; }
 
 struct SiluShared {
-  float4 u[kCP];
+  float4 u[2][kCP];  // chunk records, double-buffered (the layer-1 reverse sweep runs late)
   float w[kCP];
   float4 gs[kCP];              // ISM: (2w s, 2w); MSE: (2w' (s - t), 0)
   uint64_t bar[3];  // [0] G1 done, [1] G3 done (X, Y free again), [2] G2 done
@@ -66,7 +67,9 @@ constexpr uint32_t kXTile = 2 * kXHalf;           // 24 KB
 constexpr uint32_t kRedBytes = 4 * 4 * kCP * sizeof(float);
 static_assert(kRedBytes + kCP * sizeof(float4) <= kXTile, "scratch fits the Y tile");
 constexpr size_t kSiluTiles = 4 * umma::kTileBytes + 4 * kXTile;
-constexpr size_t kSiluSmem = kSiluTiles + sizeof(SiluShared) + 1024;
+// The dynamic shared window starts 1024-B aligned on sm_100 (checked in-kernel: a
+// misaligned start traps), so no alignment slack is requested.
+constexpr size_t kSiluSmem = kSiluTiles + sizeof(SiluShared);
 static_assert(6 * umma::kTileBytes <= kSiluTiles, "self-test tiles fit");
 
 // 1024-B aligned start inside the dynamic shared buffer (SWIZZLE_128B atoms). The offset is
@@ -74,7 +77,8 @@ static_assert(6 * umma::kTileBytes <= kSiluTiles, "self-test tiles fit");
 // addressing for everything derived from it.
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-  return p + ((1024u - (a & 1023u)) & 1023u);
+  if (a & 1023u) __trap();  // SWIZZLE_128B operand tiles need 1024-B aligned atoms
+  return p;
 }
 
 __device__ __forceinline__ float sigmoid(float a) { return fast_rcp(1.f + __expf(-a)); }
@@ -113,6 +117,16 @@ __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 
 __device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one warpgroup
   asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+}
+// the 512 compute threads (the issuer warp does not take part)
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 5, 512;" ::: "memory"); }
+// hand-offs compute -> issuer: X tile ready (6), Y tile ready (7); compute threads arrive,
+// the issuer warp waits (544 = 512 + 32)
+__device__ __forceinline__ void handoff_arrive(int id) {
+  asm volatile("bar.arrive %0, 544;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ void handoff_wait(int id) {
+  asm volatile("bar.sync %0, 544;" ::"r"(id) : "memory");
 }
 
 // Split-BF16 store of one value into a 64-row X / Y tile: hi at addr, lo at addr + kXTile.
@@ -209,11 +223,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const float bb1 = b1[h], bb2 = b2[h];
   if (tid < 32) umma::tmem_alloc(&S.tmem, kTmemCols);
   if (tid == 32) {
-    // with divergence columns, the primal and the divergence GEMM of each phase are issued
-    // by two threads of different warps (tid 0 and 32), each committing once
-    mbar_init(&S.bar[0], DIV ? 2 : 1);
-    mbar_init(&S.bar[1], DIV ? 2 : 1);
-    mbar_init(&S.bar[2], DIV ? 2 : 1);
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    mbar_init(&S.bar[2], 1);
     fence_barrier_init();
   }
   fence_proxy_async();
@@ -239,8 +251,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   float (*red)[4 * kCP] = reinterpret_cast<float (*)[4 * kCP]>(Xh + kY);
   float4* tgt = reinterpret_cast<float4*>(Xh + kY + kRedBytes);
 
-  double gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
-  double loss = 0, gb3[3] = {0, 0, 0};
+  // per-thread sums over the CTA's chunks in float32 (<= ~150 chunk terms each); the CTA and
+  // cross-CTA combines are float64
+  float gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
+  float loss = 0, gb3[3] = {0, 0, 0};
   uint32_t phase = 0, phase2 = 0, phase3 = 0;
   bool first = true;
   const int64_t nchunks = (n + kCP - 1) / kCP;
@@ -249,20 +263,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   // F3: reverse through layer 1 -> dW1 (input part), db1, for chunk cc whose G2 result is in
   // D2. The ISM runs it one chunk late, while the tensor cores compute the next chunk's G1
   // (re-reading that chunk's records, an L2 hit); MSE runs it in order from S.u.
-  auto layer1_reverse = [&](int64_t cc) {
-    float4 uu[kPPT];
-#pragma unroll
-    for (int pp = 0; pp < kPPT; ++pp) {
-      if (MODE == 1) {
-        const int64_t p = cc * kCP + p0 + pp;
-        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (p < n) A = xv[p];
-        const float x = A.x < 0.f ? A.x + L : A.x;
-        uu[pp] = make_float4(x * x_scale, A.y, A.z, A.w);
-      } else {
-        uu[pp] = S.u[p0 + pp];
-      }
-    }
+  auto layer1_reverse = [&](int ub) {
     umma::wait_mma(&S.bar[2], phase2);
     phase2 ^= 1;
     umma::fence_after();
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     if (DIV) umma::tmem_ld12(tl + cD2 + kCP + p0, vf);
 #pragma unroll
     for (int pp = 0; pp < kPPT; ++pp) {
-      const float4 u = uu[pp];
+      const float4 u = S.u[ub][p0 + pp];
       const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
       const float sg = sigmoid(a);
       const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
@@ -285,12 +286,54 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       aw1[3] = fmaf(da1, u.w, aw1[3]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) gw1[i] += (double)aw1[i];
-    gb1 += (double)ab1;
+    for (int i = 0; i < 4; ++i) gw1[i] += aw1[i];
+    gb1 += ab1;
   };
 
-  int64_t prev = -1;  // chunk whose layer-1 reverse sweep is still pending (ISM)
+  bool pending = false;  // the previous chunk's layer-1 reverse sweep is still to run (ISM)
+  int ub = 0;            // S.u buffer of the current chunk
   int it = 0;
+  if (tid >= kNCW) {
+    // issuer warp: every GEMM of the CTA in chunk order, as soon as its operands are ready.
+    // (An MMA issue blocks while the tensor pipe's queue is full, so a compute warp that
+    // issued would stall for most of the GEMM time.)
+    bool fst = true;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      handoff_wait(6);  // X written (F1 of chunk c)
+      umma::fence_after();
+      if (lane == 0) {
+        umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
+                                                              false);  // W2 h1
+        if (DIV)
+          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(
+              tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);  // B d1
+        umma::commit(&S.bar[0]);
+      }
+      __syncwarp();
+      if (ISM) {
+        handoff_wait(7);  // Y written (F2b of chunk c)
+        umma::fence_after();
+        if (lane == 0) {
+          // G3 first: the next chunk's layer-1 sweep waits for it (X, Y reuse)
+          umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(tm + cD3, sYh, sYl, sXh,
+                                                                      sXl, !fst);  // da2 h1^T
+          if (DIV)
+            umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(
+                tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
+                !fst);  // y2 d1^T
+          umma::commit(&S.bar[1]);
+          umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(tm + cD2, sW2h, sW2l, sYh, sYl,
+                                                               false);  // W2^T da2
+          if (DIV)
+            umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(
+                tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
+          umma::commit(&S.bar[2]);
+        }
+        __syncwarp();
+        fst = false;
+      }
+    }
+  } else {
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
     SILU_TRACE(0);
     // each warpgroup loads, reduces and scores its own 8 particles: only the GEMM issue points
@@ -318,7 +361,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           if (MODE == 2) t = make_float4(in.Z[r], in.Z[in.ldz + r], in.Z[2 * in.ldz + r], 0.f);
         }
       }
-      S.u[pl] = u;
+      S.u[ub][pl] = u;
       S.w[pl] = wt;
       if (MODE == 2) tgt[pl] = t;
     }
@@ -328,7 +371,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     // F1: layer 1 -> X rows p (h1) and 32 + p (d1 = silu'(a1)), column h
 #pragma unroll
     for (int i = 0; i < kPPT; ++i) {
-      const float4 u = S.u[p0 + i];
+      const float4 u = S.u[ub][p0 + i];
       const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
       const float sg = sigmoid(a);
       st_split(rb[i & 7] + i * 128, a * sg);
@@ -336,19 +379,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     }
     fence_proxy_async();
     umma::fence_before();
-    __syncthreads();
-    umma::fence_after();
+    handoff_arrive(6);
     SILU_TRACE(2);
-    if (tid == 0) {
-      umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
-                                                            false);
-      umma::commit(&S.bar[0]);
-    } else if (DIV && tid == 32) {
-      umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(
-          tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);
-      umma::commit(&S.bar[0]);
-    }
-    if (MODE == 1 && prev >= 0) layer1_reverse(prev);  // overlaps this chunk's G1
+    if (MODE == 1 && pending) layer1_reverse(ub ^ 1);  // overlaps this chunk's G1
     SILU_TRACE(3);
     umma::wait_mma(&S.bar[0], phase);
     phase ^= 1;
@@ -357,11 +390,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 
     // F2a: s and div partials over this thread's h, reduced across the warp (particles
     // 0..7 of the warpgroup by a 32-value, 8..11 by a 16-value transpose-reduce)
-    // (the D1 columns stay in registers for F2b: one TMEM round trip per chunk saved)
-    float va[16], ve[16];
-    umma::tmem_ld12(tl + cD1 + p0, va);
-    if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
     {
+      float va[16], ve[16];
+      umma::tmem_ld12(tl + cD1 + p0, va);
+      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
       float v32[32], v16[16];
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
@@ -397,16 +429,16 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         const float4 t = tgt[p];
         const float r0 = s[0] - t.x, r1 = s[1] - t.y, r2 = s[2] - t.z;
         S.gs[p] = make_float4(2.f * wi * r0, 2.f * wi * r1, 2.f * wi * r2, 0.f);
-        loss += (double)(wi * (r0 * r0 + r1 * r1 + r2 * r2));
-        gb3[0] += (double)(2.f * wi * r0);
-        gb3[1] += (double)(2.f * wi * r1);
-        gb3[2] += (double)(2.f * wi * r2);
+        loss += wi * (r0 * r0 + r1 * r1 + r2 * r2);
+        gb3[0] += 2.f * wi * r0;
+        gb3[1] += 2.f * wi * r1;
+        gb3[2] += 2.f * wi * r2;
       } else {
         const float wt = S.w[p], tw = 2.f * wt;
         S.gs[p] = make_float4(tw * s[0], tw * s[1], tw * s[2], tw);
-        loss += (double)(wt * (s[0] * s[0] + s[1] * s[1] + s[2] * s[2] + 2.f * dv));
+        loss += wt * (s[0] * s[0] + s[1] * s[1] + s[2] * s[2] + 2.f * dv);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) gb3[k] += (double)(tw * s[k]);
+        for (int k = 0; k < 3; ++k) gb3[k] += tw * s[k];
       }
     }
     if (!ISM) {  // D1 is rewritten by the next chunk's G1 only after the next CTA barrier
@@ -414,12 +446,15 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       wg_sync(wg);
       continue;
     }
-    __syncthreads();  // F2b overwrites the Y tile that holds every warpgroup's partials
+    compute_sync();  // F2b overwrites the Y tile that holds every warpgroup's partials
     SILU_TRACE(6);
 
     // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
     {
       float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
+      float va[16], ve[16];
+      umma::tmem_ld12(tl + cD1 + p0, va);
+      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
 #pragma unroll
       for (int pp = 0; pp < kPPT; ++pp) {
         const float4 G = S.gs[p0 + pp];
@@ -441,50 +476,33 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         if (DIV) st_split(rb[pp & 7] + kY + kDivRows + pp * 128, G.w * d2);
       }
 #pragma unroll
-      for (int k = 0; k < 3; ++k) gw3[k] += (double)aw3[k];
-      gb2 += (double)ab2;
+      for (int k = 0; k < 3; ++k) gw3[k] += aw3[k];
+      gb2 += ab2;
     }
     fence_proxy_async();
     umma::fence_before();
-    __syncthreads();
-    umma::fence_after();
+    handoff_arrive(7);
     SILU_TRACE(7);
-    // two issuing threads in two warps: tid 0 the primal G2 then G3 halves, tid 32 the
-    // divergence halves, so both G2 halves reach the tensor pipe ahead of G3
-    if (tid == 0) {
-      umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(tm + cD2, sW2h, sW2l, sYh, sYl,
-                                                           false);  // W2^T da2
-      umma::commit(&S.bar[2]);
-      umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(tm + cD3, sYh, sYl, sXh, sXl,
-                                                                  !first);  // da2 h1^T
-      umma::commit(&S.bar[1]);  // overlaps F3 and the next chunk's record loads
-    } else if (DIV && tid == 32) {
-      umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(
-          tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
-      umma::commit(&S.bar[2]);
-      umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(
-          tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
-          !first);  // y2 d1^T
-      umma::commit(&S.bar[1]);
-    }
     first = false;
     if (MODE == 1) {
-      prev = c;
+      pending = true;
     } else {
-      layer1_reverse(c);
+      layer1_reverse(ub);
     }
     umma::fence_before();
     wg_sync(wg);
     SILU_TRACE(8);
+    ub ^= 1;
   }
-  if (MODE == 1 && prev >= 0) layer1_reverse(prev);
+  if (MODE == 1 && pending) layer1_reverse(ub ^ 1);
+  }
 
-  if (ISM) {
+  if (ISM && tid < kNCW) {
     if (!first) {
       umma::wait_mma(&S.bar[1], phase3);
       umma::fence_after();
     }
-    __syncthreads();  // every warpgroup is done with the X / Y tiles before they are reused
+    compute_sync();  // every warpgroup is done with the X / Y tiles before they are reused
     const int64_t width = 1 + silu_params(kH);
     const int64_t oW1 = 1, ob1 = oW1 + 4 * kH, oW2 = ob1 + kH, ob2 = oW2 + kH * kH,
                   oW3 = ob2 + kH, ob3 = oW3 + 3 * kH;
@@ -526,16 +544,17 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     mine[9] = tw3[0]; mine[10] = tw3[1]; mine[11] = tw3[2];
     double* lcomb = comb + 4 * kH * 12;  // [4 warpgroups][loss, gb3]
     if (wtid < 32) {
-      loss = warp_sum(loss);
+      const double lw = warp_sum((double)loss);
+      double g3w[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) gb3[k] = warp_sum(gb3[k]);
+      for (int k = 0; k < 3; ++k) g3w[k] = warp_sum((double)gb3[k]);
       if (wtid == 0) {
-        lcomb[4 * wg] = loss;
+        lcomb[4 * wg] = lw;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) lcomb[4 * wg + 1 + k] = gb3[k];
+        for (int k = 0; k < 3; ++k) lcomb[4 * wg + 1 + k] = g3w[k];
       }
     }
-    __syncthreads();
+    compute_sync();
     // dW1[h][1+k] tangent part: sum over rows r of W3[k][r] WM[r][h] (column h); warpgroup g
     // sums rows 32g..32g+31, the four partials are added in a fixed order below
     float* cwp = reinterpret_cast<float*>(lcomb + 16);  // [4][kH][3]
@@ -550,7 +569,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 #pragma unroll
       for (int k = 0; k < 3; ++k) cwp[(wg * kH + h) * 3 + k] = cw[k];
     }
-    __syncthreads();
+    compute_sync();
     if (wg == 0) {
       double t[12];
 #pragma unroll
