@@ -86,16 +86,25 @@ def landau_sorted(ci: CellIndex, particles: ParticleEnsemble, grid: Grid, gamma:
     return U_sorted
 
 
+def gather_scores_sorted(cell_index: CellIndex, scores, flags=None) -> torch.Tensor:
+    """Scatter pid-order scores (n, dv) into the sorted records' s lanes; returns the flags."""
+    n = cell_index.perm.numel()
+    dev = cell_index.sw.device
+    s = scores if isinstance(scores, torch.Tensor) else torch.as_tensor(np.asarray(scores))
+    sp = s.to(device=dev, dtype=torch.float32).t().contiguous()  # (dv, n) planes
+    dv = sp.shape[0]
+    flags = new_flags(dev) if flags is None else flags
+    _lib.call("spic_gather_scores", _lib.ptr(sp), n, _lib.ptr(cell_index.perm), n, dv,
+              _lib.ptr(cell_index.sw), _lib.ptr(flags), _lib.stream_handle())
+    return flags
+
+
 def collision_force(particles: ParticleEnsemble, scores, cell_index: CellIndex, grid: Grid,
                     gamma: float) -> torch.Tensor:
     """U (n, dv) for every particle (ref: collision.py:92-110); non-finite scores raise."""
     n, dv = particles.n, particles.dv
     dev = particles.x.device
-    s = scores if isinstance(scores, torch.Tensor) else torch.as_tensor(np.asarray(scores))
-    sp = s.to(device=dev, dtype=torch.float32).t().contiguous()  # (dv, n) planes
-    flags = new_flags(dev)
-    _lib.call("spic_gather_scores", _lib.ptr(sp), n, _lib.ptr(cell_index.perm), n, dv,
-              _lib.ptr(cell_index.sw), _lib.ptr(flags), _lib.stream_handle())
+    flags = gather_scores_sorted(cell_index, scores)
     if flags.cpu().numpy()[_lib.FLAG_BAD_SCORE]:
         raise ValueError("invalid score input")
     U_sorted = torch.empty(dv, n, dtype=torch.float32, device=dev)

@@ -450,10 +450,26 @@ __global__ void k_fold_splits(const float* __restrict__ part, int nsplit, int dv
 
 using namespace spic;
 
+// antisymmetric (unordered-pair) path, landau_sym.cu
+size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit);
+int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32_t* cell_start,
+                        const int32_t* sub_start, int32_t M, int32_t S, double eta,
+                        float uniform_w, int32_t nsplit, int32_t c_lo, int32_t c_hi,
+                        float* U_sorted, void* scratch, size_t scratch_bytes, void* stream);
+
+// SPIC_LANDAU_VARIANT: unset -> antisymmetric kernel where eligible, 'o' -> ordered packed
+// kernel, 's' -> ordered scalar kernel (A/B checks)
+static char landau_variant() {
+  const char* var = getenv("SPIC_LANDAU_VARIANT");
+  return var ? var[0] : 0;
+}
+
 extern "C" size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nsplit) {
-  if (nsplit <= 0) nsplit = auto_nsplit(n, M, dv);
+  const int32_t ns = nsplit <= 0 ? auto_nsplit(n, M, dv) : nsplit;
   size_t b = sizeof(int32_t) * (size_t)(M + 1 + 31);
-  if (nsplit > 1) b += sizeof(float) * (size_t)nsplit * dv * n + 256;
+  if (ns > 1) b += sizeof(float) * (size_t)ns * dv * n + 256;
+  if (dv == 3 && M >= 3 && landau_variant() == 0)
+    b = std::max(b, spic_landau_sym_scratch_bytes(n, M, nsplit));
   return b;
 }
 
@@ -479,9 +495,13 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   if (c_lo < 0 || c_hi > M || c_lo > c_hi) return SPIC_ERR_ARG;
   if (n < 0 || n > INT32_MAX || M < 1 || S < 1 || !(eta > 0) || (dv != 2 && dv != 3))
     return SPIC_ERR_ARG;
-  if (nsplit <= 0) nsplit = auto_nsplit(n, M, dv);
   if (scratch_bytes < spic_landau_scratch_bytes(n, M, dv, nsplit)) return SPIC_ERR_SCRATCH;
   if (n == 0) return SPIC_OK;
+  const char var = landau_variant();
+  if (dv == 3 && M >= 3 && gamma == -3.0 && uniform_w > 0.f && var == 0)
+    return spic_landau_sym_run(xv, sw, n, cell_start, sub_start, M, S, eta, uniform_w, nsplit,
+                               c_lo, c_hi, U_sorted, scratch, scratch_bytes, stream);
+  if (nsplit <= 0) nsplit = auto_nsplit(n, M, dv);
   cudaStream_t st = (cudaStream_t)stream;
   int32_t* tile_start = (int32_t*)scratch;
   float* Upart = U_sorted;
@@ -501,8 +521,7 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   // SPIC_LANDAU_VARIANT=s forces the scalar kernel (A/B checks); the packed configuration
   // (2 packed pairs per thread, 4 CTAs/SM, 2-way j unroll) won a sweep of RP 1..3, 2..8
   // CTAs/SM and unroll 1/2/4 on config 2
-  const char* var = getenv("SPIC_LANDAU_VARIANT");
-  const bool packed = dv == 3 && gm == 0 && !(var && var[0] == 's');
+  const bool packed = dv == 3 && gm == 0 && var != 's';
   constexpr int rp = kLandauRP;
   const int TI = packed ? kLandauNT * 2 * rp : kLandauTI;
   k_landau_tiles<<<1, 1024, 0, st>>>(cell_start, M, TI, tile_start, c_lo, c_hi); spic::count_launch();

@@ -1,0 +1,626 @@
+// landau_sym.cu — antisymmetric (unordered-pair) form of the binned Landau collision sum.
+//
+// Same operator as landau.cu (ref: collision.py:49-110): U_i = sum_j w_j T_ij with
+//     T_ij = psi(dx) |z|^-1 [ u - (z.u/|z|^2) z ],  z = v_i - v_j, u = s_i - s_j.
+// T is antisymmetric (T_ji = -T_ij: z and u both flip sign), so one evaluation of an
+// unordered pair {i, j} serves both targets: U_i += w T, U_j -= w T (uniform weights).
+// That halves the pair work of the ordered kernel (41 FLOP per unordered pair instead of
+// 2 x 38 for the two ordered ones).
+//
+// Enumeration (M >= 3, dv = 3, gamma = -3, uniform w). Records are sorted by (cell, sub-cell).
+// A target tile [t0, t1) of cell c owns the pairs it forms with its FORWARD window:
+//   seg0 = [t0, t1)            the diagonal block, evaluated one-sided (both orders),
+//   seg1 = [t1, ce)            the rest of cell c (every pair in a cell is within eta),
+//   seg2 = prefix of cell c+1  up to the sub-cell after the tile's last one (periodic shift
+//                              +L for c = M-1).
+// Every unordered pair of the 3-cell stencil is thus evaluated exactly once: pairs inside a
+// cell by the tile of the earlier record, pairs across the c|c+1 border by the tile in c.
+//
+// Accumulation is deterministic. The register (i) side sums in a fixed order per thread as
+// in the ordered kernel. The streamed (j) side of each record is reduced over the CTA's
+// threads (warp reduce-scatter over 8 records + fixed-order combine of the warps in shared
+// memory) and written once per (tile, record) into a slot buffer; k_sym_fold sums a record's
+// slots in a fixed order (tiles of its own cell before it, then the tiles of cell c-1 whose
+// seg2 reaches it). The slot count is data dependent (~ n * n_cell / TI); if it exceeds the
+// caller's scratch, the tile table clears a device flag and the same kernels run the ordered
+// (full-stencil, one-sided) enumeration instead — graph-safe, no host synchronisation.
+#include <algorithm>
+#include <cstdlib>
+
+#include "f32x2.cuh"
+#include "pairs.cuh"
+
+namespace spic {
+
+constexpr int kSymTJ = 256;     // records per stage
+constexpr int kSymStages = 3;
+constexpr int kSymRP = 2;       // packed target pairs per thread (4 targets)
+
+struct SymMeta {
+  int len1;  // own-cell forward length ce - t1; -1 marks a halo tile (seg2 only)
+  int len2;  // next-cell prefix length
+};
+
+__device__ __forceinline__ bool sym_tile_cell(int c, int M, int c_lo, int c_hi, bool partial) {
+  if (c >= c_lo && c < c_hi) return true;
+  return partial && c == (c_lo - 1 + M) % M;
+}
+
+// Single CTA: tile_start[0..M] (targets tiles per cell, incl. the halo cell c_lo-1 of a
+// partial range), per-tile SymMeta, slot offsets off[0..T], the symmetric-path flag.
+__global__ void __launch_bounds__(1024) k_sym_tiles(
+    const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start, int M, int S,
+    int TI, int c_lo, int c_hi, int64_t cap_slots, int32_t* __restrict__ tile_start,
+    SymMeta* __restrict__ meta, int64_t* __restrict__ off, int32_t* __restrict__ symflag) {
+  __shared__ long long ws[33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool partial = (c_hi - c_lo) < M;
+  // phase 1: tiles per cell, exclusive scan
+  long long carry = 0;
+  for (int base = 0; base < M; base += blockDim.x) {
+    const int c = base + threadIdx.x;
+    long long v = 0;
+    if (c < M && sym_tile_cell(c, M, c_lo, c_hi, partial))
+      v = (cell_start[c + 1] - cell_start[c] + TI - 1) / TI;
+    long long inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      long long s = lane < nw ? ws[lane] : 0;
+      long long si = s;
+      for (int o = 1; o < 32; o <<= 1) {
+        long long t = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) si += t;
+      }
+      ws[lane] = si - s;
+      if (lane == 31) ws[32] = si;
+    }
+    __syncthreads();
+    if (c < M) tile_start[c] = (int)(carry + ws[wid] + inc - v);
+    carry += ws[32];
+    __syncthreads();
+  }
+  const int T = (int)carry;
+  if (threadIdx.x == 0) {
+    tile_start[M] = T;
+    tile_start[M + 1] = 0;
+  }
+  __syncthreads();
+  // phase 2: per-tile forward-window lengths and their exclusive scan
+  long long ocarry = 0;
+  for (int base = 0; base < T; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    long long F = 0;
+    if (t < T) {
+      int lo = 0, hi = M;  // largest c with tile_start[c] <= t
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (tile_start[mid] <= t) lo = mid; else hi = mid;
+      }
+      const int c = lo;
+      const int cs = cell_start[c], ce = cell_start[c + 1];
+      const int t1 = min(cs + (t - tile_start[c] + 1) * TI, ce);
+      const bool halo = !(c >= c_lo && c < c_hi);
+      const int cn = (c + 1) % M;
+      int len2;
+      if (S > 1 && sub_start) {
+        const int32_t* ss = sub_start + (size_t)c * S;
+        int b = 0;  // sub-cell of the tile's last record
+        for (int k = 1; k < S; ++k)
+          if (ss[k] <= t1 - 1) b = k;
+        const int hs = min(S - 1, b + 1);
+        len2 = sub_start[(size_t)cn * S + hs + 1] - cell_start[cn];
+      } else {
+        len2 = cell_start[cn + 1] - cell_start[cn];
+      }
+      SymMeta m;
+      m.len1 = halo ? -1 : ce - t1;
+      m.len2 = len2;
+      meta[t] = m;
+      F = (long long)max(m.len1, 0) + len2;
+    }
+    long long inc = F;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long x = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += x;
+    }
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      long long s = lane < nw ? ws[lane] : 0;
+      long long si = s;
+      for (int o = 1; o < 32; o <<= 1) {
+        long long x = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) si += x;
+      }
+      ws[lane] = si - s;
+      if (lane == 31) ws[32] = si;
+    }
+    __syncthreads();
+    if (t < T) off[t] = ocarry + ws[wid] + inc - F;
+    ocarry += ws[32];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    off[T] = ocarry;
+    *symflag = ocarry <= cap_slots ? 1 : 0;
+  }
+}
+
+// j-window tile with its kind: two-sided tiles also carry the slot offset of their first
+// record relative to off[tile]
+struct SymTileDesc {
+  int pos, cnt, wofs;
+  float shift;
+  bool two;
+};
+
+struct SymWindow {
+  int start[3], len[3], wofs[3];
+  float shift[3];
+  bool two[3];
+  int nseg;
+};
+
+__device__ __forceinline__ int sym_window_tiles(const SymWindow& w, int jlo, int jhi) {
+  int o = 0, nt = 0;
+  for (int s = 0; s < w.nseg; ++s) {
+    const int a = max(jlo, o), b = min(jhi, o + w.len[s]);
+    if (b > a) nt += (b - a + kSymTJ - 1) / kSymTJ;
+    o += w.len[s];
+  }
+  return nt;
+}
+
+__device__ __forceinline__ SymTileDesc sym_window_tile(const SymWindow& w, int jlo, int jhi,
+                                                       int q) {
+  int o = 0;
+  SymTileDesc d{0, 0, 0, 0.f, false};
+  for (int s = 0; s < w.nseg; ++s) {
+    const int a = max(jlo, o), b = min(jhi, o + w.len[s]);
+    if (b > a) {
+      const int nt = (b - a + kSymTJ - 1) / kSymTJ;
+      if (q < nt) {
+        const int lo = a + q * kSymTJ;
+        d.pos = w.start[s] + (lo - o);
+        d.cnt = min(kSymTJ, b - lo);
+        d.shift = w.shift[s];
+        d.two = w.two[s];
+        d.wofs = w.wofs[s] + (lo - o);
+        return d;
+      }
+      q -= nt;
+    }
+    o += w.len[s];
+  }
+  return d;
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// One CTA per (target tile, j-split). NT threads, 4 targets per thread as two packed
+// (even, odd) pairs; j records broadcast from shared memory (one-sided stages) or read in a
+// per-lane XOR order inside groups of 8 (two-sided stages, so the warp reduce-scatter of the
+// j-side needs no selects: lane l holds record (k ^ m_l), m_l = (l >> 2) & 7).
+template <int NT>
+__global__ void __launch_bounds__(NT, 2048 / NT / 4)
+    k_landau_sym(const float4* __restrict__ xv, const float4* __restrict__ sw,
+                 const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
+                 const int32_t* __restrict__ tile_start, const SymMeta* __restrict__ meta,
+                 const int64_t* __restrict__ off, const int32_t* __restrict__ symflag, int M,
+                 int S, float L, float wie, float wie2, int nsplit, float* __restrict__ Upart,
+                 float* __restrict__ Jslot, int64_t n) {
+  constexpr int RP = kSymRP;
+  constexpr int TI = NT * 2 * RP;
+  constexpr int NW = NT / 32;
+  // dynamic shared memory (128-aligned by hand): stages of [xv records | sw records] (the sw
+  // half at a fixed byte offset), the double-buffered per-warp j-side sums, the mbarriers
+  extern __shared__ unsigned char s_dyn[];
+  unsigned char* s_base = (unsigned char*)(((uintptr_t)s_dyn + 127) & ~(uintptr_t)127);
+  auto s_rec = reinterpret_cast<float4(*)[2][kSymTJ]>(s_base);
+  auto s_jp = reinterpret_cast<float(*)[NW][kSymTJ * 3]>(s_base + sizeof(float4) * kSymStages * 2 * kSymTJ);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_base + sizeof(float4) * kSymStages * 2 * kSymTJ +
+                                                sizeof(float) * 2 * NW * kSymTJ * 3);
+  const int tile = blockIdx.x, split = blockIdx.y;
+  if (tile >= tile_start[M]) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // zero the stage buffers once (padding records beyond a stage's count must be finite)
+  for (int k = threadIdx.x; k < kSymStages * 2 * kSymTJ; k += NT)
+    (&s_rec[0][0][0])[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSymStages; ++s) mbar_init(&s_bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const f2 W1c = mk2(wie, wie), nW2 = mk2(-wie2, -wie2);
+  int lo = 0, hi = M;  // cell of this tile
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(tile_start + mid) <= tile) lo = mid; else hi = mid;
+  }
+  const int c = lo;
+  const int cs = cell_start[c], ce = cell_start[c + 1];
+  const int t0 = cs + (tile - tile_start[c]) * TI;
+  const int t1 = min(t0 + TI, ce);
+  const bool sym = *symflag != 0;
+  SymWindow win;
+  win.nseg = 0;
+  int64_t slot0 = 0;
+  if (sym) {
+    const SymMeta m = meta[tile];
+    slot0 = off[tile];
+    if (m.len1 >= 0) {
+      win.start[0] = t0; win.len[0] = t1 - t0; win.shift[0] = 0.f; win.two[0] = false;
+      win.wofs[0] = 0;
+      win.start[1] = t1; win.len[1] = m.len1; win.shift[1] = 0.f; win.two[1] = true;
+      win.wofs[1] = 0;
+      win.nseg = 2;
+    }
+    const int cn = c + 1 == M ? 0 : c + 1;
+    const int k = win.nseg;
+    win.start[k] = cell_start[cn]; win.len[k] = m.len2;
+    win.shift[k] = c + 1 == M ? L : 0.f; win.two[k] = true;
+    win.wofs[k] = max(m.len1, 0);
+    win.nseg = k + 1;
+  } else {
+    const Window w = build_window(cell_start, sub_start, M, S, c, t0, t1, L);
+    for (int s = 0; s < w.nseg; ++s) {
+      win.start[s] = w.start[s]; win.len[s] = w.len[s]; win.shift[s] = w.shift[s];
+      win.two[s] = false; win.wofs[s] = 0;
+    }
+    win.nseg = w.nseg;
+  }
+  int wlen = 0;
+  for (int s = 0; s < win.nseg; ++s) wlen += win.len[s];
+  const int jlo = (int)(((long long)wlen * split) / nsplit);
+  const int jhi = (int)(((long long)wlen * (split + 1)) / nsplit);
+  const int ntiles = sym_window_tiles(win, jlo, jhi);
+
+  f2 X[RP], V0[RP], V1[RP], V2[RP], S0[RP], S1[RP], S2[RP], A0[RP], A1[RP], A2[RP];
+#pragma unroll
+  for (int r = 0; r < RP; ++r) {
+    float4 Ae = make_float4(1e30f, 0.f, 0.f, 0.f), Be = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 Ao = Ae, Bo = Be;
+    const int pe = t0 + threadIdx.x + (2 * r) * NT;
+    const int po = pe + NT;
+    if (pe < t1) { Ae = xv[pe]; Be = sw[pe]; }
+    if (po < t1) { Ao = xv[po]; Bo = sw[po]; }
+    X[r] = mk2(Ae.x, Ao.x);
+    V0[r] = mk2(Ae.y, Ao.y); V1[r] = mk2(Ae.z, Ao.z); V2[r] = mk2(Ae.w, Ao.w);
+    S0[r] = mk2(Be.x, Bo.x); S1[r] = mk2(Be.y, Bo.y); S2[r] = mk2(Be.z, Bo.z);
+    A0[r] = A1[r] = A2[r] = mk2(0.f, 0.f);
+  }
+  auto issue = [&](int q) {
+    const SymTileDesc d = sym_window_tile(win, jlo, jhi, q);
+    const int st = q % kSymStages;
+    // padding records up to the next group of 8: x far away -> psi = 0
+    const int ru = min(kSymTJ, (d.cnt + 7) & ~7);
+    for (int j = d.cnt; j < ru; ++j) s_rec[st][0][j].x = 1e30f;
+    mbar_expect_tx(&s_bar[st], (uint32_t)(2 * d.cnt * sizeof(float4)));
+    bulk_g2s(&s_rec[st][0][0], xv + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
+    bulk_g2s(&s_rec[st][1][0], sw + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
+  };
+  if (threadIdx.x == 0) {
+    fence_proxy_async();
+    for (int q = 0; q < min(ntiles, kSymStages); ++q) issue(q);
+  }
+  __syncthreads();  // padding writes of the prologue stages
+  const uint32_t mofs = (uint32_t)(((lane >> 2) & 7) * sizeof(float4));
+  constexpr uint32_t kSwOfs = kSymTJ * sizeof(float4);
+
+  for (int q = 0; q < ntiles; ++q) {
+    const int st = q % kSymStages;
+    const SymTileDesc d = sym_window_tile(win, jlo, jhi, q);
+    f2 XA[RP];
+    const f2 sh = mk2(d.shift, d.shift);
+#pragma unroll
+    for (int r = 0; r < RP; ++r) XA[r] = sub2(X[r], sh);
+    mbar_wait(&s_bar[st], (uint32_t)((q / kSymStages) & 1));
+    const uint32_t sbase = smem_u32(&s_rec[st][0][0]);
+    if (!d.two) {
+      // one-sided: broadcast records, i-side only (the diagonal block / ordered fallback)
+      const float4* __restrict__ P = s_rec[st][0];
+      const float4* __restrict__ Q = s_rec[st][1];
+#pragma unroll 2
+      for (int jj = 0; jj < d.cnt; ++jj) {
+        const float4 A = P[jj];
+        const float4 B = Q[jj];
+        const f2 xj = mk2(A.x, A.x), vj0 = mk2(A.y, A.y), vj1 = mk2(A.z, A.z), vj2 = mk2(A.w, A.w);
+        const f2 sj0 = mk2(B.x, B.x), sj1 = mk2(B.y, B.y), sj2 = mk2(B.z, B.z);
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          const f2 dx = sub2(XA[r], xj);
+          float ce_, co_;
+          un2(fma2(abs2(dx), nW2, W1c), ce_, co_);
+          ce_ = fmaxf(ce_, 0.f);
+          co_ = fmaxf(co_, 0.f);
+          const f2 z0 = sub2(V0[r], vj0), z1 = sub2(V1[r], vj1), z2 = sub2(V2[r], vj2);
+          const f2 u0 = sub2(S0[r], sj0), u1 = sub2(S1[r], sj1), u2 = sub2(S2[r], sj2);
+          const f2 zz = fma2(z2, z2, fma2(z1, z1, mul2(z0, z0)));
+          const f2 zu = fma2(z2, u2, fma2(z1, u1, mul2(z0, u0)));
+          float zze, zzo;
+          un2(zz, zze, zzo);
+          const float qe = rsqrtf(zze), qo = rsqrtf(zzo);
+          const f2 rp = mk2(zze > kEps2 ? qe : 0.f, zzo > kEps2 ? qo : 0.f);
+          const f2 cw = mul2(mk2(ce_, co_), rp);
+          const f2 nq = neg2(mul2(mul2(rp, rp), zu));
+          A0[r] = fma2(cw, fma2(nq, z0, u0), A0[r]);
+          A1[r] = fma2(cw, fma2(nq, z1, u1), A1[r]);
+          A2[r] = fma2(cw, fma2(nq, z2, u2), A2[r]);
+        }
+      }
+    } else {
+      float* jp = &s_jp[q & 1][wid][0];
+      for (int jb = 0; jb < d.cnt; jb += 8) {
+        float P0[8], P1[8], P2[8];
+        const uint32_t gb = (sbase + (uint32_t)jb * sizeof(float4)) | mofs;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t a = gb ^ (uint32_t)(k * sizeof(float4));
+          const float4 A = lds128(a);
+          const float4 B = lds128(a + kSwOfs);
+          const f2 xj = mk2(A.x, A.x), vj0 = mk2(A.y, A.y), vj1 = mk2(A.z, A.z), vj2 = mk2(A.w, A.w);
+          const f2 sj0 = mk2(B.x, B.x), sj1 = mk2(B.y, B.y), sj2 = mk2(B.z, B.z);
+          f2 J0, J1, J2;
+#pragma unroll
+          for (int r = 0; r < RP; ++r) {
+            const f2 dx = sub2(XA[r], xj);
+            float ce_, co_;
+            un2(fma2(abs2(dx), nW2, W1c), ce_, co_);
+            ce_ = fmaxf(ce_, 0.f);
+            co_ = fmaxf(co_, 0.f);
+            const f2 z0 = sub2(V0[r], vj0), z1 = sub2(V1[r], vj1), z2 = sub2(V2[r], vj2);
+            const f2 u0 = sub2(S0[r], sj0), u1 = sub2(S1[r], sj1), u2 = sub2(S2[r], sj2);
+            const f2 zz = fma2(z2, z2, fma2(z1, z1, mul2(z0, z0)));
+            const f2 zu = fma2(z2, u2, fma2(z1, u1, mul2(z0, u0)));
+            float zze, zzo;
+            un2(zz, zze, zzo);
+            const float qe = rsqrtf(zze), qo = rsqrtf(zzo);
+            const f2 rp = mk2(zze > kEps2 ? qe : 0.f, zzo > kEps2 ? qo : 0.f);
+            const f2 cw = mul2(mk2(ce_, co_), rp);
+            const f2 nq = neg2(mul2(mul2(rp, rp), zu));
+            const f2 d0 = fma2(nq, z0, u0), d1 = fma2(nq, z1, u1), d2 = fma2(nq, z2, u2);
+            A0[r] = fma2(cw, d0, A0[r]);
+            A1[r] = fma2(cw, d1, A1[r]);
+            A2[r] = fma2(cw, d2, A2[r]);
+            if (r == 0) {
+              J0 = mul2(cw, d0); J1 = mul2(cw, d1); J2 = mul2(cw, d2);
+            } else {
+              J0 = fma2(cw, d0, J0); J1 = fma2(cw, d1, J1); J2 = fma2(cw, d2, J2);
+            }
+          }
+          float e, o;
+          un2(J0, e, o); P0[k] = e + o;
+          un2(J1, e, o); P1[k] = e + o;
+          un2(J2, e, o); P2[k] = e + o;
+        }
+        // warp reduce-scatter: after the xor-16/8/4 exchanges lane l holds the 8-lane sum of
+        // record jb + m_l; the xor-2/1 butterflies complete the 32-lane sum
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          P0[k] += __shfl_xor_sync(0xffffffffu, P0[k + 4], 16);
+          P1[k] += __shfl_xor_sync(0xffffffffu, P1[k + 4], 16);
+          P2[k] += __shfl_xor_sync(0xffffffffu, P2[k + 4], 16);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          P0[k] += __shfl_xor_sync(0xffffffffu, P0[k + 2], 8);
+          P1[k] += __shfl_xor_sync(0xffffffffu, P1[k + 2], 8);
+          P2[k] += __shfl_xor_sync(0xffffffffu, P2[k + 2], 8);
+        }
+        P0[0] += __shfl_xor_sync(0xffffffffu, P0[1], 4);
+        P1[0] += __shfl_xor_sync(0xffffffffu, P1[1], 4);
+        P2[0] += __shfl_xor_sync(0xffffffffu, P2[1], 4);
+        P0[0] += __shfl_xor_sync(0xffffffffu, P0[0], 2);
+        P1[0] += __shfl_xor_sync(0xffffffffu, P1[0], 2);
+        P2[0] += __shfl_xor_sync(0xffffffffu, P2[0], 2);
+        P0[0] += __shfl_xor_sync(0xffffffffu, P0[0], 1);
+        P1[0] += __shfl_xor_sync(0xffffffffu, P1[0], 1);
+        P2[0] += __shfl_xor_sync(0xffffffffu, P2[0], 1);
+        const int cc = lane & 3;
+        if (cc < 3) jp[(jb + ((lane >> 2) & 7)) * 3 + cc] = cc == 0 ? P0[0] : (cc == 1 ? P1[0] : P2[0]);
+      }
+    }
+    __syncthreads();  // stage st consumed; warp slices of a two-sided stage complete
+    if (threadIdx.x == 0 && q + kSymStages < ntiles) {
+      fence_proxy_async();
+      issue(q + kSymStages);
+    }
+    if (d.two) {  // fixed-order combine of the warps' j-side sums: U_j -= w T
+      const float* jb = &s_jp[q & 1][0][0];
+      float* dst = Jslot + (size_t)(slot0 + d.wofs) * 3;
+      for (int k = threadIdx.x; k < d.cnt * 3; k += NT) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += jb[w * kSymTJ * 3 + k];
+        dst[k] = -s;
+      }
+    }
+  }
+  float* out = Upart + (size_t)split * 3 * n;
+#pragma unroll
+  for (int r = 0; r < RP; ++r) {
+    float a0e, a0o, a1e, a1o, a2e, a2o;
+    un2(A0[r], a0e, a0o);
+    un2(A1[r], a1e, a1o);
+    un2(A2[r], a2e, a2o);
+    const int pe = t0 + threadIdx.x + (2 * r) * NT;
+    const int po = pe + NT;
+    if (pe < t1) { out[pe] = a0e; out[n + pe] = a1e; out[2 * n + pe] = a2e; }
+    if (po < t1) { out[po] = a0o; out[n + po] = a1o; out[2 * n + po] = a2o; }
+  }
+}
+
+// U_sorted[d][p] = sum_split Upart + (symmetric path) the record's j-side slots, all in a
+// fixed order: tiles of its own cell before its tile, then the tiles of cell c-1 whose seg2
+// reaches it. Sorted positions [k0, k1) only (a domain rank's owned targets).
+__global__ void __launch_bounds__(256) k_sym_fold(
+    const float* __restrict__ Upart, int nsplit, int64_t n, const int32_t* __restrict__ cell_start,
+    const int32_t* __restrict__ tile_start, const SymMeta* __restrict__ meta,
+    const int64_t* __restrict__ off, const int32_t* __restrict__ symflag, int M, int TI,
+    const float* __restrict__ Jslot, int c_lo, int c_hi, float* __restrict__ U) {
+  const bool sym = *symflag != 0;
+  const int64_t k0 = cell_start[c_lo], k1 = cell_start[c_hi];
+  for (int64_t p = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < k1;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    float u0 = 0.f, u1 = 0.f, u2 = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+      const float* P = Upart + (size_t)s * 3 * n;
+      u0 += P[p]; u1 += P[n + p]; u2 += P[2 * n + p];
+    }
+    if (sym) {
+      int lo = 0, hi = M;  // cell of p: largest c with cell_start[c] <= p
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(cell_start + mid) <= p) lo = mid; else hi = mid;
+      }
+      const int c = lo;
+      const int cs = cell_start[c];
+      const int rel = (int)(p - cs);
+      const int tc = tile_start[c];
+      const int tp = tc + rel / TI;
+      for (int t = tc; t < tp; ++t) {
+        const int64_t sl = off[t] + (rel - (t - tc + 1) * TI);
+        u0 += Jslot[sl * 3]; u1 += Jslot[sl * 3 + 1]; u2 += Jslot[sl * 3 + 2];
+      }
+      const int cm = c == 0 ? M - 1 : c - 1;
+      for (int t = tile_start[cm]; t < tile_start[cm + 1]; ++t) {
+        const SymMeta m = meta[t];
+        if (rel < m.len2) {
+          const int64_t sl = off[t] + max(m.len1, 0) + rel;
+          u0 += Jslot[sl * 3]; u1 += Jslot[sl * 3 + 1]; u2 += Jslot[sl * 3 + 2];
+        }
+      }
+    }
+    U[p] = u0; U[n + p] = u1; U[2 * n + p] = u2;
+  }
+}
+
+}  // namespace spic
+
+using namespace spic;
+
+namespace {
+
+constexpr size_t sym_smem_bytes(int NT) {
+  return 128 + sizeof(float4) * kSymStages * 2 * kSymTJ + sizeof(float) * 2 * (NT / 32) * kSymTJ * 3 +
+         sizeof(uint64_t) * kSymStages;
+}
+
+int sym_nt() {
+  const char* e = getenv("SPIC_SYM_NT");
+  return (e && atoi(e) == 256) ? 256 : 128;
+}
+
+}  // namespace
+
+// Layout of the symmetric path's scratch (all offsets 256-aligned):
+//   tile_start i32[M+2] | meta SymMeta[Tmax] | off i64[Tmax+1] | flag i32 | Upart f32[nsplit][3][n]
+//   | Jslot f32[cap][3]
+struct SymScratch {
+  int32_t* tile_start;
+  SymMeta* meta;
+  int64_t* off;
+  int32_t* flag;
+  float* Upart;
+  float* Jslot;
+  int64_t cap;
+  size_t bytes;
+};
+
+static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+static SymScratch sym_layout(void* base, int64_t n, int M, int nsplit, int TI) {
+  SymScratch s{};
+  const int64_t Tmax = n / TI + M + 2;
+  // slot estimate for a near-uniform ensemble: each tile's forward window ~ one cell plus a
+  // sub-cell; 1.3x headroom (an exceeding ensemble runs the ordered path, see k_sym_tiles)
+  const int64_t ncell = n / std::max(M, 1);
+  int64_t cap = (int64_t)(1.3 * (double)Tmax * (double)(ncell + 2 * TI)) + 4096;
+  if (const char* e = getenv("SPIC_SYM_CAP_SLOTS")) cap = atoll(e);  // tests: force the fallback
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t at = o;
+    o = align256(o + b);
+    return (char*)base + at;
+  };
+  s.tile_start = (int32_t*)take(sizeof(int32_t) * (M + 2));
+  s.meta = (SymMeta*)take(sizeof(SymMeta) * Tmax);
+  s.off = (int64_t*)take(sizeof(int64_t) * (Tmax + 1));
+  s.flag = (int32_t*)take(sizeof(int32_t) * 8);
+  s.Upart = (float*)take(sizeof(float) * (size_t)nsplit * 3 * n);
+  s.Jslot = (float*)take(sizeof(float) * (size_t)cap * 3);
+  s.cap = cap;
+  s.bytes = o;
+  return s;
+}
+
+// nsplit for the symmetric kernel: whole waves of (CTAs per SM) x SMs
+int spic_landau_sym_nsplit(int64_t n, int32_t M) {
+  const int NT = sym_nt();
+  return pair_nsplit_slots(n, M, NT * 2 * kSymRP, (2048 / NT / 4) * kNumSMs);
+}
+
+size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit) {
+  const int NT = sym_nt();
+  if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
+  return sym_layout(nullptr, n, M, nsplit, NT * 2 * kSymRP).bytes + 256;
+}
+
+int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32_t* cell_start,
+                        const int32_t* sub_start, int32_t M, int32_t S, double eta,
+                        float uniform_w, int32_t nsplit, int32_t c_lo, int32_t c_hi,
+                        float* U_sorted, void* scratch, size_t scratch_bytes, void* stream) {
+  const int NT = sym_nt();
+  const int TI = NT * 2 * kSymRP;
+  if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
+  uintptr_t b = ((uintptr_t)scratch + 255) & ~(uintptr_t)255;
+  SymScratch s = sym_layout((void*)b, n, M, nsplit, TI);
+  if (s.bytes + (b - (uintptr_t)scratch) > scratch_bytes) return SPIC_ERR_SCRATCH;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double L = (double)M * eta;
+  const float wie = (float)((double)uniform_w / eta), wie2 = (float)((double)uniform_w / (eta * eta));
+  k_sym_tiles<<<1, 1024, 0, st>>>(cell_start, S > 1 ? sub_start : nullptr, M, S, TI, c_lo, c_hi,
+                                  s.cap, s.tile_start, s.meta, s.off, s.flag);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  const bool partial = (c_hi - c_lo) < M;
+  const int64_t ncells = (c_hi - c_lo) + (partial ? 1 : 0);
+  dim3 grid((unsigned)(n / TI + ncells + 1), (unsigned)nsplit);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_landau_sym<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sym_smem_bytes(128));
+    cudaFuncSetAttribute(k_landau_sym<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sym_smem_bytes(256));
+    attr_set = true;
+  }
+  if (NT == 256)
+    k_landau_sym<256><<<grid, 256, sym_smem_bytes(256), st>>>(
+        (const float4*)xv, (const float4*)sw, cell_start, S > 1 ? sub_start : nullptr,
+        s.tile_start, s.meta, s.off, s.flag, M, S, (float)L, wie, wie2, nsplit, s.Upart, s.Jslot, n);
+  else
+    k_landau_sym<128><<<grid, 128, sym_smem_bytes(128), st>>>(
+        (const float4*)xv, (const float4*)sw, cell_start, S > 1 ? sub_start : nullptr,
+        s.tile_start, s.meta, s.off, s.flag, M, S, (float)L, wie, wie2, nsplit, s.Upart, s.Jslot, n);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+  if (blocks > 0) {  // owned sorted range [cell_start[c_lo], cell_start[c_hi]) read on device
+    k_sym_fold<<<blocks, 256, 0, st>>>(s.Upart, nsplit, n, cell_start, s.tile_start, s.meta,
+                                       s.off, s.flag, M, TI, s.Jslot, c_lo, c_hi, U_sorted);
+    spic::count_launch();
+    SPIC_CHECK_LAUNCH();
+  }
+  return SPIC_OK;
+}

@@ -190,9 +190,9 @@ static __global__ void k_landau_tiles(const int32_t* __restrict__ cell_start, in
 
 // j-split of a pair kernel: choose nsplit so the (tile, split) CTA count fills whole waves
 // of the resident CTA slots (4 per SM); wave quantisation, not the pair count, sets the tail
-static inline int pair_nsplit(int64_t n, int M, int TI) {
+static inline int pair_nsplit_slots(int64_t n, int M, int TI, int resident) {
   const double tiles = (double)(n / TI) + 0.5 * M > 1.0 ? (double)(n / TI) + 0.5 * M : 1.0;
-  const double slots = 4.0 * kNumSMs;
+  const double slots = (double)resident;
   const int64_t window = 2 * n / (M > 1 ? M : 1);  // records in a culled j-window (approx.)
   int cap = (int)(window / 1024);
   cap = cap < 1 ? 1 : (cap > 16 ? 16 : cap);
@@ -208,6 +208,10 @@ static inline int pair_nsplit(int64_t n, int M, int TI) {
     }
   }
   return best;
+}
+
+static inline int pair_nsplit(int64_t n, int M, int TI) {
+  return pair_nsplit_slots(n, M, TI, 4 * kNumSMs);
 }
 
 }  // namespace spic

@@ -668,3 +668,104 @@ def test_vml_engine_with_collisions_matches_oracle(spic):
     dxx = np.abs(xs - st["x"])
     assert np.max(np.minimum(dxx, L - dxx)) <= 1e-5 * L
     check_field(p.v.double().cpu().numpy(), st["v"], tol=1e-5)
+
+
+# ------------------------------------------------- antisymmetric pair path (landau_sym.cu)
+def _landau_sorted_env(p, grid, ci, env):
+    """U (sorted order) through spic_landau with SPIC_* environment overrides."""
+    import os
+
+    from paper_2603_25832_b200.collision import landau_sorted
+
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        U = torch.empty(3, p.n, dtype=torch.float32, device="cuda")
+        landau_sorted(ci, p, grid, -3.0, U)
+        torch.cuda.synchronize()
+        return U.double().cpu().numpy()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("case", ["config0", "M3_ragged", "clustered", "tiny_cells"])
+def test_antisymmetric_pair_path_matches_ordered_and_oracle(spic, case):
+    """The unordered-pair kernel (default for dv = 3, gamma = -3, uniform w, M >= 3) against
+    the ordered kernel (SPIC_LANDAU_VARIANT=o) and the float64 oracle; its ordered fallback
+    (slot capacity forced to 0) is the ordered enumeration; runs are bit-reproducible."""
+    from paper_2603_25832_b200.collision import build_cell_index, gather_scores_sorted
+    from paper_2603_25832_b200.pic import Grid
+
+    rng = np.random.default_rng({"config0": 1, "M3_ragged": 2, "clustered": 3, "tiny_cells": 4}[case])
+    if case == "config0":
+        n, M, L, S = 65536, 64, 4 * math.pi, 16
+        x = rng.uniform(0, L, n)
+    elif case == "M3_ragged":  # 3 cells, counts not multiples of the tile, wrap pairs
+        n, M, L, S = 3001, 3, 3.0, 4
+        x = np.concatenate([rng.uniform(0, 1, 1700), rng.uniform(1, 2, 300), rng.uniform(2, 3, 1001)])
+    elif case == "clustered":  # empty cells, one dense cell, records near cell borders
+        n, M, L, S = 20000, 16, 8.0, 8
+        x = np.concatenate([rng.uniform(2.0, 2.5, 12000), rng.uniform(0, L, 7990),
+                            np.full(10, 4.0 - 1e-6)])
+    else:  # fewer particles than cells
+        n, M, L, S = 100, 64, 2 * math.pi, 1
+        x = rng.uniform(0, L, n)
+    x = x.astype(np.float32).astype(np.float64)
+    x[x >= L] = 0.0
+    v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
+    v[5] = v[6]  # a z = 0 pair
+    s = (rng.normal(size=(n, 3)) * 2).astype(np.float32).astype(np.float64)
+    p = ens(x, v, np.full(n, L / n))
+    grid = Grid(M, L / M)
+    ci = build_cell_index(p, grid, S=S)
+    gather_scores_sorted(ci, s)
+    perm = ci.perm.cpu().numpy()
+    ref = O.collision_force(x, v, p.w.double().cpu().numpy(), s, grid.eta, M, -3.0)[perm].T
+    U_sym = _landau_sorted_env(p, grid, ci, {})
+    U_sym2 = _landau_sorted_env(p, grid, ci, {})
+    U_ord = _landau_sorted_env(p, grid, ci, {"SPIC_LANDAU_VARIANT": "o"})
+    U_fb = _landau_sorted_env(p, grid, ci, {"SPIC_SYM_CAP_SLOTS": "0"})
+    check_field(U_sym, ref)
+    check_field(U_ord, ref)
+    check_field(U_fb, ref)
+    assert np.array_equal(U_sym, U_sym2)
+    # the fallback runs the same ordered enumeration as the ordered kernel (different blocking)
+    check_field(U_fb, U_ord, tol=1e-5)
+    # antisymmetry: total momentum of the unordered sum vanishes to float32 rounding
+    mom = np.abs(U_sym.sum(1)).max() / np.abs(U_sym).sum()
+    assert mom < 1e-6, mom
+
+
+def test_antisymmetric_pair_path_partial_cell_range(spic):
+    """spic_landau_range over owned cells [c_lo, c_hi) (a domain rank's targets, halo cell
+    c_lo - 1 contributing through its forward window) equals the full-ring result there."""
+    from paper_2603_25832_b200 import _lib
+    from paper_2603_25832_b200.collision import build_cell_index, gather_scores_sorted
+    from paper_2603_25832_b200.pic import Grid
+
+    rng = np.random.default_rng(5)
+    n, M, L, S = 40000, 32, 8.0, 8
+    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    x[x >= L] = 0.0
+    v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
+    s = (rng.normal(size=(n, 3)) * 2).astype(np.float32).astype(np.float64)
+    p = ens(x, v, np.full(n, L / n))
+    grid = Grid(M, L / M)
+    ci = build_cell_index(p, grid, S=S)
+    gather_scores_sorted(ci, s)
+    full = _landau_sorted_env(p, grid, ci, {})
+    cs = ci.cell_start.cpu().numpy()
+    for c_lo, c_hi in ((0, 8), (5, 20), (24, 32), (1, 31)):
+        U = torch.zeros(3, n, dtype=torch.float32, device="cuda")
+        buf, nb = _lib.scratch("landau_t", _lib.query("spic_landau_scratch_bytes", n, M, 3, 0))
+        _lib.call("spic_landau_range", _lib.ptr(ci.xv), _lib.ptr(ci.sw), n, 3,
+                  _lib.ptr(ci.cell_start), _lib.ptr(ci.sub_start), M, S, float(grid.eta), -3.0,
+                  float(p.uniform_w), 0, c_lo, c_hi, _lib.ptr(U), _lib.ptr(buf), nb,
+                  _lib.stream_handle())
+        torch.cuda.synchronize()
+        a, b = cs[c_lo], cs[c_hi]
+        check_field(U.double().cpu().numpy()[:, a:b], full[:, a:b], tol=1e-5)
