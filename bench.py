@@ -38,7 +38,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-FLOP_PER_PAIR = 38.0
+FLOP_PER_PAIR = 38.0        # ordered pair kernel, per ordered live pair
+FLOP_PER_UPAIR = 41.0       # antisymmetric kernel, per unordered live pair
+
+
+def pair_flops(live_ordered: float, n: int) -> float:
+    """Algorithmic FLOP of one pair-kernel launch. The default (antisymmetric) kernel evaluates
+    each unordered live pair once: 41 FLOP x (live - n) / 2 (live counts ordered pairs incl.
+    the n self pairs); SPIC_LANDAU_VARIANT=o/s selects the ordered kernel (38 per ordered pair)."""
+    if os.environ.get("SPIC_LANDAU_VARIANT"):
+        return FLOP_PER_PAIR * live_ordered
+    return FLOP_PER_UPAIR * max(live_ordered - n, 0.0) / 2.0
+
+
+PAIR_KERNEL = ("spic_landau (k_landau_x2, ordered pairs)" if os.environ.get("SPIC_LANDAU_VARIANT")
+               else "spic_landau (k_landau_sym, unordered pairs)")
 METRIC = "particle-steps/s (full VML step, SBTM)"
 
 WORKLOADS = {
@@ -441,7 +455,8 @@ def config1_microbench(torch, device, n: int = 131072, reps: int = 3) -> dict:
     en /= float(np.sum((L / n) * np.linalg.norm(vs, axis=1) * np.linalg.norm(Us, axis=1)))
     pairs = float(n) * n
     return {"n": n, "ms": ms, "pair_interactions_per_s": pairs / (ms * 1e-3),
-            "tflops": FLOP_PER_PAIR * pairs / (ms * 1e-3) / 1e12,
+            "tflops": pair_flops(pairs, n) / (ms * 1e-3) / 1e12,
+            "ordered_equivalent_tflops": FLOP_PER_PAIR * pairs / (ms * 1e-3) / 1e12,
             "momentum_rel": mom, "energy_rel": en}
 
 
@@ -614,7 +629,8 @@ def main():
                "d2h_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4 + dh.numel() * 8)}
         sim.check()
 
-    achieved = FLOP_PER_PAIR * live / (coll_avg_ms * 1e-3) / 1e12
+    flop_launch = pair_flops(live, n)
+    achieved = flop_launch / (coll_avg_ms * 1e-3) / 1e12
     silu_rf = None
     if wl["estimator"] == "sbtm" and wl.get("net") == "silu":
         silu_rf = silu_kernel_roofline(torch, device, sim, wl, args.workload)
@@ -645,10 +661,12 @@ def main():
         "pair_interactions_per_s": world * live / (coll_avg_ms * 1e-3),
         "live_pairs_per_step": live,
         "collision_ms": coll_avg_ms,
-        "roofline_pair": {"bound": "fp32", "kernel": "spic_landau (k_landau_x2)",
+        "roofline_pair": {"bound": "fp32", "kernel": PAIR_KERNEL,
                           "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                           "frac": achieved / peak, "traffic": traffic,
-                          "flop_per_launch": FLOP_PER_PAIR * live, "launch_ms": coll_avg_ms,
+                          "ordered_equivalent_frac": FLOP_PER_PAIR * live / (coll_avg_ms * 1e-3)
+                          / 1e12 / peak,
+                          "flop_per_launch": flop_launch, "launch_ms": coll_avg_ms,
                           "launches_per_step": 1,
                           "peak_source": "measured in-run: spic_fp32_probe (FFMA2 chains, "
                                          "592 CTAs)"},

@@ -468,7 +468,7 @@ extern "C" size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, in
   const int32_t ns = nsplit <= 0 ? auto_nsplit(n, M, dv) : nsplit;
   size_t b = sizeof(int32_t) * (size_t)(M + 1 + 31);
   if (ns > 1) b += sizeof(float) * (size_t)ns * dv * n + 256;
-  if (dv == 3 && M >= 3 && landau_variant() == 0)
+  if (dv == 3 && landau_variant() == 0)
     b = std::max(b, spic_landau_sym_scratch_bytes(n, M, nsplit));
   return b;
 }
@@ -498,7 +498,8 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   if (scratch_bytes < spic_landau_scratch_bytes(n, M, dv, nsplit)) return SPIC_ERR_SCRATCH;
   if (n == 0) return SPIC_OK;
   const char var = landau_variant();
-  if (dv == 3 && M >= 3 && gamma == -3.0 && uniform_w > 0.f && var == 0)
+  if (dv == 3 && gamma == -3.0 && uniform_w > 0.f && var == 0 &&
+      (M >= 3 || (c_lo == 0 && c_hi == M)))
     return spic_landau_sym_run(xv, sw, n, cell_start, sub_start, M, S, eta, uniform_w, nsplit,
                                c_lo, c_hi, U_sorted, scratch, scratch_bytes, stream);
   if (nsplit <= 0) nsplit = auto_nsplit(n, M, dv);

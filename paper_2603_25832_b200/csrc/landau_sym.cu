@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(1024) k_sym_tiles(
       const bool halo = !(c >= c_lo && c < c_hi);
       const int cn = (c + 1) % M;
       int len2;
-      if (S > 1 && sub_start) {
+      if (M <= 2) {  // deduplicated stencil (per-pair minimum image): cell 0 pairs with cell 1
+        len2 = (M == 2 && c == 0) ? cell_start[2] - cell_start[1] : 0;
+      } else if (S > 1 && sub_start) {
         const int32_t* ss = sub_start + (size_t)c * S;
         int b = 0;  // sub-cell of the tile's last record
         for (int k = 1; k < S; ++k)
@@ -212,7 +214,7 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 // (even, odd) pairs; j records broadcast from shared memory (one-sided stages) or read in a
 // per-lane XOR order inside groups of 8 (two-sided stages, so the warp reduce-scatter of the
 // j-side needs no selects: lane l holds record (k ^ m_l), m_l = (l >> 2) & 7).
-template <int NT>
+template <int NT, bool MINIMG>
 __global__ void __launch_bounds__(NT, 2048 / NT / 4)
     k_landau_sym(const float4* __restrict__ xv, const float4* __restrict__ sw,
                  const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 4)
   }
   __syncthreads();
   const f2 W1c = mk2(wie, wie), nW2 = mk2(-wie2, -wie2);
+  const f2 invL2 = mk2(1.0f / L, 1.0f / L), negL2 = mk2(-L, -L);
   int lo = 0, hi = M;  // cell of this tile
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 4)
     const int cn = c + 1 == M ? 0 : c + 1;
     const int k = win.nseg;
     win.start[k] = cell_start[cn]; win.len[k] = m.len2;
-    win.shift[k] = c + 1 == M ? L : 0.f; win.two[k] = true;
+    win.shift[k] = (c + 1 == M && !MINIMG) ? L : 0.f; win.two[k] = true;
     win.wofs[k] = max(m.len1, 0);
     win.nseg = k + 1;
   } else {
@@ -289,7 +292,10 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 4)
   f2 X[RP], V0[RP], V1[RP], V2[RP], S0[RP], S1[RP], S2[RP], A0[RP], A1[RP], A2[RP];
 #pragma unroll
   for (int r = 0; r < RP; ++r) {
-    float4 Ae = make_float4(1e30f, 0.f, 0.f, 0.f), Be = make_float4(0.f, 0.f, 0.f, 0.f);
+    // padding targets: x = NaN -> max(NaN, 0) = 0 weight (also under the minimum image,
+    // which would fold a merely distant x back into the box), so they add nothing to the
+    // j-side sums
+    float4 Ae = make_float4(__int_as_float(0x7fffffff), 0.f, 0.f, 0.f), Be = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 Ao = Ae, Bo = Be;
     const int pe = t0 + threadIdx.x + (2 * r) * NT;
     const int po = pe + NT;
@@ -303,9 +309,9 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 4)
   auto issue = [&](int q) {
     const SymTileDesc d = sym_window_tile(win, jlo, jhi, q);
     const int st = q % kSymStages;
-    // padding records up to the next group of 8: x far away -> psi = 0
+    // padding records up to the next group of 8: x = NaN -> zero weight (see the targets)
     const int ru = min(kSymTJ, (d.cnt + 7) & ~7);
-    for (int j = d.cnt; j < ru; ++j) s_rec[st][0][j].x = 1e30f;
+    for (int j = d.cnt; j < ru; ++j) s_rec[st][0][j].x = __int_as_float(0x7fffffff);
     mbar_expect_tx(&s_bar[st], (uint32_t)(2 * d.cnt * sizeof(float4)));
     bulk_g2s(&s_rec[st][0][0], xv + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
     bulk_g2s(&s_rec[st][1][0], sw + d.pos, d.cnt * sizeof(float4), &s_bar[st]);
@@ -339,7 +345,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 4)
         const f2 sj0 = mk2(B.x, B.x), sj1 = mk2(B.y, B.y), sj2 = mk2(B.z, B.z);
 #pragma unroll
         for (int r = 0; r < RP; ++r) {
-          const f2 dx = sub2(XA[r], xj);
+          f2 dx = sub2(XA[r], xj);
+          if (MINIMG) dx = fma2(rint2(mul2(dx, invL2)), negL2, dx);
           float ce_, co_;
           un2(fma2(abs2(dx), nW2, W1c), ce_, co_);
           ce_ = fmaxf(ce_, 0.f);
@@ -374,7 +381,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 4)
           f2 J0, J1, J2;
 #pragma unroll
           for (int r = 0; r < RP; ++r) {
-            const f2 dx = sub2(XA[r], xj);
+            f2 dx = sub2(XA[r], xj);
+          if (MINIMG) dx = fma2(rint2(mul2(dx, invL2)), negL2, dx);
             float ce_, co_;
             un2(fma2(abs2(dx), nW2, W1c), ce_, co_);
             ce_ = fmaxf(ce_, 0.f);
@@ -567,12 +575,12 @@ static SymScratch sym_layout(void* base, int64_t n, int M, int nsplit, int TI) {
 
 // nsplit for the symmetric kernel: whole waves of (CTAs per SM) x SMs
 int spic_landau_sym_nsplit(int64_t n, int32_t M) {
-  const int NT = sym_nt();
+  const int NT = M <= 2 ? 128 : sym_nt();
   return pair_nsplit_slots(n, M, NT * 2 * kSymRP, (2048 / NT / 4) * kNumSMs);
 }
 
 size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit) {
-  const int NT = sym_nt();
+  const int NT = M <= 2 ? 128 : sym_nt();
   if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
   return sym_layout(nullptr, n, M, nsplit, NT * 2 * kSymRP).bytes + 256;
 }
@@ -581,7 +589,7 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
                         const int32_t* sub_start, int32_t M, int32_t S, double eta,
                         float uniform_w, int32_t nsplit, int32_t c_lo, int32_t c_hi,
                         float* U_sorted, void* scratch, size_t scratch_bytes, void* stream) {
-  const int NT = sym_nt();
+  const int NT = M <= 2 ? 128 : sym_nt();
   const int TI = NT * 2 * kSymRP;
   if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
   uintptr_t b = ((uintptr_t)scratch + 255) & ~(uintptr_t)255;
@@ -590,7 +598,7 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
   cudaStream_t st = (cudaStream_t)stream;
   const double L = (double)M * eta;
   const float wie = (float)((double)uniform_w / eta), wie2 = (float)((double)uniform_w / (eta * eta));
-  k_sym_tiles<<<1, 1024, 0, st>>>(cell_start, S > 1 ? sub_start : nullptr, M, S, TI, c_lo, c_hi,
+  k_sym_tiles<<<1, 1024, 0, st>>>(cell_start, (S > 1 && M >= 3) ? sub_start : nullptr, M, S, TI, c_lo, c_hi,
                                   s.cap, s.tile_start, s.meta, s.off, s.flag);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
@@ -599,20 +607,26 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
   dim3 grid((unsigned)(n / TI + ncells + 1), (unsigned)nsplit);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_landau_sym<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_landau_sym<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sym_smem_bytes(128));
-    cudaFuncSetAttribute(k_landau_sym<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_landau_sym<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sym_smem_bytes(256));
+    cudaFuncSetAttribute(k_landau_sym<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sym_smem_bytes(128));
     attr_set = true;
   }
-  if (NT == 256)
-    k_landau_sym<256><<<grid, 256, sym_smem_bytes(256), st>>>(
-        (const float4*)xv, (const float4*)sw, cell_start, S > 1 ? sub_start : nullptr,
-        s.tile_start, s.meta, s.off, s.flag, M, S, (float)L, wie, wie2, nsplit, s.Upart, s.Jslot, n);
+  const int32_t* ssp = (S > 1 && M >= 3) ? sub_start : nullptr;
+#define SPIC_SYM(NT_, MI_)                                                                        \
+  k_landau_sym<NT_, MI_><<<grid, NT_, sym_smem_bytes(NT_), st>>>(                                 \
+      (const float4*)xv, (const float4*)sw, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag, \
+      M, S, (float)L, wie, wie2, nsplit, s.Upart, s.Jslot, n)
+  if (M <= 2)
+    SPIC_SYM(128, true);
+  else if (NT == 256)
+    SPIC_SYM(256, false);
   else
-    k_landau_sym<128><<<grid, 128, sym_smem_bytes(128), st>>>(
-        (const float4*)xv, (const float4*)sw, cell_start, S > 1 ? sub_start : nullptr,
-        s.tile_start, s.meta, s.off, s.flag, M, S, (float)L, wie, wie2, nsplit, s.Upart, s.Jslot, n);
+    SPIC_SYM(128, false);
+#undef SPIC_SYM
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);

@@ -692,7 +692,7 @@ def _landau_sorted_env(p, grid, ci, env):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("case", ["config0", "M3_ragged", "clustered", "tiny_cells"])
+@pytest.mark.parametrize("case", ["config0", "M3_ragged", "clustered", "tiny_cells", "M1", "M2"])
 def test_antisymmetric_pair_path_matches_ordered_and_oracle(spic, case):
     """The unordered-pair kernel (default for dv = 3, gamma = -3, uniform w, M >= 3) against
     the ordered kernel (SPIC_LANDAU_VARIANT=o) and the float64 oracle; its ordered fallback
@@ -700,7 +700,8 @@ def test_antisymmetric_pair_path_matches_ordered_and_oracle(spic, case):
     from paper_2603_25832_b200.collision import build_cell_index, gather_scores_sorted
     from paper_2603_25832_b200.pic import Grid
 
-    rng = np.random.default_rng({"config0": 1, "M3_ragged": 2, "clustered": 3, "tiny_cells": 4}[case])
+    rng = np.random.default_rng({"config0": 1, "M3_ragged": 2, "clustered": 3, "tiny_cells": 4,
+                                 "M1": 5, "M2": 6}[case])
     if case == "config0":
         n, M, L, S = 65536, 64, 4 * math.pi, 16
         x = rng.uniform(0, L, n)
@@ -711,8 +712,11 @@ def test_antisymmetric_pair_path_matches_ordered_and_oracle(spic, case):
         n, M, L, S = 20000, 16, 8.0, 8
         x = np.concatenate([rng.uniform(2.0, 2.5, 12000), rng.uniform(0, L, 7990),
                             np.full(10, 4.0 - 1e-6)])
-    else:  # fewer particles than cells
+    elif case == "tiny_cells":  # fewer particles than cells
         n, M, L, S = 100, 64, 2 * math.pi, 1
+        x = rng.uniform(0, L, n)
+    else:  # M <= 2: deduplicated stencil, per-pair minimum image across the periodic ends
+        n, M, L, S = (5000, 1, 2.0, 8) if case == "M1" else (6001, 2, 2.0, 4)
         x = rng.uniform(0, L, n)
     x = x.astype(np.float32).astype(np.float64)
     x[x >= L] = 0.0
