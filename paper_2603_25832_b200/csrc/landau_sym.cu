@@ -34,7 +34,6 @@ namespace spic {
 
 constexpr int kSymTJ = 256;     // records per stage
 constexpr int kSymStages = 3;
-constexpr int kSymRP = 2;       // packed target pairs per thread (4 targets)
 
 struct SymMeta {
   int len1;  // own-cell forward length ce - t1; -1 marks a halo tile (seg2 only)
@@ -214,15 +213,14 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 // (even, odd) pairs; j records broadcast from shared memory (one-sided stages) or read in a
 // per-lane XOR order inside groups of 8 (two-sided stages, so the warp reduce-scatter of the
 // j-side needs no selects: lane l holds record (k ^ m_l), m_l = (l >> 2) & 7).
-template <int NT, bool MINIMG>
-__global__ void __launch_bounds__(NT, 2048 / NT / 4)
+template <int NT, int RP, int MINB, bool MINIMG>
+__global__ void __launch_bounds__(NT, MINB)
     k_landau_sym(const float4* __restrict__ xv, const float4* __restrict__ sw,
                  const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
                  const int32_t* __restrict__ tile_start, const SymMeta* __restrict__ meta,
                  const int64_t* __restrict__ off, const int32_t* __restrict__ symflag, int M,
                  int S, float L, float wie, float wie2, int nsplit, float* __restrict__ Upart,
                  float* __restrict__ Jslot, int64_t n) {
-  constexpr int RP = kSymRP;
   constexpr int TI = NT * 2 * RP;
   constexpr int NW = NT / 32;
   // dynamic shared memory (128-aligned by hand): stages of [xv records | sw records] (the sw
@@ -525,9 +523,18 @@ constexpr size_t sym_smem_bytes(int NT) {
          sizeof(uint64_t) * kSymStages;
 }
 
-int sym_nt() {
-  const char* e = getenv("SPIC_SYM_NT");
-  return (e && atoi(e) == 256) ? 256 : 128;
+// kernel configuration: threads per CTA, packed target pairs per thread, resident CTAs per SM
+struct SymCfg {
+  int nt, rp, minb;
+  int ti() const { return nt * 2 * rp; }
+};
+constexpr SymCfg kSymCfgs[] = {{128, 2, 4}, {128, 2, 3}, {128, 3, 3}, {256, 2, 2}, {128, 3, 2}};
+
+SymCfg sym_cfg(int M) {
+  if (M <= 2) return kSymCfgs[0];
+  const char* e = getenv("SPIC_SYM_CFG");
+  const int k = e ? atoi(e) : 0;
+  return kSymCfgs[(k >= 0 && k < 5) ? k : 0];
 }
 
 }  // namespace
@@ -575,22 +582,36 @@ static SymScratch sym_layout(void* base, int64_t n, int M, int nsplit, int TI) {
 
 // nsplit for the symmetric kernel: whole waves of (CTAs per SM) x SMs
 int spic_landau_sym_nsplit(int64_t n, int32_t M) {
-  const int NT = M <= 2 ? 128 : sym_nt();
-  return pair_nsplit_slots(n, M, NT * 2 * kSymRP, (2048 / NT / 4) * kNumSMs);
+  const SymCfg c = sym_cfg(M);
+  return pair_nsplit_slots(n, M, c.ti(), c.minb * kNumSMs);
 }
 
 size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit) {
-  const int NT = M <= 2 ? 128 : sym_nt();
   if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
-  return sym_layout(nullptr, n, M, nsplit, NT * 2 * kSymRP).bytes + 256;
+  return sym_layout(nullptr, n, M, nsplit, sym_cfg(M).ti()).bytes + 256;
+}
+
+template <int NT, int RP, int MINB, bool MINIMG>
+static void launch_sym(dim3 grid, cudaStream_t st, const float* xv, const float* sw,
+                       const int32_t* cell_start, const int32_t* ssp, const SymScratch& s, int M,
+                       int S, float L, float wie, float wie2, int nsplit, int64_t n) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_landau_sym<NT, RP, MINB, MINIMG>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem_bytes(NT));
+    attr = true;
+  }
+  k_landau_sym<NT, RP, MINB, MINIMG><<<grid, NT, sym_smem_bytes(NT), st>>>(
+      (const float4*)xv, (const float4*)sw, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag,
+      M, S, L, wie, wie2, nsplit, s.Upart, s.Jslot, n);
 }
 
 int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32_t* cell_start,
                         const int32_t* sub_start, int32_t M, int32_t S, double eta,
                         float uniform_w, int32_t nsplit, int32_t c_lo, int32_t c_hi,
                         float* U_sorted, void* scratch, size_t scratch_bytes, void* stream) {
-  const int NT = M <= 2 ? 128 : sym_nt();
-  const int TI = NT * 2 * kSymRP;
+  const SymCfg cfg = sym_cfg(M);
+  const int TI = cfg.ti();
   if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
   uintptr_t b = ((uintptr_t)scratch + 255) & ~(uintptr_t)255;
   SymScratch s = sym_layout((void*)b, n, M, nsplit, TI);
@@ -605,28 +626,20 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
   const bool partial = (c_hi - c_lo) < M;
   const int64_t ncells = (c_hi - c_lo) + (partial ? 1 : 0);
   dim3 grid((unsigned)(n / TI + ncells + 1), (unsigned)nsplit);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_landau_sym<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sym_smem_bytes(128));
-    cudaFuncSetAttribute(k_landau_sym<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sym_smem_bytes(256));
-    cudaFuncSetAttribute(k_landau_sym<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sym_smem_bytes(128));
-    attr_set = true;
-  }
   const int32_t* ssp = (S > 1 && M >= 3) ? sub_start : nullptr;
-#define SPIC_SYM(NT_, MI_)                                                                        \
-  k_landau_sym<NT_, MI_><<<grid, NT_, sym_smem_bytes(NT_), st>>>(                                 \
-      (const float4*)xv, (const float4*)sw, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag, \
-      M, S, (float)L, wie, wie2, nsplit, s.Upart, s.Jslot, n)
+  const float Lf = (float)L;
   if (M <= 2)
-    SPIC_SYM(128, true);
-  else if (NT == 256)
-    SPIC_SYM(256, false);
+    launch_sym<128, 2, 4, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+  else if (cfg.nt == 256)
+    launch_sym<256, 2, 2, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+  else if (cfg.rp == 3 && cfg.minb == 3)
+    launch_sym<128, 3, 3, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+  else if (cfg.rp == 3)
+    launch_sym<128, 3, 2, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+  else if (cfg.minb == 3)
+    launch_sym<128, 2, 3, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
   else
-    SPIC_SYM(128, false);
-#undef SPIC_SYM
+    launch_sym<128, 2, 4, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
