@@ -65,9 +65,19 @@ __global__ void k_bin_count(const float* __restrict__ x, int64_t n, double eta, 
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * T;
   const int64_t end = min((int64_t)n, base + T);
-  for (int64_t i = base + threadIdx.x; i < end; i += blockDim.x) {
-    CellKey ck = cell_key(x[i], eta, M, S);
-    atomicAdd(&hist[ck.cell * S + ck.sub], 1);
+  for (int64_t i0 = base + threadIdx.x; i0 < end; i0 += 8 * (int64_t)blockDim.x) {
+    float xs[8];  // loads of eight strides issued before their keys
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + u * (int64_t)blockDim.x;
+      xs[u] = i < end ? x[i] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u * (int64_t)blockDim.x < end) {
+        CellKey ck = cell_key(xs[u], eta, M, S);
+        atomicAdd(&hist[ck.cell * S + ck.sub], 1);
+      }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < K; k += blockDim.x)
@@ -176,12 +186,23 @@ __global__ void __launch_bounds__(256) k_bin_scatter(
   const int T = W * 32 * G;
   const int64_t wbase = (int64_t)blockIdx.x * T + (int64_t)wid * 32 * G;
   int* my = hist + wid * K;
-  // pass 1: per-warp histogram of its sub-chunk
-  for (int g = 0; g < G; ++g) {
-    int64_t i = wbase + g * 32 + lane;
-    if (i < n) {
-      CellKey ck = cell_key(x[i], eta, M, S);
-      atomicAdd(&my[ck.cell * S + ck.sub], 1);
+  // pass 1: per-warp histogram of its sub-chunk (positions loaded kPF groups ahead: the
+  // sweep is latency-bound, one warp per key-histogram slice)
+  constexpr int kPF = 8;
+  for (int g0 = 0; g0 < G; g0 += kPF) {
+    float xs[kPF];
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+      const int64_t i = wbase + (int64_t)(g0 + u) * 32 + lane;
+      xs[u] = (g0 + u < G && i < n) ? x[i] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+      const int64_t i = wbase + (int64_t)(g0 + u) * 32 + lane;
+      if (g0 + u < G && i < n) {
+        CellKey ck = cell_key(xs[u], eta, M, S);
+        atomicAdd(&my[ck.cell * S + ck.sub], 1);
+      }
     }
   }
   __syncthreads();
@@ -195,34 +216,48 @@ __global__ void __launch_bounds__(256) k_bin_scatter(
     }
   }
   __syncthreads();
-  // pass 3: replay in pid order, rank within 32-groups by key
-  for (int g = 0; g < G; ++g) {
-    int64_t i = wbase + g * 32 + lane;
-    bool valid = i < n;
-    unsigned active = __ballot_sync(0xffffffffu, valid);
-    if (!active) break;
-    if (valid) {
-      float xi = x[i];
-      CellKey ck = cell_key(xi, eta, M, S);
-      int key = ck.cell * S + ck.sub;
-      unsigned peers = __match_any_sync(active, key);
-      int rank = __popc(peers & lanemask_lt());
-      int basepos = my[key];
-      __syncwarp(active);
-      if (rank == 0) my[key] = basepos + __popc(peers);
-      int pos = basepos + rank;
-      if (perm) perm[pos] = (int32_t)i;
-      if (xv) {
-        float4 r;
-        r.x = ck.wrapped ? (float)((double)xi - L) : xi;
-        r.y = v[i];
-        r.z = v[ldv + i];
-        r.w = dv > 2 ? v[2 * ldv + i] : 0.f;
-        xv[pos] = r;
-      }
-      if (sw) sw[pos] = make_float4(0.f, 0.f, 0.f, w ? w[i] : 0.f);
+  // pass 3: replay in pid order, rank within 32-groups by key (record fields loaded kPF
+  // groups ahead; the key ranks are the only serial dependency)
+  for (int g0 = 0; g0 < G; g0 += kPF) {
+    float xs[kPF], v0[kPF], v1[kPF], v2[kPF], ws[kPF];
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+      const int64_t i = wbase + (int64_t)(g0 + u) * 32 + lane;
+      const bool ok = g0 + u < G && i < n;
+      xs[u] = ok ? x[i] : 0.f;
+      v0[u] = (ok && xv) ? v[i] : 0.f;
+      v1[u] = (ok && xv) ? v[ldv + i] : 0.f;
+      v2[u] = (ok && xv && dv > 2) ? v[2 * ldv + i] : 0.f;
+      ws[u] = (ok && w) ? w[i] : 0.f;
     }
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+      const int64_t i = wbase + (int64_t)(g0 + u) * 32 + lane;
+      const bool valid = g0 + u < G && i < n;
+      const unsigned active = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const float xi = xs[u];
+        CellKey ck = cell_key(xi, eta, M, S);
+        int key = ck.cell * S + ck.sub;
+        unsigned peers = __match_any_sync(active, key);
+        int rank = __popc(peers & lanemask_lt());
+        int basepos = my[key];
+        __syncwarp(active);
+        if (rank == 0) my[key] = basepos + __popc(peers);
+        int pos = basepos + rank;
+        if (perm) perm[pos] = (int32_t)i;
+        if (xv) {
+          float4 r;
+          r.x = ck.wrapped ? (float)((double)xi - L) : xi;
+          r.y = v0[u];
+          r.z = v1[u];
+          r.w = v2[u];
+          xv[pos] = r;
+        }
+        if (sw) sw[pos] = make_float4(0.f, 0.f, 0.f, ws[u]);
+      }
+      __syncwarp();
+    }
   }
 }
 
