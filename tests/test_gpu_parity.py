@@ -773,3 +773,60 @@ def test_antisymmetric_pair_path_partial_cell_range(spic):
         torch.cuda.synchronize()
         a, b = cs[c_lo], cs[c_hi]
         check_field(U.double().cpu().numpy()[:, a:b], full[:, a:b], tol=1e-5)
+
+
+@pytest.mark.parametrize("case", ["config0_silverman", "config0_fixed", "M3_ragged", "M1", "M2"])
+def test_symmetric_blob_path_matches_ordered_and_oracle(spic, case):
+    """The unordered-pair blob sums (default for dv = 3, uniform w) against the ordered sweep
+    (SPIC_BLOB_VARIANT=o), the float64 oracle and the forced ordered fallback; Silverman
+    bandwidths differ per cell, so pairs across a cell border take two exponentials."""
+    import os
+
+    from paper_2603_25832_b200.collision import build_cell_index
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.score import blob_score
+
+    rng = np.random.default_rng({"config0_silverman": 1, "config0_fixed": 2, "M3_ragged": 3,
+                                 "M1": 4, "M2": 5}[case])
+    bw = None
+    if case.startswith("config0"):
+        n, M, L, S = 65536, 64, 4 * math.pi, 16
+        x = rng.uniform(0, L, n)
+        v = rng.normal(size=(n, 3)) * (1.0 + 0.5 * np.sin(x)[:, None])  # h varies per cell
+        bw = 0.3 if case == "config0_fixed" else None
+    elif case == "M3_ragged":
+        n, M, L, S = 3001, 3, 3.0, 4
+        x = np.concatenate([rng.uniform(0, 1, 1700), rng.uniform(1, 2, 300), rng.uniform(2, 3, 1001)])
+        v = rng.normal(size=(n, 3))
+    else:
+        n, M, L, S = (5000, 1, 2.0, 8) if case == "M1" else (6001, 2, 2.0, 4)
+        x = rng.uniform(0, L, n)
+        v = rng.normal(size=(n, 3))
+    x = x.astype(np.float32).astype(np.float64)
+    x[x >= L] = 0.0
+    v = v.astype(np.float32).astype(np.float64)
+    p = ens(x, v, np.full(n, L / n))
+    grid = Grid(M, L / M)
+    ci = build_cell_index(p, grid, S=S)
+
+    def run(env):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            return blob_score(p, ci, grid, bw).double().cpu().numpy()
+        finally:
+            for k, val in old.items():
+                if val is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = val
+
+    ref = O.blob_score(x, v, p.w.double().cpu().numpy(), grid.eta, M, bw)
+    s_sym = run({})
+    s_ord = run({"SPIC_BLOB_VARIANT": "o"})
+    s_fb = run({"SPIC_SYM_CAP_SLOTS": "0"})
+    assert np.array_equal(s_sym, run({}))
+    check_field(s_sym, ref, tol=2e-4)
+    check_field(s_ord, ref, tol=2e-4)
+    check_field(s_fb, ref, tol=2e-4)
+    check_field(s_sym, s_ord, tol=1e-4)
