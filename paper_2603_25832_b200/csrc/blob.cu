@@ -362,10 +362,29 @@ static int blob_nsplit(int64_t n, int M, int dv) {
 
 using namespace spic;
 
+// symmetric (unordered-pair) path, blob_sym.cu
+size_t spic_blob_sym_scratch_bytes(int64_t n, int32_t M);
+int spic_blob_sym_run(const float4* xv, float4* sw, const int32_t* perm, int64_t n,
+                      const int32_t* cell_start, const int32_t* sub_start, int32_t M, int32_t S,
+                      double eta, const float* h_cell, float h_fixed, float uniform_w,
+                      long long* bad_pid, int32_t* flags, void* scratch, size_t scratch_bytes,
+                      cudaStream_t st);
+
+// SPIC_BLOB_VARIANT=o selects the ordered sweep (A/B checks)
+static bool blob_ordered_forced() {
+  const char* e = getenv("SPIC_BLOB_VARIANT");
+  return e && e[0] == 'o';
+}
+
+static size_t blob_s1_bytes(int32_t M) { return (sizeof(double) * 3 * (size_t)M + 255) & ~(size_t)255; }
+
 extern "C" size_t spic_blob_scratch_bytes(int64_t n, int32_t M, int32_t dv) {
   int ns = blob_nsplit(n, M, dv);
-  return sizeof(float) * (size_t)ns * 4 * n + sizeof(double) * 3 * (size_t)M +
-         sizeof(int32_t) * (M + 1) + 1024;
+  size_t b = sizeof(float) * (size_t)ns * 4 * n + sizeof(double) * 3 * (size_t)M +
+             sizeof(int32_t) * (M + 1) + 1024;
+  if (dv == 3 && !blob_ordered_forced())
+    b = std::max(b, blob_s1_bytes(M) + spic_blob_sym_scratch_bytes(n, M) + 256);
+  return b;
 }
 
 extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_t n, int32_t dv,
@@ -380,9 +399,11 @@ extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_
   if (n == 0) return SPIC_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int ns = blob_nsplit(n, M, dv);
+  const bool symp = dv == 3 && uniform_w > 0.f && !blob_ordered_forced();
   float* part = (float*)scratch;
   uintptr_t pp = (uintptr_t)(part + (size_t)ns * 4 * n);
   pp = (pp + 255) & ~(uintptr_t)255;
+  if (symp) pp = ((uintptr_t)scratch + 255) & ~(uintptr_t)255;  // S1 first, then the sym region
   double* S1 = (double*)pp;
   int32_t* tile_start = (int32_t*)(S1 + 3 * (size_t)M);
   const float4* xv4 = (const float4*)xv;
@@ -392,6 +413,13 @@ extern "C" int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_
     k_blob_silverman<<<M, 256, 0, st>>>(xv4, cell_start, M, dv, S1, h_cell); spic::count_launch();
     SPIC_CHECK_LAUNCH();
     hc = h_cell;
+  }
+  if (symp) {
+    char* sr = (char*)S1 + blob_s1_bytes(M);
+    const size_t used = (size_t)(sr - (char*)scratch);
+    return spic_blob_sym_run(xv4, (float4*)sw, perm, n, cell_start, sub_start, M, S, eta, hc,
+                             (float)bandwidth, uniform_w, bad_pid, flags, sr,
+                             scratch_bytes > used ? scratch_bytes - used : 0, st);
   }
   const bool packed = dv == 3;
   const int TI = packed ? kLandauNT * 4 : kLandauTI;

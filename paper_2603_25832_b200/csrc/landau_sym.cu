@@ -24,21 +24,9 @@
 // seg2 reaches it). The slot count is data dependent (~ n * n_cell / TI); if it exceeds the
 // caller's scratch, the tile table clears a device flag and the same kernels run the ordered
 // (full-stencil, one-sided) enumeration instead — graph-safe, no host synchronisation.
-#include <algorithm>
-#include <cstdlib>
-
-#include "f32x2.cuh"
-#include "pairs.cuh"
+#include "sym.cuh"
 
 namespace spic {
-
-constexpr int kSymTJ = 256;     // records per stage
-constexpr int kSymStages = 3;
-
-struct SymMeta {
-  int len1;  // own-cell forward length ce - t1; -1 marks a halo tile (seg2 only)
-  int len2;  // next-cell prefix length
-};
 
 __device__ __forceinline__ bool sym_tile_cell(int c, int M, int c_lo, int c_hi, bool partial) {
   if (c >= c_lo && c < c_hi) return true;
@@ -152,63 +140,6 @@ __global__ void __launch_bounds__(1024) k_sym_tiles(
   }
 }
 
-// j-window tile with its kind: two-sided tiles also carry the slot offset of their first
-// record relative to off[tile]
-struct SymTileDesc {
-  int pos, cnt, wofs;
-  float shift;
-  bool two;
-};
-
-struct SymWindow {
-  int start[3], len[3], wofs[3];
-  float shift[3];
-  bool two[3];
-  int nseg;
-};
-
-__device__ __forceinline__ int sym_window_tiles(const SymWindow& w, int jlo, int jhi) {
-  int o = 0, nt = 0;
-  for (int s = 0; s < w.nseg; ++s) {
-    const int a = max(jlo, o), b = min(jhi, o + w.len[s]);
-    if (b > a) nt += (b - a + kSymTJ - 1) / kSymTJ;
-    o += w.len[s];
-  }
-  return nt;
-}
-
-__device__ __forceinline__ SymTileDesc sym_window_tile(const SymWindow& w, int jlo, int jhi,
-                                                       int q) {
-  int o = 0;
-  SymTileDesc d{0, 0, 0, 0.f, false};
-  for (int s = 0; s < w.nseg; ++s) {
-    const int a = max(jlo, o), b = min(jhi, o + w.len[s]);
-    if (b > a) {
-      const int nt = (b - a + kSymTJ - 1) / kSymTJ;
-      if (q < nt) {
-        const int lo = a + q * kSymTJ;
-        d.pos = w.start[s] + (lo - o);
-        d.cnt = min(kSymTJ, b - lo);
-        d.shift = w.shift[s];
-        d.two = w.two[s];
-        d.wofs = w.wofs[s] + (lo - o);
-        return d;
-      }
-      q -= nt;
-    }
-    o += w.len[s];
-  }
-  return d;
-}
-
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr));
-  return v;
-}
-
 // One CTA per (target tile, j-split). NT threads, 4 targets per thread as two packed
 // (even, odd) pairs; j records broadcast from shared memory (one-sided stages) or read in a
 // per-lane XOR order inside groups of 8 (two-sided stages, so the warp reduce-scatter of the
@@ -254,33 +185,9 @@ __global__ void __launch_bounds__(NT, MINB)
   const int t0 = cs + (tile - tile_start[c]) * TI;
   const int t1 = min(t0 + TI, ce);
   const bool sym = *symflag != 0;
-  SymWindow win;
-  win.nseg = 0;
-  int64_t slot0 = 0;
-  if (sym) {
-    const SymMeta m = meta[tile];
-    slot0 = off[tile];
-    if (m.len1 >= 0) {
-      win.start[0] = t0; win.len[0] = t1 - t0; win.shift[0] = 0.f; win.two[0] = false;
-      win.wofs[0] = 0;
-      win.start[1] = t1; win.len[1] = m.len1; win.shift[1] = 0.f; win.two[1] = true;
-      win.wofs[1] = 0;
-      win.nseg = 2;
-    }
-    const int cn = c + 1 == M ? 0 : c + 1;
-    const int k = win.nseg;
-    win.start[k] = cell_start[cn]; win.len[k] = m.len2;
-    win.shift[k] = (c + 1 == M && !MINIMG) ? L : 0.f; win.two[k] = true;
-    win.wofs[k] = max(m.len1, 0);
-    win.nseg = k + 1;
-  } else {
-    const Window w = build_window(cell_start, sub_start, M, S, c, t0, t1, L);
-    for (int s = 0; s < w.nseg; ++s) {
-      win.start[s] = w.start[s]; win.len[s] = w.len[s]; win.shift[s] = w.shift[s];
-      win.two[s] = false; win.wofs[s] = 0;
-    }
-    win.nseg = w.nseg;
-  }
+  const SymWindow win =
+      sym_build_window(sym, meta, cell_start, sub_start, M, S, c, tile, t0, t1, L, MINIMG);
+  const int64_t slot0 = sym ? off[tile] : 0;
   int wlen = 0;
   for (int s = 0; s < win.nseg; ++s) wlen += win.len[s];
   const int jlo = (int)(((long long)wlen * split) / nsplit);
@@ -410,29 +317,11 @@ __global__ void __launch_bounds__(NT, MINB)
           un2(J1, e, o); P1[k] = e + o;
           un2(J2, e, o); P2[k] = e + o;
         }
-        // warp reduce-scatter: after the xor-16/8/4 exchanges lane l holds the 8-lane sum of
-        // record jb + m_l; the xor-2/1 butterflies complete the 32-lane sum
+        float PP[3][8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          P0[k] += __shfl_xor_sync(0xffffffffu, P0[k + 4], 16);
-          P1[k] += __shfl_xor_sync(0xffffffffu, P1[k + 4], 16);
-          P2[k] += __shfl_xor_sync(0xffffffffu, P2[k + 4], 16);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          P0[k] += __shfl_xor_sync(0xffffffffu, P0[k + 2], 8);
-          P1[k] += __shfl_xor_sync(0xffffffffu, P1[k + 2], 8);
-          P2[k] += __shfl_xor_sync(0xffffffffu, P2[k + 2], 8);
-        }
-        P0[0] += __shfl_xor_sync(0xffffffffu, P0[1], 4);
-        P1[0] += __shfl_xor_sync(0xffffffffu, P1[1], 4);
-        P2[0] += __shfl_xor_sync(0xffffffffu, P2[1], 4);
-        P0[0] += __shfl_xor_sync(0xffffffffu, P0[0], 2);
-        P1[0] += __shfl_xor_sync(0xffffffffu, P1[0], 2);
-        P2[0] += __shfl_xor_sync(0xffffffffu, P2[0], 2);
-        P0[0] += __shfl_xor_sync(0xffffffffu, P0[0], 1);
-        P1[0] += __shfl_xor_sync(0xffffffffu, P1[0], 1);
-        P2[0] += __shfl_xor_sync(0xffffffffu, P2[0], 1);
+        for (int k = 0; k < 8; ++k) { PP[0][k] = P0[k]; PP[1][k] = P1[k]; PP[2][k] = P2[k]; }
+        sym_reduce_scatter8<3>(PP);
+        P0[0] = PP[0][0]; P1[0] = PP[1][0]; P2[0] = PP[2][0];
         const int cc = lane & 3;
         if (cc < 3) jp[(jb + ((lane >> 2) & 7)) * 3 + cc] = cc == 0 ? P0[0] : (cc == 1 ? P1[0] : P2[0]);
       }
@@ -484,30 +373,10 @@ __global__ void __launch_bounds__(256) k_sym_fold(
       const float* P = Upart + (size_t)s * 3 * n;
       u0 += P[p]; u1 += P[n + p]; u2 += P[2 * n + p];
     }
-    if (sym) {
-      int lo = 0, hi = M;  // cell of p: largest c with cell_start[c] <= p
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(cell_start + mid) <= p) lo = mid; else hi = mid;
-      }
-      const int c = lo;
-      const int cs = cell_start[c];
-      const int rel = (int)(p - cs);
-      const int tc = tile_start[c];
-      const int tp = tc + rel / TI;
-      for (int t = tc; t < tp; ++t) {
-        const int64_t sl = off[t] + (rel - (t - tc + 1) * TI);
+    if (sym)
+      sym_for_slots(p, cell_start, tile_start, meta, off, M, TI, [&](int64_t sl) {
         u0 += Jslot[sl * 3]; u1 += Jslot[sl * 3 + 1]; u2 += Jslot[sl * 3 + 2];
-      }
-      const int cm = c == 0 ? M - 1 : c - 1;
-      for (int t = tile_start[cm]; t < tile_start[cm + 1]; ++t) {
-        const SymMeta m = meta[t];
-        if (rel < m.len2) {
-          const int64_t sl = off[t] + max(m.len1, 0) + rel;
-          u0 += Jslot[sl * 3]; u1 += Jslot[sl * 3 + 1]; u2 += Jslot[sl * 3 + 2];
-        }
-      }
-    }
+      });
     U[p] = u0; U[n + p] = u1; U[2 * n + p] = u2;
   }
 }
@@ -538,47 +407,6 @@ SymCfg sym_cfg(int M) {
 }
 
 }  // namespace
-
-// Layout of the symmetric path's scratch (all offsets 256-aligned):
-//   tile_start i32[M+2] | meta SymMeta[Tmax] | off i64[Tmax+1] | flag i32 | Upart f32[nsplit][3][n]
-//   | Jslot f32[cap][3]
-struct SymScratch {
-  int32_t* tile_start;
-  SymMeta* meta;
-  int64_t* off;
-  int32_t* flag;
-  float* Upart;
-  float* Jslot;
-  int64_t cap;
-  size_t bytes;
-};
-
-static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
-
-static SymScratch sym_layout(void* base, int64_t n, int M, int nsplit, int TI) {
-  SymScratch s{};
-  const int64_t Tmax = n / TI + M + 2;
-  // slot estimate for a near-uniform ensemble: each tile's forward window ~ one cell plus a
-  // sub-cell; 1.3x headroom (an exceeding ensemble runs the ordered path, see k_sym_tiles)
-  const int64_t ncell = n / std::max(M, 1);
-  int64_t cap = (int64_t)(1.3 * (double)Tmax * (double)(ncell + 2 * TI)) + 4096;
-  if (const char* e = getenv("SPIC_SYM_CAP_SLOTS")) cap = atoll(e);  // tests: force the fallback
-  size_t o = 0;
-  auto take = [&](size_t b) {
-    size_t at = o;
-    o = align256(o + b);
-    return (char*)base + at;
-  };
-  s.tile_start = (int32_t*)take(sizeof(int32_t) * (M + 2));
-  s.meta = (SymMeta*)take(sizeof(SymMeta) * Tmax);
-  s.off = (int64_t*)take(sizeof(int64_t) * (Tmax + 1));
-  s.flag = (int32_t*)take(sizeof(int32_t) * 8);
-  s.Upart = (float*)take(sizeof(float) * (size_t)nsplit * 3 * n);
-  s.Jslot = (float*)take(sizeof(float) * (size_t)cap * 3);
-  s.cap = cap;
-  s.bytes = o;
-  return s;
-}
 
 // nsplit for the symmetric kernel: whole waves of (CTAs per SM) x SMs
 int spic_landau_sym_nsplit(int64_t n, int32_t M) {
