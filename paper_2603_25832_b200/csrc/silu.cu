@@ -43,7 +43,14 @@ __device__ long long g_silu_trace[64 * 16];
   do {                                                                                 \
     if (blockIdx.x == 0 && threadIdx.x == 0 && it < 64) g_silu_trace[it * 16 + (k)] = clock64(); \
   } while (0)
+#define SILU_TRACE_I(k)                                                                \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && lane == 0 && iit < 64) g_silu_trace[iit * 16 + (k)] = clock64(); \
+  } while (0)
 #else
+#define SILU_TRACE_I(k) \
+  do {                  \
+  } while (0)
 #define SILU_TRACE(k) \
   do {                \
   } while (0)
@@ -263,10 +270,12 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   // F3: reverse through layer 1 -> dW1 (input part), db1, for chunk cc whose G2 result is in
   // D2. The ISM runs it one chunk late, while the tensor cores compute the next chunk's G1
   // (re-reading that chunk's records, an L2 hit); MSE runs it in order from S.u.
+  int it = 0;  // chunk iteration of this CTA (trace stamps)
   auto layer1_reverse = [&](int ub) {
     umma::wait_mma(&S.bar[2], phase2);
     phase2 ^= 1;
     umma::fence_after();
+    SILU_TRACE(9);
     float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
     float vd[16], vf[16];
     umma::tmem_ld12(tl + cD2 + p0, vd);
@@ -292,15 +301,16 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 
   bool pending = false;  // the previous chunk's layer-1 reverse sweep is still to run (ISM)
   int ub = 0;            // S.u buffer of the current chunk
-  int it = 0;
   if (tid >= kNCW) {
     // issuer warp: every GEMM of the CTA in chunk order, as soon as its operands are ready.
     // (An MMA issue blocks while the tensor pipe's queue is full, so a compute warp that
     // issued would stall for most of the GEMM time.)
     bool fst = true;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    int iit = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++iit) {
       handoff_wait(6);  // X written (F1 of chunk c)
       umma::fence_after();
+      SILU_TRACE_I(10);
       if (lane == 0) {
         umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
                                                               false);  // W2 h1
@@ -310,9 +320,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         umma::commit(&S.bar[0]);
       }
       __syncwarp();
+      SILU_TRACE_I(11);
       if (ISM) {
         handoff_wait(7);  // Y written (F2b of chunk c)
         umma::fence_after();
+        SILU_TRACE_I(12);
         if (lane == 0) {
           // G3 first: the next chunk's layer-1 sweep waits for it (X, Y reuse)
           umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(tm + cD3, sYh, sYl, sXh,
@@ -330,6 +342,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           umma::commit(&S.bar[2]);
         }
         __syncwarp();
+        SILU_TRACE_I(13);
         fst = false;
       }
     }
@@ -338,11 +351,16 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     SILU_TRACE(0);
     // each warpgroup loads, reduces and scores its own 8 particles: only the GEMM issue points
     // need the whole CTA, everything else synchronises one warpgroup (named barrier)
-    if (ISM && !first) {  // the previous chunk's weight-gradient GEMMs still read X and Y
-      umma::wait_mma(&S.bar[1], phase3);
-      phase3 ^= 1;
-      umma::fence_after();
-    }
+    auto wait_g3 = [&]() {  // the previous chunk's weight-gradient GEMMs still read X and Y
+      if (ISM && !first) {
+        umma::wait_mma(&S.bar[1], phase3);
+        phase3 ^= 1;
+        umma::fence_after();
+      }
+    };
+    // MSE keeps its targets in the Y tile: wait before loading; the ISM loads its records and
+    // runs the layer-1 arithmetic while G3 drains, and waits only before the X stores
+    if (MODE != 1) wait_g3();
     if (wtid < kPPT) {
       const int pl = p0 + wtid;
       const int64_t p = c * kCP + pl;
@@ -369,13 +387,31 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     SILU_TRACE(1);
 
     // F1: layer 1 -> X rows p (h1) and 32 + p (d1 = silu'(a1)), column h
+    if (MODE == 1) {
+      float f1h[kPPT], f1d[kPPT];
 #pragma unroll
-    for (int i = 0; i < kPPT; ++i) {
-      const float4 u = S.u[ub][p0 + i];
-      const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
-      const float sg = sigmoid(a);
-      st_split(rb[i & 7] + i * 128, a * sg);
-      if (DIV) st_split(rb[i & 7] + kDivRows + i * 128, sg * fmaf(a, 1.f - sg, 1.f));
+      for (int i = 0; i < kPPT; ++i) {
+        const float4 u = S.u[ub][p0 + i];
+        const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
+        const float sg = sigmoid(a);
+        f1h[i] = a * sg;
+        f1d[i] = sg * fmaf(a, 1.f - sg, 1.f);
+      }
+      wait_g3();
+#pragma unroll
+      for (int i = 0; i < kPPT; ++i) {
+        st_split(rb[i & 7] + i * 128, f1h[i]);
+        st_split(rb[i & 7] + kDivRows + i * 128, f1d[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kPPT; ++i) {
+        const float4 u = S.u[ub][p0 + i];
+        const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
+        const float sg = sigmoid(a);
+        st_split(rb[i & 7] + i * 128, a * sg);
+        if (DIV) st_split(rb[i & 7] + kDivRows + i * 128, sg * fmaf(a, 1.f - sg, 1.f));
+      }
     }
     fence_proxy_async();
     umma::fence_before();

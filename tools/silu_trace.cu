@@ -57,5 +57,20 @@ int main() {
   for (int k = 0; k <= 8; ++k)
     printf("%-20s %8.0f cycles %5.1f%%\n", names[k], sum[k] / cnt, 100 * sum[k] / tot);
   printf("%-20s %8.0f cycles (%d chunks)\n", "chunk total", tot / cnt, cnt);
+  // absolute offsets from the chunk's F1 hand-off (stamp 2): issuer and G2-arrival stamps
+  double a9 = 0, a10 = 0, a11 = 0, a4 = 0, a12 = 0, a13 = 0, a7 = 0;
+  for (int it = 4; it < 4 + cnt; ++it) {
+    const double t2 = (double)h[it * 16 + 2];
+    a10 += h[it * 16 + 10] - t2;   // issuer sees X ready
+    a11 += h[it * 16 + 11] - t2;   // G1 issued
+    a9 += h[(it + 1) * 16 + 9] - (double)h[(it + 1) * 16 + 2];  // next chunk: F3 got G2(prev)
+    a4 += h[it * 16 + 4] - t2;     // G1 complete seen by compute
+    a7 += h[it * 16 + 7] - t2;     // F2b done
+    a12 += h[it * 16 + 12] - t2;   // issuer sees Y ready
+    a13 += h[it * 16 + 13] - t2;   // G3 + G2 issued
+  }
+  printf("from F1 hand-off: issuer X-ready %+.0f, G1 issued %+.0f, G1 done %+.0f, F2b done %+.0f,\n"
+         "  issuer Y-ready %+.0f, G3+G2 issued %+.0f; next chunk's F3 got G2 %+.0f after its F1 hand-off\n",
+         a10 / cnt, a11 / cnt, a4 / cnt, a7 / cnt, a12 / cnt, a13 / cnt, a9 / cnt);
   return 0;
 }
