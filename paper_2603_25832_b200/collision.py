@@ -78,7 +78,7 @@ def landau_sorted(ci: CellIndex, particles: ParticleEnsemble, grid: Grid, gamma:
                   U_sorted: torch.Tensor, nsplit: int = 0) -> torch.Tensor:
     """U in sorted order (dv, n) from the records (scores already in ci.sw)."""
     n, dv = particles.n, particles.dv
-    buf, nb = _lib.scratch("landau", _lib.query("spic_landau_scratch_bytes", n, grid.M, dv, nsplit))
+    buf, nb = _lib.scratch("pairs", _lib.query("spic_landau_scratch_bytes", n, grid.M, dv, nsplit))
     _lib.call("spic_landau", _lib.ptr(ci.xv), _lib.ptr(ci.sw), n, dv, _lib.ptr(ci.cell_start),
               _lib.ptr(ci.sub_start) if ci.S > 1 else None, grid.M, ci.S, float(grid.eta),
               float(gamma), float(particles.uniform_w), int(nsplit), _lib.ptr(U_sorted),

@@ -312,8 +312,17 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       umma::fence_after();
       SILU_TRACE_I(10);
       if (lane == 0) {
-        umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
-                                                              false);  // W2 h1
+        if constexpr (MODE == 0) {
+          // the forward double-buffers X (odd chunks in the unused B tiles) and D1 (odd chunks
+          // in the D2 columns)
+          const bool odd = iit & 1;
+          const uint32_t xb = odd ? sBh : sXh;
+          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + (odd ? cD2 : cD1), sW2h,
+                                                                sW2l, xb, xb + kXTile, false);
+        } else {
+          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
+                                                                false);  // W2 h1
+        }
         if (DIV)
           umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(
               tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);  // B d1
@@ -345,6 +354,78 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         SILU_TRACE_I(13);
         fst = false;
       }
+    }
+  } else if constexpr (MODE == 0) {
+    // Forward only: layer-1 sweep of chunk i (into X buffer i & 1) runs while the tensor cores
+    // compute G1 of chunk i - 1 (from the other buffer, into the other accumulator), whose
+    // scores follow. Nothing else shares the B tiles or the D2 columns in this mode.
+    const uint32_t xdelta = sBh - sXh;
+    int64_t cprev = -1;
+    for (int64_t c = blockIdx.x;; c += gridDim.x, ++it) {
+      const bool has = c < nchunks;
+      const int buf = it & 1;
+      if (has) {
+        if (wtid < kPPT) {
+          const int pl = p0 + wtid;
+          const int64_t p = c * kCP + pl;
+          float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (p < n) {
+            const float4 A = xv[p];
+            const float x = A.x < 0.f ? A.x + L : A.x;  // % M quirk records carry x - L
+            u = make_float4(x * x_scale, A.y, A.z, A.w);
+          }
+          S.u[buf][pl] = u;
+        }
+        wg_sync(wg);
+#pragma unroll
+        for (int i = 0; i < kPPT; ++i) {
+          const float4 u = S.u[buf][p0 + i];
+          const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
+          st_split(rb[i & 7] + (buf ? xdelta : 0u) + i * 128, a * sigmoid(a));
+        }
+        fence_proxy_async();
+        umma::fence_before();
+        handoff_arrive(6);
+      }
+      if (cprev >= 0) {
+        umma::wait_mma(&S.bar[0], phase);
+        phase ^= 1;
+        umma::fence_after();
+        {
+          float va[16];
+          umma::tmem_ld12(tl + (buf ? cD1 : cD2) + p0, va);  // chunk cprev used buffer buf ^ 1
+          float v32[32], v16[16];
+#pragma unroll
+          for (int pp = 0; pp < kPPT; ++pp) {
+            const float a2 = va[pp] + bb2;
+            const float h2 = a2 * sigmoid(a2);
+            float* dst = pp < 8 ? &v32[4 * pp] : &v16[4 * (pp - 8)];
+            dst[0] = w3[0] * h2;
+            dst[1] = w3[1] * h2;
+            dst[2] = w3[2] * h2;
+            dst[3] = 0.f;
+          }
+          const float r32 = transpose_reduce32(v32, lane);
+          const float r16 = transpose_reduce16(v16, lane);
+          red[quarter][4 * p0 + lane] = r32;
+          if (lane < 16) red[quarter][4 * (p0 + 8) + lane] = r16;
+        }
+        wg_sync(wg);
+        if (wtid < kPPT) {
+          const int p = p0 + wtid;
+          float sc[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            sc[k] = b3[k] + ((red[0][4 * p + k] + red[1][4 * p + k]) +
+                             (red[2][4 * p + k] + red[3][4 * p + k]));
+          const int64_t q = cprev * kCP + p;
+          if (q < n) sw_out[q] = make_float4(sc[0], sc[1], sc[2], sw[q].w);
+        }
+        umma::fence_before();
+        wg_sync(wg);  // red is rewritten by the next chunk
+      }
+      if (!has) break;
+      cprev = c;
     }
   } else {
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {

@@ -186,6 +186,10 @@ static inline SymScratch sym_layout(void* base, int64_t n, int M, int nsplit, in
   // sub-cell; 1.3x headroom (an exceeding ensemble runs the ordered path, see k_sym_tiles)
   const int64_t ncell = n / std::max(M, 1);
   int64_t cap = (int64_t)(1.3 * (double)Tmax * (double)(ncell + 2 * TI)) + 4096;
+  // at most 16 GiB of slots (a near-uniform n = 2^24, M = 1024 ensemble needs ~7 GB); a
+  // degenerate ensemble (e.g. one huge cell) beyond that takes the ordered path
+  const int64_t cap_max = ((int64_t)16 << 30) / (int64_t)(sizeof(float) * nc);
+  cap = std::min(cap, cap_max);
   if (const char* e = getenv("SPIC_SYM_CAP_SLOTS")) cap = atoll(e);  // tests: force the fallback
   size_t o = 0;
   auto take = [&](size_t b) {

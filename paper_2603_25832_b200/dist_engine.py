@@ -218,7 +218,7 @@ class DistSimulation:
             raise TypeError("unsupported estimator for the device step engine")
         ntot = n + h
         U = torch.empty(dv, max(ntot, 1), dtype=torch.float32, device=self.dev)
-        buf, nb = _lib.scratch("landau", _lib.query("spic_landau_scratch_bytes", ntot, g.M, dv,
+        buf, nb = _lib.scratch("pairs", _lib.query("spic_landau_scratch_bytes", ntot, g.M, dv,
                                                     self.opt.landau_split))
         ev = None
         if self.time_collision:

@@ -440,7 +440,7 @@ def blob_sorted(ci: CellIndex, particles: ParticleEnsemble, grid: Grid, bandwidt
     dev = particles.x.device
     if h_cell is None:
         h_cell = torch.empty(grid.M, dtype=torch.float32, device=dev)
-    buf, nb = _lib.scratch("blob", _lib.query("spic_blob_scratch_bytes", n, grid.M, dv))
+    buf, nb = _lib.scratch("pairs", _lib.query("spic_blob_scratch_bytes", n, grid.M, dv))
     _lib.call("spic_blob", _lib.ptr(ci.xv), _lib.ptr(ci.sw), _lib.ptr(ci.perm), n, dv,
               _lib.ptr(ci.cell_start), _lib.ptr(ci.sub_start) if ci.S > 1 else None, grid.M, ci.S,
               float(grid.eta), float(bandwidth) if bandwidth is not None else -1.0,
