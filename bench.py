@@ -460,6 +460,68 @@ def config1_microbench(torch, device, n: int = 131072, reps: int = 3) -> dict:
             "momentum_rel": mom, "energy_rel": en}
 
 
+def hbm_peak_gbs() -> float:
+    """Measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs); the profiling recipe's fallback
+    6650 GB/s only when the driver-written file is absent."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        return 6650.0
+
+
+def hbm_microbench(torch, device, peak_gbs: float, n: int = 1 << 24, M: int = 1024,
+                   reps: int = 5) -> dict:
+    """HBM-bound kernels at config-4 size (n = 2^24, M = 1024: 400+ MB of particle state,
+    beyond the 126 MB L2): push (interpolate + Lorentz + advance + wrap), binning, deposit.
+    Each launch is timed alone with CUDA events after an L2 flush. Algorithmic bytes per
+    particle: push 24 (read + write x, v0, v1; the Lorentz step with B = (0, 0, B3) leaves v2
+    as it is — SURVEY §8(d) counts 32 with v2), binning 52, deposit 16 (the
+    x, v record; uniform weights)."""
+    from paper_2603_25832_b200 import _lib
+    from paper_2603_25832_b200.collision import auto_sub_cells, build_cell_index
+    from paper_2603_25832_b200.pic import Grid, deposit_from_index
+    from paper_2603_25832_b200.state import ParticleEnsemble, new_flags
+
+    rng = np.random.default_rng(3)
+    L = 4 * math.pi
+    p = ParticleEnsemble.from_arrays(rng.uniform(0, L, n).astype(np.float32),
+                                     rng.normal(size=(n, 3)).astype(np.float32),
+                                     np.full(n, L / n, np.float32), device=device)
+    grid = Grid(M, L / M)
+    S = auto_sub_cells(n, M)
+    E = [torch.zeros(M, dtype=torch.float64, device=device) for _ in range(3)]
+    flags = new_flags(device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    ci = build_cell_index(p, grid, S)
+    st = _lib.stream_handle()
+
+    def timed(fn):
+        out = []
+        for _ in range(reps + 1):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return statistics.median(out[1:])
+
+    res = {"n": n, "M": M, "sub_cells": S, "l2": "flushed before every timed launch",
+           "peak_gbs": peak_gbs}
+    for name, fn, bpp in (
+            ("push", lambda: _lib.call("spic_push", _lib.ptr(p.x), _lib.ptr(p.vp), n, n, 3,
+                                       _lib.ptr(E[0]), _lib.ptr(E[1]), _lib.ptr(E[2]), M,
+                                       float(grid.eta), 0.0, _lib.ptr(flags), st), 24),
+            ("bin", lambda: build_cell_index(p, grid, S, out=ci), 52),
+            ("deposit", lambda: deposit_from_index(ci, p, grid), 16)):
+        ms = timed(fn)
+        gbs = bpp * n / (ms * 1e-3) / 1e9
+        res[name] = {"ms": ms, "bytes_per_particle": bpp, "achieved_gbs": gbs,
+                     "frac": gbs / peak_gbs}
+    return res
+
+
 def build_dist_sim(wl: dict, seed: int, device, world: int):
     """Weak-scaled decomposed problem: world x (n, M, L) of the workload, cell ranges per rank."""
     from paper_2603_25832_b200.dist_engine import DistSimulation
@@ -688,6 +750,10 @@ def main():
             out["config1_microbench"] = mb
         except Exception as exc:  # noqa: BLE001
             out["config1_microbench"] = {"error": str(exc)}
+        try:
+            out["hbm_kernels"] = hbm_microbench(torch, device, hbm_peak_gbs())
+        except Exception as exc:  # noqa: BLE001
+            out["hbm_kernels"] = {"error": str(exc)}
     if world == 1 and args.workload + "ss" in WORKLOADS:
         # the same config with the reference's own softsign network (like-for-like with the
         # reference arm, which has no SiLU network)
