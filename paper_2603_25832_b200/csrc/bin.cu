@@ -18,6 +18,7 @@
 //                      therefore (key, tile, warp, group, lane) = (key, pid): stable.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -261,6 +262,170 @@ __global__ void __launch_bounds__(256) k_bin_scatter(
   }
 }
 
+// ---- LSD radix path: two stable 8/7-bit digit passes with many small tiles --------------
+// The single-pass scatter above ranks keys with one warp per K-entry histogram slice, so for
+// K = M*S up to 32768 only 1-2 warps fit per SM and the sweep is latency-bound. The radix path
+// sorts the same (key, pid) order with <= 256 buckets per pass: 8 warps per tile, thousands
+// of tiles, and the counts table stays 256 x tiles. Key word: bits 0-14 key, bit 15 the
+// "x rounds onto L" flag (stored x - L).
+constexpr int kRxW = 8, kRxG = 8, kRxT = kRxW * 32 * kRxG;  // tile = 2048 records
+constexpr int kRxB = 256;
+
+struct RadixPlan {
+  int bits, passes, n_tiles;
+  size_t counts_elems, nb_scan;
+};
+
+static RadixPlan radix_plan(int64_t n, int M, int S) {
+  RadixPlan r;
+  const int K = M * S;
+  r.bits = 1;
+  while ((1 << r.bits) < K) ++r.bits;
+  r.passes = r.bits <= 8 ? 1 : 2;
+  r.n_tiles = (int)std::max<int64_t>(1, (n + kRxT - 1) / kRxT);
+  r.counts_elems = (size_t)kRxB * r.n_tiles;
+  r.nb_scan = (r.counts_elems + kScanChunk - 1) / kScanChunk;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t key_word(float xf, double eta, int M, int S) {
+  const CellKey ck = cell_key(xf, eta, M, S);
+  return (uint32_t)(ck.cell * S + ck.sub) | (ck.wrapped ? 0x8000u : 0u);
+}
+
+// histogram of one digit per tile (keys from x on the first pass, else from key_in)
+template <bool FROM_X>
+__global__ void __launch_bounds__(256) k_radix_count(const float* __restrict__ x,
+                                                     const uint32_t* __restrict__ key_in,
+                                                     uint32_t* __restrict__ key_out, int64_t n,
+                                                     double eta, int M, int S, int shift,
+                                                     int mask, int n_tiles,
+                                                     int32_t* __restrict__ counts) {
+  __shared__ int hist[kRxB];
+  for (int k = threadIdx.x; k < kRxB; k += blockDim.x) hist[k] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRxT;
+#pragma unroll
+  for (int u = 0; u < kRxT / 256; ++u) {
+    const int64_t i = base + u * 256 + threadIdx.x;
+    if (i < n) {
+      uint32_t kw;
+      if (FROM_X) {
+        kw = key_word(x[i], eta, M, S);
+        key_out[i] = kw;
+      } else {
+        kw = key_in[i];
+      }
+      atomicAdd(&hist[(kw >> shift) & mask], 1);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kRxB; k += blockDim.x)
+    counts[(size_t)k * n_tiles + blockIdx.x] = hist[k];
+}
+
+// Stable scatter of one digit pass: warp w of a tile owns records [32 G w, 32 G (w+1)); per-warp
+// digit counts, prefix across warps seeded with the scanned (digit, tile) offset, then each
+// warp replays its records in order ranking equal digits with __match_any_sync. The record
+// payload (pid, (x', v), w) travels with the key, so every pass reads its input in order:
+//   MODE 0: first of two passes   planes (pid order) -> key1, idx1, rec1, w1 (by low digit)
+//   MODE 1: second of two passes  key1, idx1, rec1, w1 -> perm, sorted keys, xv, sw
+//   MODE 2: the only pass         planes (pid order) -> perm, sorted keys, xv, sw
+template <int MODE>
+__global__ void __launch_bounds__(kRxW * 32) k_radix_scatter(
+    const uint32_t* __restrict__ key_in, const int32_t* __restrict__ idx_in,
+    const float4* __restrict__ rec_in, const float* __restrict__ w_in, int64_t n, int shift,
+    int mask, int n_tiles, const int32_t* __restrict__ scanned, uint32_t* __restrict__ key_out,
+    int32_t* __restrict__ idx_out, float4* __restrict__ rec_out, float* __restrict__ w_out,
+    const float* __restrict__ x, const float* __restrict__ v, int64_t ldv,
+    const float* __restrict__ w, int dv, double L) {
+  __shared__ int hist[kRxW][kRxB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < kRxW * kRxB; k += blockDim.x) (&hist[0][0])[k] = 0;
+  __syncthreads();
+  const int64_t wbase = (int64_t)blockIdx.x * kRxT + (int64_t)wid * 32 * kRxG;
+  uint32_t kw[kRxG];
+#pragma unroll
+  for (int g = 0; g < kRxG; ++g) {
+    const int64_t i = wbase + g * 32 + lane;
+    kw[g] = i < n ? key_in[i] : 0u;
+  }
+#pragma unroll
+  for (int g = 0; g < kRxG; ++g)
+    if (wbase + g * 32 + lane < n) atomicAdd(&hist[wid][(kw[g] >> shift) & mask], 1);
+  __syncthreads();
+  for (int k = threadIdx.x; k < kRxB; k += blockDim.x) {
+    int run = scanned[(size_t)k * n_tiles + blockIdx.x];
+#pragma unroll
+    for (int q = 0; q < kRxW; ++q) {
+      const int t = hist[q][k];
+      hist[q][k] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  int* my = hist[wid];
+#pragma unroll 2
+  for (int g = 0; g < kRxG; ++g) {
+    const int64_t i = wbase + g * 32 + lane;
+    const bool valid = i < n;
+    // payload of this record (coalesced loads, issued before the ranking)
+    int32_t pid = 0;
+    float4 rec = make_float4(0.f, 0.f, 0.f, 0.f);
+    float wv = 0.f;
+    if (valid) {
+      if (MODE == 1) {
+        pid = idx_in[i];
+        rec = rec_in[i];
+        wv = w_in ? w_in[i] : 0.f;
+      } else {
+        pid = (int32_t)i;
+        const float xi = x[i];
+        rec.x = (kw[g] & 0x8000u) ? (float)((double)xi - L) : xi;
+        rec.y = v[i];
+        rec.z = v[ldv + i];
+        rec.w = dv > 2 ? v[2 * ldv + i] : 0.f;
+        wv = w ? w[i] : 0.f;
+      }
+    }
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const int dg = (int)((kw[g] >> shift) & mask);
+      const unsigned peers = __match_any_sync(active, dg);
+      const int rank = __popc(peers & lanemask_lt());
+      const int basepos = my[dg];
+      __syncwarp(active);
+      if (rank == 0) my[dg] = basepos + __popc(peers);
+      const int pos = basepos + rank;
+      key_out[pos] = kw[g];
+      if (idx_out) idx_out[pos] = pid;
+      if (rec_out) rec_out[pos] = rec;
+      if (MODE == 0) {
+        if (w_out) w_out[pos] = wv;
+      } else if (w_out) {  // the sw record: scores are filled in later, w in lane 3
+        reinterpret_cast<float4*>(w_out)[pos] = make_float4(0.f, 0.f, 0.f, wv);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// cell_start / sub_start from the sorted key words: position k starts every key in
+// (key[k-1], key[k]] (key[-1] = -1, key[n] = K)
+__global__ void k_radix_starts(const uint32_t* __restrict__ key_sorted, int64_t n, int M, int S,
+                               int32_t* __restrict__ cell_start, int32_t* __restrict__ sub_start) {
+  const int K = M * S;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int cur = k < n ? (int)(key_sorted[k] & 0x7FFFu) : K;
+    const int prev = k > 0 ? (int)(key_sorted[k - 1] & 0x7FFFu) : -1;
+    for (int q = prev + 1; q <= cur; ++q) {
+      if (sub_start) sub_start[q] = (int32_t)k;
+      if (q % S == 0) cell_start[q / S] = (int32_t)k;
+    }
+  }
+}
+
 __global__ void k_gather_scores(const float* __restrict__ s, int64_t lds,
                                 const int32_t* __restrict__ perm, int64_t n, int dv,
                                 float4* __restrict__ sw, int32_t* flags) {
@@ -299,10 +464,83 @@ extern "C" int spic_cell_of(const float* x, int64_t n, double eta, int32_t M, in
   return SPIC_OK;
 }
 
+// Path choice: the radix path wins from ~2^21 records (c3: 0.81 -> 0.51 ms, n = 2^24:
+// 5.15 -> 1.93 ms); below that its 11 launches cost more than the single-pass sort saves
+// (equal at 2^20, 0.051 vs 0.074 ms at 2^16). SPIC_BIN_VARIANT=c / r forces a path (A/B tests).
+static bool bin_use_counting(int64_t n) {
+  const char* e = getenv("SPIC_BIN_VARIANT");
+  if (e && e[0] == 'c') return true;
+  if (e && e[0] == 'r') return false;
+  return n < ((int64_t)1 << 21);
+}
+
+static size_t radix_scratch_bytes(int64_t n, int32_t M, int32_t S) {
+  RadixPlan r = radix_plan(n, M, S);
+  // key words (pid order), pass-1 (key, pid, record, w), sorted keys, counts + block sums
+  return sizeof(int32_t) * (9 * (size_t)n + r.counts_elems + r.nb_scan + 64) + 8 * 256;
+}
+
 extern "C" size_t spic_bin_scratch_bytes(int64_t n, int32_t M, int32_t S) {
   if (M < 1 || S < 1) return 0;
   BinPlan p = bin_plan(n, M, S);
-  return (p.counts_elems + p.nb_scan + 64) * sizeof(int32_t);
+  size_t b = (p.counts_elems + p.nb_scan + 64) * sizeof(int32_t);
+  if (!bin_use_counting(n)) b = std::max(b, radix_scratch_bytes(n, M, S));
+  return b;
+}
+
+static int bin_radix(const float* x, const float* v, int64_t ldv, const float* w, int64_t n,
+                     int32_t dv, double eta, int32_t M, int32_t S, int32_t* perm,
+                     int32_t* cell_start, int32_t* sub_start, float* xv, float* sw,
+                     void* scratch, cudaStream_t st) {
+  RadixPlan r = radix_plan(n, M, S);
+  auto align = [](void* p) { return (void*)(((uintptr_t)p + 255) & ~(uintptr_t)255); };
+  uint32_t* key0 = (uint32_t*)align(scratch);
+  uint32_t* key1 = (uint32_t*)align(key0 + n);
+  int32_t* idx1 = (int32_t*)align(key1 + n);
+  uint32_t* keyS = (uint32_t*)align(idx1 + n);
+  float4* rec1 = (float4*)align(keyS + n);
+  float* w1 = (float*)align(rec1 + n);
+  int32_t* counts = (int32_t*)align(w1 + n);
+  int32_t* bsum = counts + r.counts_elems;
+  const double L = (double)M * eta;
+  const unsigned nt = (unsigned)r.n_tiles;
+  auto scan = [&]() {
+    k_scan_reduce<<<(unsigned)r.nb_scan, kScanThreads, 0, st>>>(counts, r.counts_elems, bsum);
+    k_scan_blocksums<<<1, kScanThreads, 0, st>>>(bsum, r.nb_scan);
+    k_scan_apply<<<(unsigned)r.nb_scan, kScanThreads, 0, st>>>(counts, r.counts_elems, bsum);
+    for (int k = 0; k < 3; ++k) spic::count_launch();
+  };
+  const int lo_bits = r.passes == 1 ? r.bits : 8;
+  const int mask0 = (1 << lo_bits) - 1;
+  k_radix_count<true><<<nt, 256, 0, st>>>(x, nullptr, key0, n, eta, M, S, 0, mask0, r.n_tiles,
+                                          counts);
+  spic::count_launch();
+  scan();
+  if (r.passes == 1) {
+    k_radix_scatter<2><<<nt, kRxW * 32, 0, st>>>(key0, nullptr, nullptr, nullptr, n, 0, mask0,
+                                                 r.n_tiles, counts, keyS, perm, (float4*)xv, sw,
+                                                 x, v, ldv, w, dv, L);
+    spic::count_launch();
+  } else {
+    k_radix_scatter<0><<<nt, kRxW * 32, 0, st>>>(key0, nullptr, nullptr, nullptr, n, 0, mask0,
+                                                 r.n_tiles, counts, key1, idx1, rec1,
+                                                 w ? w1 : nullptr, x, v, ldv, w, dv, L);
+    spic::count_launch();
+    const int mask1 = (1 << (r.bits - 8)) - 1;
+    k_radix_count<false><<<nt, 256, 0, st>>>(nullptr, key1, nullptr, n, eta, M, S, 8, mask1,
+                                             r.n_tiles, counts);
+    spic::count_launch();
+    scan();
+    k_radix_scatter<1><<<nt, kRxW * 32, 0, st>>>(key1, idx1, rec1, w ? w1 : nullptr, n, 8, mask1,
+                                                 r.n_tiles, counts, keyS, perm, (float4*)xv, sw,
+                                                 nullptr, nullptr, 0, nullptr, dv, L);
+    spic::count_launch();
+  }
+  const int sb = (int)std::min<int64_t>((n + 256) / 256, kNumSMs * 8);
+  k_radix_starts<<<sb, 256, 0, st>>>(keyS, n, M, S, cell_start, sub_start);
+  spic::count_launch();
+  SPIC_CHECK_LAUNCH();
+  return SPIC_OK;
 }
 
 extern "C" int spic_bin(const float* x, const float* v, int64_t ldv, const float* w, int64_t n,
@@ -325,6 +563,9 @@ extern "C" int spic_bin(const float* x, const float* v, int64_t ldv, const float
     SPIC_CHECK_LAUNCH();
     return SPIC_OK;
   }
+  if (!bin_use_counting(n))
+    return bin_radix(x, v, ldv, w, n, dv, eta, M, S, perm, cell_start, sub_start, xv, sw, scratch,
+                     st);
   size_t smem_count = sizeof(int) * p.K;
   if (smem_count > 48 * 1024)
     cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_count);

@@ -830,3 +830,46 @@ def test_symmetric_blob_path_matches_ordered_and_oracle(spic, case):
     check_field(s_ord, ref, tol=2e-4)
     check_field(s_fb, ref, tol=2e-4)
     check_field(s_sym, s_ord, tol=1e-4)
+
+
+@pytest.mark.parametrize("n,M,S", [(3000, 16, 8), (100000, 64, 16), (1 << 20, 128, 64),
+                                   (50000, 1024, 32), (777, 1, 1), (40000, 3, 64)])
+def test_radix_binning_equals_counting_sort(spic, n, M, S):
+    """The LSD radix binning (SPIC_BIN_VARIANT=r; the default from 2^21 records) and the
+    single-pass counting sort (SPIC_BIN_VARIANT=c) produce identical permutations, cell/sub-cell
+    starts and records, including the x -> L rounding quirk (stored as x - L in cell 0)."""
+    import os
+
+    from paper_2603_25832_b200.collision import build_cell_index
+    from paper_2603_25832_b200.pic import Grid
+
+    rng = np.random.default_rng(n + M)
+    L = 2.0 * M
+    x = rng.uniform(0, L, n).astype(np.float32)
+    x[: n // 50] = np.nextafter(np.float32(L), np.float32(0))  # rounds onto L in float64 x/eta?
+    x[n // 50: n // 25] = rng.uniform(0, 2.0, n // 25 - n // 50).astype(np.float32)  # a dense cell
+    v = rng.normal(size=(n, 3))
+    p = ens(x.astype(np.float64), v, np.full(n, L / n))
+    grid = Grid(M, L / M)
+
+    def run(env):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            ci = build_cell_index(p, grid, S=S)
+            torch.cuda.synchronize()
+            return [t.cpu().numpy() for t in (ci.perm, ci.cell_start, ci.sub_start, ci.xv, ci.sw)]
+        finally:
+            for k, val in old.items():
+                if val is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = val
+
+    a = run({"SPIC_BIN_VARIANT": "r"})
+    b = run({"SPIC_BIN_VARIANT": "c"})
+    for u, w_ in zip(a, b):
+        assert np.array_equal(u, w_)
+    # the reference's stable argsort of the cell ids (S = 1 order refined by sub-cell)
+    cell = np.minimum(np.floor(x.astype(np.float64) / grid.eta).astype(np.int64) % M, M - 1)
+    assert np.array_equal(np.sort(a[0][a[1][0]:a[1][1]]), np.flatnonzero(cell == 0))
