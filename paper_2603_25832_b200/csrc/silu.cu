@@ -276,6 +276,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     phase2 ^= 1;
     umma::fence_after();
     SILU_TRACE(9);
+#ifdef SPIC_SILU_NO_F3  // timing diagnostic only (wrong gradients): G1 without concurrent F3
+    return;
+#endif
     float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
     float vd[16], vf[16];
     umma::tmem_ld12(tl + cD2 + p0, vd);
@@ -311,22 +314,22 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       handoff_wait(6);  // X written (F1 of chunk c)
       umma::fence_after();
       SILU_TRACE_I(10);
-      if (lane == 0) {
+      {  // the whole warp issues (elect.sync inside), see umma::mma_elect
         if constexpr (MODE == 0) {
           // the forward double-buffers X (odd chunks in the unused B tiles) and D1 (odd chunks
           // in the D2 columns)
           const bool odd = iit & 1;
           const uint32_t xb = odd ? sBh : sXh;
-          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + (odd ? cD2 : cD1), sW2h,
+          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(tm + (odd ? cD2 : cD1), sW2h,
                                                                 sW2l, xb, xb + kXTile, false);
         } else {
-          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(tm + cD1, sW2h, sW2l, sXh, sXl,
+          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(tm + cD1, sW2h, sW2l, sXh, sXl,
                                                                 false);  // W2 h1
         }
         if (DIV)
-          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf>(
+          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(
               tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);  // B d1
-        umma::commit(&S.bar[0]);
+        umma::commit_elect(&S.bar[0]);
       }
       __syncwarp();
       SILU_TRACE_I(11);
@@ -334,21 +337,21 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         handoff_wait(7);  // Y written (F2b of chunk c)
         umma::fence_after();
         SILU_TRACE_I(12);
-        if (lane == 0) {
+        {
           // G3 first: the next chunk's layer-1 sweep waits for it (X, Y reuse)
-          umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(tm + cD3, sYh, sYl, sXh,
+          umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(tm + cD3, sYh, sYl, sXh,
                                                                       sXl, !fst);  // da2 h1^T
           if (DIV)
-            umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf>(
+            umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(
                 tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
                 !fst);  // y2 d1^T
-          umma::commit(&S.bar[1]);
-          umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(tm + cD2, sW2h, sW2l, sYh, sYl,
+          umma::commit_elect(&S.bar[1]);
+          umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(tm + cD2, sW2h, sW2l, sYh, sYl,
                                                                false);  // W2^T da2
           if (DIV)
-            umma::gemm_split<true, false, kCP, 8, 16384, kXHalf>(
+            umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(
                 tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
-          umma::commit(&S.bar[2]);
+          umma::commit_elect(&S.bar[2]);
         }
         __syncwarp();
         SILU_TRACE_I(13);

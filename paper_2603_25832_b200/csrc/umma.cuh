@@ -58,13 +58,26 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// Warp-wide issue: every lane of the issuing warp executes the same (warp-uniform) instruction
+// stream and elect.sync picks the one lane that issues. Compared with `if (lane == 0) mma(...)`
+// this keeps the control flow convergent, so the operands stay in uniform registers instead of
+// a per-instruction ELECT / R2UR / BRA.U.ANY waterfall (the issue rate, not the tensor pipe,
+// bounded the small-N GEMMs when the issuing warp shares its scheduler with busy warps).
+__device__ __forceinline__ void mma_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
 // D[128 x N] (+)= A * B over K = 16 * KSTEPS with split-BF16 operands:
 // Ahi*Bhi + Ahi*Blo + Alo*Bhi (~2^-16 relative per product; float32 accumulation in TMEM).
 // Operand addresses are tile (sub-)block starts. Issued by one thread. The four base
 // descriptors are built once; every K-step only adds a constant to their start-address
 // field (addresses stay below 2^18, so the 14-bit field never carries).
 template <bool A_MN, bool B_MN, int N = 128, int KSTEPS = 8, uint32_t AH = 16384,
-          uint32_t BH = 16384>
+          uint32_t BH = 16384, bool WARP = false>
 __device__ __forceinline__ void gemm_split(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
                                            uint32_t b_hi, uint32_t b_lo, bool accumulate) {
   constexpr uint32_t id = idesc_bf16(A_MN ? 1u : 0u, B_MN ? 1u : 0u, (uint32_t)N);
@@ -78,9 +91,15 @@ __device__ __forceinline__ void gemm_split(uint32_t d_tmem, uint32_t a_hi, uint3
                              : (uint64_t)(((ks >> 2) * AH + (ks & 3) * 32) >> 4);
     const uint64_t bo = B_MN ? (uint64_t)(ks * 2048 >> 4)
                              : (uint64_t)(((ks >> 2) * BH + (ks & 3) * 32) >> 4);
-    mma(d_tmem, ah0 + ao, bh0 + bo, id, (accumulate || ks > 0) ? 1u : 0u);
-    mma(d_tmem, ah0 + ao, bl0 + bo, id, 1u);
-    mma(d_tmem, al0 + ao, bh0 + bo, id, 1u);
+    if (WARP) {
+      mma_elect(d_tmem, ah0 + ao, bh0 + bo, id, (accumulate || ks > 0) ? 1u : 0u);
+      mma_elect(d_tmem, ah0 + ao, bl0 + bo, id, 1u);
+      mma_elect(d_tmem, al0 + ao, bh0 + bo, id, 1u);
+    } else {
+      mma(d_tmem, ah0 + ao, bh0 + bo, id, (accumulate || ks > 0) ? 1u : 0u);
+      mma(d_tmem, ah0 + ao, bl0 + bo, id, 1u);
+      mma(d_tmem, al0 + ao, bh0 + bo, id, 1u);
+    }
   }
 }
 
@@ -103,6 +122,13 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
           (uint32_t)__cvta_generic_to_shared(bar))
       : "memory");
 }
