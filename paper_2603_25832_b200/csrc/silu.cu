@@ -346,6 +346,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
                 tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
                 !fst);  // y2 d1^T
           umma::commit_elect(&S.bar[1]);
+#ifdef SPIC_SILU_TRACE_G3  // timing diagnostic: stamp G3's completion before issuing G2
+          {
+            uint32_t ph = (uint32_t)(iit & 1);
+            umma::wait_mma(&S.bar[1], ph);
+            SILU_TRACE_I(14);
+          }
+#endif
           umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(tm + cD2, sW2h, sW2l, sYh, sYl,
                                                                false);  // W2^T da2
           if (DIV)

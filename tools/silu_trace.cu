@@ -69,6 +69,9 @@ int main() {
     a12 += h[it * 16 + 12] - t2;   // issuer sees Y ready
     a13 += h[it * 16 + 13] - t2;   // G3 + G2 issued
   }
+  double a14 = 0;
+  for (int it = 4; it < 4 + cnt; ++it) a14 += h[it * 16 + 14] - (double)h[it * 16 + 12];
+  if (h[4 * 16 + 14]) printf("G3 complete %.0f cycles after the issuer saw Y ready\n", a14 / cnt);
   printf("from F1 hand-off: issuer X-ready %+.0f, G1 issued %+.0f, G1 done %+.0f, F2b done %+.0f,\n"
          "  issuer Y-ready %+.0f, G3+G2 issued %+.0f; next chunk's F3 got G2 %+.0f after its F1 hand-off\n",
          a10 / cnt, a11 / cnt, a4 / cnt, a7 / cnt, a12 / cnt, a13 / cnt, a9 / cnt);
