@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     bool fst = true;
     int iit = 0;
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++iit) {
-      handoff_wait(6);  // X written (F1 of chunk c)
+      handoff_wait(MODE == 0 && (iit & 1) ? 8 : 6);  // X written (F1 of chunk c)
       umma::fence_after();
       SILU_TRACE_I(10);
       {  // the whole warp issues (elect.sync inside), see umma::mma_elect
@@ -395,7 +395,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         }
         fence_proxy_async();
         umma::fence_before();
-        handoff_arrive(6);
+        // bar.arrive does not wait, so a warpgroup can run one chunk ahead of another (never
+        // two: that needs G1 of the chunk before, i.e. everyone's arrival for it). Alternating
+        // barrier IDs by chunk parity keep an early arrival from completing the issuer's
+        // barrier of the previous chunk before a lagging warpgroup has written its rows.
+        handoff_arrive(buf ? 8 : 6);
       }
       if (cprev >= 0) {
         umma::wait_mma(&S.bar[0], phase);

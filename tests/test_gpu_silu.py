@@ -249,3 +249,20 @@ def test_run_end_to_end_with_silu_net(lib, tmp_path):
     assert np.all(np.isfinite(E))
     assert abs(E[-1] - E[0]) <= 1e-2 * abs(E[0])
     assert (tmp_path / "diagnostics.csv").exists()
+
+
+def test_silu_forward_large_n_repeatable(lib):
+    """n = 2^22 (~590 chunks per CTA through the double-buffered forward pipeline): three
+    launches are bit-identical and a sample matches the float64 oracle. Guards the per-chunk
+    hand-off between the compute warpgroups and the MMA-issuing warp."""
+    from paper_2603_25832_b200.silu_net import silu_forward
+
+    n, L = 1 << 22, 2 * math.pi / 1.25
+    params = _params(seed=3)
+    x, v, _ = _ensemble(n, L, seed=4)
+    net = _net(params)
+    outs = [silu_forward(net, x, v, L).cpu().numpy() for _ in range(3)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    idx = np.random.default_rng(5).choice(n, 4096, replace=False)
+    ref, _ = so.forward(params, so.inputs(x[idx], v[idx], L), H)
+    assert relL2(outs[0][idx], ref) <= 1e-4
