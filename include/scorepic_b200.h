@@ -66,7 +66,9 @@ int spic_fp32_probe(int32_t iters, int32_t blocks, float* out, double* flop, voi
 int spic_cell_of(const float* x, int64_t n, double eta, int32_t M, int32_t* cell, void* stream);
 
 size_t spic_bin_scratch_bytes(int64_t n, int32_t M, int32_t S);
-/* Stable counting sort by key = (cell, sub) where sub = floor(frac(x/eta)*S).
+/* Stable sort by key = (cell, sub) where sub = floor(frac(x/eta)*S): a single-pass counting
+ * sort below 2^21 records, an LSD radix sort (two <= 8-bit digit passes) above; both give the
+ * same permutation.
  * S == 1 gives exactly np.argsort(cell_of(x), kind="stable") (the reference CellIndex).
  * Outputs: perm[n] (sorted position -> pid), cell_start[M+1], sub_start[M*S+1] (nullable).
  * Optional fused gather (all nullable): xv[n], sw[n] (w lane only) in sorted order. */
@@ -84,7 +86,11 @@ size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nspli
 /* U (sorted order, float[dv][n]) for all targets against their 3-cell stencil.
  * gamma must be -3 (dv=3) or -2 (dv=2) or any value (generic pow path).
  * uniform_w > 0: all weights equal uniform_w (sw.w ignored). nsplit: j-window split
- * factor (0 = automatic). */
+ * factor (0 = automatic).
+ * dv = 3, gamma = -3, uniform_w > 0 run the antisymmetric unordered-pair kernel (each pair
+ * evaluated once for both targets; deterministic slot fold); its slot storage is part of
+ * the scratch (sized for a near-uniform ensemble, <= 16 GiB); an ensemble needing more
+ * runs the ordered enumeration inside the same launches. Results identical to 1e-6 rel. */
 int spic_landau(const float* xv, const float* sw, int64_t n, int32_t dv, const int32_t* cell_start,
                 const int32_t* sub_start, int32_t M, int32_t S, double eta, double gamma,
                 float uniform_w, int32_t nsplit, float* U_sorted, void* scratch,
@@ -120,7 +126,8 @@ int spic_count_live_pairs(const float* xv, int64_t n, const int32_t* cell_start,
  *      score.py:493-500, blob_score score.py:503-523) -------------------------------------- */
 size_t spic_blob_scratch_bytes(int64_t n, int32_t M, int32_t dv);
 /* Writes s into sw lanes 0..dv-1 (sorted order). bandwidth <= 0: Silverman per cell over
- * the stencil. On den <= 0 / non-finite: SPIC_FLAG_ISOLATED and *bad_pid = pid of the first
+ * the stencil. dv = 3 with uniform_w > 0 sums over unordered pairs (symmetric weights;
+ * a second exponential only across two cells' Silverman bandwidths). On den <= 0 / non-finite: SPIC_FLAG_ISOLATED and *bad_pid = pid of the first
  * offending particle in (cell, pid) order (bad_pid must be preset to INT64_MAX). */
 int spic_blob(const float* xv, float* sw, const int32_t* perm, int64_t n, int32_t dv,
               const int32_t* cell_start, const int32_t* sub_start, int32_t M, int32_t S, double eta,
