@@ -15,6 +15,7 @@
 // tiles, 512 TMEM columns); per-CTA float64 partial rows are reduced in a fixed order and
 // finalized by the shared AdamW kernel (adamw.cuh).
 #include <algorithm>
+#include <cstdlib>
 
 #include "adamw.cuh"
 #include "common.cuh"
@@ -804,6 +805,18 @@ __global__ void __launch_bounds__(1024) k_silu_finalize(
                       reset_lr, apply_step, params32, grads_out, loss_out, cand, flags);
 }
 
+// multi-CTA finalize (kSiluFinCTAs x 256 threads; sync = [ticket, ok flags])
+constexpr int kSiluFinCTAs = 32;
+__global__ void __launch_bounds__(256) k_silu_finalize_mc(
+    const double* __restrict__ row, int64_t P, bool mse, double* __restrict__ params,
+    double* __restrict__ m, double* __restrict__ v2, double* __restrict__ opt, double beta1,
+    double beta2, double eps, double wd, int reset_lr, int apply_step, float* __restrict__ params32,
+    double* __restrict__ grads_out, double* __restrict__ loss_out, double* cand, int32_t* flags,
+    int32_t* sync) {
+  adamw_with_recovery_mc(row[0], row + 1, P, mse, params, m, v2, opt, beta1, beta2, eps, wd,
+                         reset_lr, apply_step, params32, grads_out, loss_out, cand, flags, sync);
+}
+
 }  // namespace spic
 
 using namespace spic;
@@ -811,9 +824,10 @@ using namespace spic;
 extern "C" int64_t spic_silu_num_params(int32_t H) { return silu_params(H); }
 
 extern "C" size_t spic_silu_scratch_bytes(int64_t n) {
-  // [blocks][1 + P] partials, the reduced row, candidate parameters
+  // [blocks][1 + P] partials, the reduced row, candidate parameters, finalize sync words
   const size_t width = 1 + (size_t)silu_params(kH);
-  return sizeof(double) * ((size_t)(silu_blocks(n) + 1) * width + (size_t)silu_params(kH)) + 64;
+  return sizeof(double) * ((size_t)(silu_blocks(n) + 1) * width + (size_t)silu_params(kH)) + 64 +
+         sizeof(int32_t) * 64;
 }
 
 extern "C" int64_t spic_silu_row_offset(int64_t n) {
@@ -898,9 +912,19 @@ extern "C" int spic_silu_finalize(void* scratch, int64_t n, int32_t H, int32_t m
   if (n < 1) return SPIC_ERR_ARG;
   const int64_t P = silu_params(kH);
   double* row = (double*)((char*)scratch + spic_silu_row_offset(n));
-  k_silu_finalize<<<1, 1024, 0, (cudaStream_t)stream>>>(
-      row, P, mse != 0, params64, m, v2, opt_state, beta1, beta2, eps, weight_decay, reset_lr,
-      apply_step, params32, grads_out, loss_out, row + 1 + P, flags);
+  int32_t* sync = (int32_t*)(row + 1 + P + P);
+  cudaStream_t st = (cudaStream_t)stream;
+  const char* fv = getenv("SPIC_SILU_FINALIZE");  // "1": the single-CTA kernel (A/B tests)
+  if (fv && fv[0] == '1') {
+    k_silu_finalize<<<1, 1024, 0, st>>>(row, P, mse != 0, params64, m, v2, opt_state, beta1, beta2,
+                                        eps, weight_decay, reset_lr, apply_step, params32,
+                                        grads_out, loss_out, row + 1 + P, flags);
+  } else {
+    cudaMemsetAsync(sync, 0, sizeof(int32_t), st);  // the barrier ticket
+    k_silu_finalize_mc<<<kSiluFinCTAs, 256, 0, st>>>(
+        row, P, mse != 0, params64, m, v2, opt_state, beta1, beta2, eps, weight_decay, reset_lr,
+        apply_step, params32, grads_out, loss_out, row + 1 + P, flags, sync);
+  }
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;

@@ -266,3 +266,45 @@ def test_silu_forward_large_n_repeatable(lib):
     idx = np.random.default_rng(5).choice(n, 4096, replace=False)
     ref, _ = so.forward(params, so.inputs(x[idx], v[idx], L), H)
     assert relL2(outs[0][idx], ref) <= 1e-4
+
+
+@pytest.mark.parametrize("lr", [1e-3, 1e300])
+def test_silu_multicta_finalize_equals_single_cta(lib, lr):
+    """The multi-CTA AdamW finalize (default) against the single-CTA kernel
+    (SPIC_SILU_FINALIZE=1): identical parameters, moments, optimizer state and flags, also when
+    the first candidate is non-finite (lr = 1e300: restore and halve until finite)."""
+    import os
+
+    from paper_2603_25832_b200.score import AdamW
+    from paper_2603_25832_b200.silu_net import _silu_finalize, _silu_partials, records
+    from paper_2603_25832_b200.state import new_flags
+
+    L = 4 * math.pi
+    params = _params(seed=7)
+    x, v, w = _ensemble(20000, L, seed=8)
+    out = []
+    for env in ({}, {"SPIC_SILU_FINALIZE": "1"}):
+        old = {k: os.environ.get(k) for k in ("SPIC_SILU_FINALIZE",)}
+        os.environ.update(env)
+        try:
+            net = _net(params)
+            xv, sw = records(x, v, w, L, "cuda")
+            opt = AdamW(lr=lr, device="cuda")
+            flags = new_flags("cuda")
+            for _ in range(2):
+                buf = _silu_partials(net, xv, sw, xv.shape[0], L)
+                _silu_finalize(net, buf, xv.shape[0], opt, reset_lr=False, apply_step=True,
+                               flags=flags)
+            torch.cuda.synchronize()
+            out.append([t.cpu().numpy().copy() for t in (net.params64, net.params32, opt.m, opt.v,
+                                                          opt.state, flags)])
+        finally:
+            for k, val in old.items():
+                if val is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = val
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
+    if lr > 1.0:
+        assert out[0][5][lib.FLAG_LR_HALVINGS] > 0
