@@ -44,11 +44,18 @@ __device__ long long g_silu_trace[64 * 16];
   do {                                                                                 \
     if (blockIdx.x == 0 && threadIdx.x == 0 && it < 64) g_silu_trace[it * 16 + (k)] = clock64(); \
   } while (0)
+#define SILU_TRACE_K(k)                                                                \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_silu_trace[63 * 16 + (k)] = clock64();   \
+  } while (0)
 #define SILU_TRACE_I(k)                                                                \
   do {                                                                                 \
     if (blockIdx.x == 0 && lane == 0 && iit < 64) g_silu_trace[iit * 16 + (k)] = clock64(); \
   } while (0)
 #else
+#define SILU_TRACE_K(k) \
+  do {                  \
+  } while (0)
 #define SILU_TRACE_I(k) \
   do {                  \
   } while (0)
@@ -196,6 +203,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const float4* __restrict__ sw = in.sw;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
+  static_assert(56 * 1024 + 16 * 32 * 17 * 8 <= 4 * 32768, "epilogue staging fits below X");
   uint8_t* W2h = base;
   uint8_t* W2l = base + 1 * umma::kTileBytes;
   uint8_t* Bh = base + 2 * umma::kTileBytes;
@@ -205,6 +213,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   constexpr uint32_t kY = 2 * kXTile;
   constexpr uint32_t kDivRows = kCP * 128;  // byte offset of the divergence rows
 
+  SILU_TRACE_K(0);
   const int tid = threadIdx.x, h = tid & (kH - 1), wg = tid >> 7, lane = tid & 31;
   const int quarter = (tid >> 5) & 3, wtid = tid & 127;
   const float* W1 = params;
@@ -241,6 +250,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   __syncthreads();
   umma::fence_after();
   const uint32_t tm = S.tmem;
+  SILU_TRACE_K(1);
   const uint32_t tl = tm + ((uint32_t)(quarter * 32) << 16);  // this warp's TMEM lanes
   const uint32_t sW2h = smem_u32(W2h), sW2l = smem_u32(W2l), sBh = smem_u32(Bh),
                  sBl = smem_u32(Bl), sXh = smem_u32(Xh), sXl = sXh + kXTile,
@@ -629,6 +639,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   if (MODE == 1 && pending) layer1_reverse(ub ^ 1);
   }
 
+  SILU_TRACE_K(2);
   if (ISM && tid < kNCW) {
     if (!first) {
       umma::wait_mma(&S.bar[1], phase3);
@@ -650,22 +661,40 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       float v[32], m[32];
       umma::tmem_ld32(tl + cD3 + (uint32_t)(32 * wg), v);
       if (DIV) umma::tmem_ld32(tl + cD4 + (uint32_t)(32 * wg), m);
+      // the dW2 row block (rows 32q.. of this warp, columns 32g..32g+31) goes out through a
+      // per-warp shared-memory transpose in two 16-column halves, so each store instruction
+      // writes two 128-B row segments instead of 32 scattered doubles (free space after the
+      // per-h combine area: base + 56 KB .. + 124 KB, 4352 B per warp)
+      constexpr int kStg = 17;  // padded row stride (doubles)
+      double* stg = reinterpret_cast<double*>(base + 56 * 1024) + (size_t)(tid >> 5) * 32 * kStg;
+      const int q32 = h & ~31;  // first row of this warp
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int hp = 32 * wg + i;
-        double g = first ? 0.0 : (double)v[i];
-        if (DIV && !first) {
-          const float Chh = fmaf(w3[2], W1[hp * 4 + 3], fmaf(w3[1], W1[hp * 4 + 2], w3[0] * W1[hp * 4 + 1]));
-          const float wm = W2[h * kH + hp] * m[i];
-          g += (double)(Chh * m[i]);
-          WM[h * kWMs + hp] = wm;
-          tw3[0] = fmaf(W1[hp * 4 + 1], wm, tw3[0]);
-          tw3[1] = fmaf(W1[hp * 4 + 2], wm, tw3[1]);
-          tw3[2] = fmaf(W1[hp * 4 + 3], wm, tw3[2]);
-        } else if (DIV) {
-          WM[h * kWMs + hp] = 0.f;
+      for (int half = 0; half < 2; ++half) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int i = 16 * half + j;
+          const int hp = 32 * wg + i;
+          double g = first ? 0.0 : (double)v[i];
+          if (DIV && !first) {
+            const float Chh = fmaf(w3[2], W1[hp * 4 + 3], fmaf(w3[1], W1[hp * 4 + 2], w3[0] * W1[hp * 4 + 1]));
+            const float wm = W2[h * kH + hp] * m[i];
+            g += (double)(Chh * m[i]);
+            WM[h * kWMs + hp] = wm;
+            tw3[0] = fmaf(W1[hp * 4 + 1], wm, tw3[0]);
+            tw3[1] = fmaf(W1[hp * 4 + 2], wm, tw3[1]);
+            tw3[2] = fmaf(W1[hp * 4 + 3], wm, tw3[2]);
+          } else if (DIV) {
+            WM[h * kWMs + hp] = 0.f;
+          }
+          stg[lane * kStg + j] = g;
         }
-        row[oW2 + h * kH + hp] = g;
+        __syncwarp();
+#pragma unroll
+        for (int rr = 0; rr < 32; rr += 2) {
+          const int r = rr + (lane >> 4), cc = lane & 15;
+          row[oW2 + (size_t)(q32 + r) * kH + 32 * wg + 16 * half + cc] = stg[r * kStg + cc];
+        }
+        __syncwarp();
       }
     }
     // per-h sums over the four warpgroups in a fixed order (in the free W2 tiles)
@@ -730,6 +759,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   }
   umma::fence_before();
   __syncthreads();
+  SILU_TRACE_K(3);
   if (tid < 32) umma::tmem_free(tm, kTmemCols);
 }
 

@@ -4,6 +4,7 @@
 // Phases: 0 top, 1 records loaded, 2 F1 done (G1 issue), 3 previous chunk's F3 done,
 // 4 G1 done, 5 F2a done, 6 per-particle done, 7 F2b done, 8 G2/G3 issued.
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <random>
 #include "../paper_2603_25832_b200/csrc/silu.cu"
@@ -13,9 +14,9 @@ void count_launch() {}
 __global__ void k_ism_reduce_cols(const double*, int, int64_t, double*) {}
 }  // namespace spic
 
-int main() {
+int main(int argc, char** argv) {
   using namespace spic;
-  const int64_t n = 1 << 20;
+  const int64_t n = argc > 1 ? atoll(argv[1]) : (1 << 20);
   const int P = (int)silu_params(kH);
   std::mt19937 g(1);
   std::normal_distribution<float> nd(0.f, 1.f);
@@ -72,6 +73,9 @@ int main() {
   double a14 = 0;
   for (int it = 4; it < 4 + cnt; ++it) a14 += h[it * 16 + 14] - (double)h[it * 16 + 12];
   if (h[4 * 16 + 14]) printf("G3 complete %.0f cycles after the issuer saw Y ready\n", a14 / cnt);
+  printf("kernel (CTA 0): prologue %lld, chunk loop %lld, epilogue %lld cycles\n",
+         h[63 * 16 + 1] - h[63 * 16 + 0], h[63 * 16 + 2] - h[63 * 16 + 1],
+         h[63 * 16 + 3] - h[63 * 16 + 2]);
   printf("from F1 hand-off: issuer X-ready %+.0f, G1 issued %+.0f, G1 done %+.0f, F2b done %+.0f,\n"
          "  issuer Y-ready %+.0f, G3+G2 issued %+.0f; next chunk's F3 got G2 %+.0f after its F1 hand-off\n",
          a10 / cnt, a11 / cnt, a4 / cnt, a7 / cnt, a12 / cnt, a13 / cnt, a9 / cnt);
