@@ -196,14 +196,15 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
                                                  const SiluInputs in, int64_t n,
                                                  float x_scale, float L,
                                                  float4* __restrict__ sw_out,
-                                                 double* __restrict__ part) {
+                                                 double* __restrict__ part,
+                                                 float* __restrict__ part_w2) {
   constexpr bool ISM = MODE != 0;  // training modes (loss + gradient partials)
   constexpr bool DIV = MODE == 1;  // divergence columns
   const float4* __restrict__ xv = in.xv;
   const float4* __restrict__ sw = in.sw;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = align1024(smem_raw);
-  static_assert(56 * 1024 + 16 * 32 * 17 * 8 <= 4 * 32768, "epilogue staging fits below X");
+  static_assert(56 * 1024 + 16 * 32 * 17 * 4 <= 4 * 32768, "epilogue staging fits below X");
   uint8_t* W2h = base;
   uint8_t* W2l = base + 1 * umma::kTileBytes;
   uint8_t* Bh = base + 2 * umma::kTileBytes;
@@ -646,10 +647,12 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       umma::fence_after();
     }
     compute_sync();  // every warpgroup is done with the X / Y tiles before they are reused
+    SILU_TRACE_K(4);
     const int64_t width = 1 + silu_params(kH);
     const int64_t oW1 = 1, ob1 = oW1 + 4 * kH, oW2 = ob1 + kH, ob2 = oW2 + kH * kH,
                   oW3 = ob2 + kH, ob3 = oW3 + 3 * kH;
     double* row = part + (size_t)blockIdx.x * width;
+    float* prow = part_w2 + (size_t)blockIdx.x * kH * kH;  // dW2 partials (float)
     // dW2 = D3 + C (.) M (row h, columns h'); warpgroup g takes columns 32g..32g+31. The
     // tangent terms of dW3 (row sums of (W2 (.) M) W1[:,1+k]) and dW1 (column sums of
     // W3[k] (W2 (.) M)) go through shared memory: WM = W2 (.) M as float [h][h'].
@@ -665,8 +668,18 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       // per-warp shared-memory transpose in two 16-column halves, so each store instruction
       // writes two 128-B row segments instead of 32 scattered doubles (free space after the
       // per-h combine area: base + 56 KB .. + 124 KB, 4352 B per warp)
-      constexpr int kStg = 17;  // padded row stride (doubles)
-      double* stg = reinterpret_cast<double*>(base + 56 * 1024) + (size_t)(tid >> 5) * 32 * kStg;
+      // this thread's W2 row segment W2[h][32g .. 32g+31] (128 B) by eight 16-B loads
+      float w2r[32];
+      if (DIV && !first) {
+        const float4* w2v = reinterpret_cast<const float4*>(W2 + h * kH + 32 * wg);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 t4 = __ldg(w2v + k);
+          w2r[4 * k] = t4.x; w2r[4 * k + 1] = t4.y; w2r[4 * k + 2] = t4.z; w2r[4 * k + 3] = t4.w;
+        }
+      }
+      constexpr int kStg = 17;  // padded row stride (floats)
+      float* stg = reinterpret_cast<float*>(base + 56 * 1024) + (size_t)(tid >> 5) * 32 * kStg;
       const int q32 = h & ~31;  // first row of this warp
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -674,11 +687,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         for (int j = 0; j < 16; ++j) {
           const int i = 16 * half + j;
           const int hp = 32 * wg + i;
-          double g = first ? 0.0 : (double)v[i];
+          float g = first ? 0.f : v[i];
           if (DIV && !first) {
             const float Chh = fmaf(w3[2], W1[hp * 4 + 3], fmaf(w3[1], W1[hp * 4 + 2], w3[0] * W1[hp * 4 + 1]));
-            const float wm = W2[h * kH + hp] * m[i];
-            g += (double)(Chh * m[i]);
+            const float wm = w2r[i] * m[i];
+            g = fmaf(Chh, m[i], g);
             WM[h * kWMs + hp] = wm;
             tw3[0] = fmaf(W1[hp * 4 + 1], wm, tw3[0]);
             tw3[1] = fmaf(W1[hp * 4 + 2], wm, tw3[1]);
@@ -692,11 +705,12 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 #pragma unroll
         for (int rr = 0; rr < 32; rr += 2) {
           const int r = rr + (lane >> 4), cc = lane & 15;
-          row[oW2 + (size_t)(q32 + r) * kH + 32 * wg + 16 * half + cc] = stg[r * kStg + cc];
+          prow[(size_t)(q32 + r) * kH + 32 * wg + 16 * half + cc] = stg[r * kStg + cc];
         }
         __syncwarp();
       }
     }
+    SILU_TRACE_K(5);
     // per-h sums over the four warpgroups in a fixed order (in the free W2 tiles)
     double* comb = reinterpret_cast<double*>(W2h);  // [4][kH][12] + [4][4]
     double* mine = comb + (size_t)(wg * kH + h) * 12;
@@ -716,6 +730,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       }
     }
     compute_sync();
+    SILU_TRACE_K(6);
     // dW1[h][1+k] tangent part: sum over rows r of W3[k][r] WM[r][h] (column h); warpgroup g
     // sums rows 32g..32g+31, the four partials are added in a fixed order below
     float* cwp = reinterpret_cast<float*>(lcomb + 16);  // [4][kH][3]
@@ -731,6 +746,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       for (int k = 0; k < 3; ++k) cwp[(wg * kH + h) * 3 + k] = cw[k];
     }
     compute_sync();
+    SILU_TRACE_K(7);
     if (wg == 0) {
       double t[12];
 #pragma unroll
@@ -853,11 +869,18 @@ using namespace spic;
 
 extern "C" int64_t spic_silu_num_params(int32_t H) { return silu_params(H); }
 
-extern "C" size_t spic_silu_scratch_bytes(int64_t n) {
-  // [blocks][1 + P] partials, the reduced row, candidate parameters, finalize sync words
+// byte offset of the float dW2 partial block inside the scratch (256-B aligned)
+static size_t silu_f32_offset(int64_t n) {
   const size_t width = 1 + (size_t)silu_params(kH);
-  return sizeof(double) * ((size_t)(silu_blocks(n) + 1) * width + (size_t)silu_params(kH)) + 64 +
-         sizeof(int32_t) * 64;
+  const size_t b = sizeof(double) * ((size_t)(silu_blocks(n) + 1) * width + (size_t)silu_params(kH)) +
+                   64 + sizeof(int32_t) * 64;
+  return (b + 255) & ~(size_t)255;
+}
+
+extern "C" size_t spic_silu_scratch_bytes(int64_t n) {
+  // [blocks][1 + P] partials, the reduced row, candidate parameters, finalize sync words,
+  // then the per-CTA dW2 partials as float [blocks][H * H] (the rows' W2 range is unused)
+  return silu_f32_offset(n) + sizeof(float) * (size_t)silu_blocks(n) * kH * kH;
 }
 
 extern "C" int64_t spic_silu_row_offset(int64_t n) {
@@ -876,8 +899,9 @@ static int silu_launch(int mode, const float* params32, int32_t H, const SiluInp
   do {                                                                                         \
     cudaFuncSetAttribute(k_silu<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                          (int)kSiluSmem);                                                      \
-    k_silu<MD><<<blocks, kNT, kSiluSmem, st>>>(params32, in, n, x_scale, L, (float4*)sw_out,   \
-                                               part);                                          \
+    k_silu<MD><<<blocks, kNT, kSiluSmem, st>>>(                                                \
+        params32, in, n, x_scale, L, (float4*)sw_out, part,                                    \
+        part ? (float*)((char*)part + silu_f32_offset(n)) : nullptr);                          \
   } while (0)
   if (mode == 0) SPIC_SILU_LAUNCH(0);
   else if (mode == 1) SPIC_SILU_LAUNCH(1);
@@ -888,12 +912,32 @@ static int silu_launch(int mode, const float* params32, int32_t H, const SiluInp
   return SPIC_OK;
 }
 
+// Deterministic column sums of the per-CTA partial rows (one warp per column, float64): the
+// dW2 columns come from the float block, the rest from the float64 rows.
+__global__ void k_silu_reduce_cols(const double* __restrict__ part, const float* __restrict__ pw2,
+                                   int rows, int64_t width, int64_t oW2, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t col = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (col >= width) return;
+  double s = 0.0;
+  if (col >= oW2 && col < oW2 + kH * kH) {
+    const int64_t c = col - oW2;
+    for (int r = lane; r < rows; r += 32) s += (double)pw2[(size_t)r * kH * kH + c];
+  } else {
+    for (int r = lane; r < rows; r += 32) s += part[(size_t)r * width + col];
+  }
+  s = warp_sum(s);
+  if (lane == 0) out[col] = s;
+}
+
 static int silu_reduce(int64_t n, void* scratch, cudaStream_t st) {
   const int rows = silu_blocks(n);
   const int64_t width = 1 + silu_params(kH);
   double* part = (double*)scratch;
-  k_ism_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(part, rows, width,
-                                                                 part + (size_t)rows * width);
+  const int64_t oW2 = 1 + 4 * kH + kH;
+  k_silu_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(
+      part, (const float*)((char*)scratch + silu_f32_offset(n)), rows, width, oW2,
+      part + (size_t)rows * width);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;

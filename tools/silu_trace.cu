@@ -76,6 +76,10 @@ int main(int argc, char** argv) {
   printf("kernel (CTA 0): prologue %lld, chunk loop %lld, epilogue %lld cycles\n",
          h[63 * 16 + 1] - h[63 * 16 + 0], h[63 * 16 + 2] - h[63 * 16 + 1],
          h[63 * 16 + 3] - h[63 * 16 + 2]);
+  printf("epilogue: G3 wait+sync %lld, tangent/dW2 rows %lld, combine %lld, dW1 tangent %lld, "
+         "final rows %lld\n", h[63 * 16 + 4] - h[63 * 16 + 2], h[63 * 16 + 5] - h[63 * 16 + 4],
+         h[63 * 16 + 6] - h[63 * 16 + 5], h[63 * 16 + 7] - h[63 * 16 + 6],
+         h[63 * 16 + 3] - h[63 * 16 + 7]);
   printf("from F1 hand-off: issuer X-ready %+.0f, G1 issued %+.0f, G1 done %+.0f, F2b done %+.0f,\n"
          "  issuer Y-ready %+.0f, G3+G2 issued %+.0f; next chunk's F3 got G2 %+.0f after its F1 hand-off\n",
          a10 / cnt, a11 / cnt, a4 / cnt, a7 / cnt, a12 / cnt, a13 / cnt, a9 / cnt);
