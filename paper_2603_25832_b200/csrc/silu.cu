@@ -224,13 +224,22 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const float* W3 = b2 + kH;
   const float* b3 = W3 + 3 * kH;
 
-  for (int e = tid; e < kH * kH; e += kNT) {
-    const int r = e / kH, cc = e % kH;  // W2[r][cc]
-    umma::store_split(W2h, W2l, r, cc, W2[e]);
+  // operand tiles, eight columns (one 16-B swizzle chunk) per step
+  for (int e8 = tid; e8 < kH * kH / 8; e8 += kNT) {
+    const int r = (e8 * 8) / kH, c0 = (e8 * 8) % kH;  // W2[r][c0 .. c0+7]
+    const float4 wa = __ldg(reinterpret_cast<const float4*>(W2 + r * kH + c0));
+    const float4 wb = __ldg(reinterpret_cast<const float4*>(W2 + r * kH + c0 + 4));
+    float w[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+    umma::store_split8(W2h, W2l, r, c0, w);
     if (DIV) {
-      const float Crc = fmaf(W3[2 * kH + r], W1[cc * 4 + 3],
-                             fmaf(W3[kH + r], W1[cc * 4 + 2], W3[r] * W1[cc * 4 + 1]));
-      umma::store_split(Bh, Bl, r, cc, W2[e] * Crc);
+      const float a0 = W3[r], a1 = W3[kH + r], a2 = W3[2 * kH + r];
+      float bv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float4 w1c = __ldg(reinterpret_cast<const float4*>(W1) + c0 + k);  // W1[c][0..3]
+        bv[k] = w[k] * fmaf(a2, w1c.w, fmaf(a1, w1c.z, a0 * w1c.y));
+      }
+      umma::store_split8(Bh, Bl, r, c0, bv);
     }
   }
   float w1[4], w3[3];

@@ -229,5 +229,22 @@ __device__ __forceinline__ void store_split(uint8_t* hi_tile, uint8_t* lo_tile, 
   *reinterpret_cast<__nv_bfloat16*>(lo_tile + o) = l;
 }
 
+// Eight consecutive columns c0..c0+7 (c0 % 8 == 0) of row r: one 16-B swizzle chunk per tile.
+__device__ __forceinline__ void store_split8(uint8_t* hi_tile, uint8_t* lo_tile, int r, int c0,
+                                             const float (&x)[8]) {
+  uint32_t hw[4], lw[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * k], x[2 * k + 1]);
+    const float2 hf = __bfloat1622float2(h2);
+    const __nv_bfloat162 l2 = __floats2bfloat162_rn(x[2 * k] - hf.x, x[2 * k + 1] - hf.y);
+    hw[k] = *reinterpret_cast<const uint32_t*>(&h2);
+    lw[k] = *reinterpret_cast<const uint32_t*>(&l2);
+  }
+  const uint32_t o = tile_off(r, c0);
+  *reinterpret_cast<uint4*>(hi_tile + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+  *reinterpret_cast<uint4*>(lo_tile + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
 }  // namespace umma
 }  // namespace spic
