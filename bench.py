@@ -360,7 +360,7 @@ def variant_line(torch, device, wl: dict, seed: int, steps: int = 3) -> dict:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     total = 0.0
     for _ in range(steps):
-        flush.zero_()
+        l2_flush(flush)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         sim.replay(1)
@@ -460,6 +460,14 @@ def config1_microbench(torch, device, n: int = 131072, reps: int = 3) -> dict:
             "momentum_rel": mom, "energy_rel": en}
 
 
+def l2_flush(buf) -> None:
+    """Evict L2 between timed regions: write a 256 MiB buffer (twice L2), then read it back so
+    the lines left in L2 are clean — otherwise the timed kernel that follows pays for writing
+    back up to 126 MB of the flush's dirty lines."""
+    buf.zero_()
+    buf.view(-1, 4096).amax(dim=1)
+
+
 def hbm_peak_gbs() -> float:
     """Measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs); the profiling recipe's fallback
     6650 GB/s only when the driver-written file is absent."""
@@ -498,7 +506,7 @@ def hbm_microbench(torch, device, peak_gbs: float, n: int = 1 << 24, M: int = 10
     def timed(fn):
         out = []
         for _ in range(reps + 1):
-            flush.zero_()
+            l2_flush(flush)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()
@@ -628,7 +636,7 @@ def main():
     evs = []
     with ClockSampler(local) as clk:
         for k in range(args.steps):
-            flush.zero_()
+            l2_flush(flush)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             if use_graph:
@@ -716,7 +724,7 @@ def main():
                    "mode": wl["mode"], "estimator": wl["estimator"], "K_ism": wl["K"],
                    "hidden": wl["hidden"], "net": NET_LABEL[wl.get("net", "softsign")],
                    "divergence": wl["divergence"], "sub_cells": sim.S,
-                   "l2": "flushed between timed steps (256 MiB write, outside timed windows)",
+                   "l2": "flushed between timed steps (256 MiB write + read-back, outside timed windows)",
                    "parallelism": ("single GPU" if world == 1 else
                         f"cell-range decomposition over {world} ranks (NCCL): migration, "
                         "halo, rho/J and ISM-gradient allreduces")},

@@ -14,9 +14,12 @@
 //       each node's partials in a fixed order and applies the field step: deterministic,
 //       no atomics (the reference uses np.bincount).
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
+#include "pairs.cuh"
 
 namespace spic {
 
@@ -147,6 +150,228 @@ __global__ void __launch_bounds__(kDepThreads) k_deposit_partials(
   if (threadIdx.x == 0)
 #pragma unroll
     for (int q = 0; q < 12; ++q) partials[(size_t)blockIdx.x * 12 + q] = a[q];
+}
+
+// One record's hat weights into the 12 slot sums of its cell c (slot s -> node c + s - 1).
+template <int DV>
+__device__ __forceinline__ void dep_accum(double (&a)[12], const float4 A, float w, double inv_eta,
+                                          double cm, int M) {
+  const double wv = (double)w;  // 0 for padding: adds nothing
+  const double g = fma((double)A.x, inv_eta, -0.5);
+  const double fl = floor(g);
+  const double w1 = wv * (g - fl), w0 = wv - w1;
+  // particle in cell c: fl is c - 1 (nodes c-1, c) or c (nodes c, c+1)
+  const bool hi = (M == 1) ? false : fl > cm;
+  const double wm = hi ? 0.0 : w0, wc = hi ? w0 : w1, wp = hi ? w1 : 0.0;
+  const double q[4] = {1.0, (double)A.y, (double)A.z, (double)A.w};
+#pragma unroll
+  for (int j = 0; j < 1 + DV; ++j) {
+    a[j] = fma(wm, q[j], a[j]);
+    a[4 + j] = fma(wc, q[j], a[4 + j]);
+    a[8 + j] = fma(wp, q[j], a[8 + j]);
+  }
+}
+
+// Deposit partials, v2: the same per-(cell, chunk) slot sums with a lighter float64 body —
+// g = x * (1/eta) - 1/2 by one DFMA (the reference divides; the hat weights are continuous in
+// g, so a 1-ulp difference moves nothing across a node), w0 = w - w1, the three node weights
+// selected once per particle — and <= 64 registers so four CTAs fit per SM. Records are
+// loaded U ahead; the chunk count gives >= 4 waves so the tail wave is short.
+template <int DV, int U, int MINB>
+__global__ void __launch_bounds__(kDepThreads, MINB) k_deposit_partials_v2(
+    const float4* __restrict__ xv, const float4* __restrict__ sw,
+    const int32_t* __restrict__ cell_start, int M, int CH, double inv_eta, float uniform_w,
+    double* __restrict__ partials) {
+  __shared__ double red[(kDepThreads / 32) * 12];
+  const int c = blockIdx.x / CH, k = blockIdx.x % CH;
+  const int cs = cell_start[c], cnt = cell_start[c + 1] - cs;
+  const int p0 = cs + (int)(((long long)cnt * k) / CH);
+  const int p1 = cs + (int)(((long long)cnt * (k + 1)) / CH);
+  const bool uni = uniform_w > 0.f;
+  const double cm = (double)c - 0.5;  // fl > c - 1/2 picks the node pair (c, c+1)
+  double a[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) a[q] = 0.0;
+  for (int pb = p0 + threadIdx.x; pb < p1; pb += U * kDepThreads) {
+    float4 AU[U];
+    float WU[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = pb + u * kDepThreads;
+      AU[u] = p < p1 ? xv[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+      WU[u] = p < p1 ? (uni ? 1.f : sw[p].w) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) dep_accum<DV>(a, AU[u], WU[u], inv_eta, cm, M);
+  }
+  if (uni)
+#pragma unroll
+    for (int q = 0; q < 12; ++q) a[q] *= (double)uniform_w;
+  block_sum<12>(a, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < 12; ++q) partials[(size_t)blockIdx.x * 12 + q] = a[q];
+}
+
+// Deposit partials, v4: the CTA's contiguous record range [p0, p1) of its (cell, chunk) unit
+// streamed into shared memory by bulk copies (cp.async.bulk + mbarrier, nstages stages of rs
+// records; the sw records alongside for per-particle weights), so each SM keeps ~190 KB of
+// reads in flight independent of the float64 arithmetic; threads then take records from
+// shared memory. Same slot sums and fixed reduction order as v2. (A persistent form that walks
+// several units per CTA with one pipeline measured 2-3x slower: ~5 us per unit start.)
+constexpr int kMaxStages = 8;
+struct BulkCfg {  // records per stage, stages, CTAs per SM (SPIC_DEP_CFG="rs,stages,ctas")
+  int rs, stages, ctas;
+};
+static BulkCfg bulk_cfg(const char* env, BulkCfg def) {
+  const char* e = getenv(env);
+  BulkCfg c = def;
+  if (e && sscanf(e, "%d,%d,%d", &c.rs, &c.stages, &c.ctas) == 3 && c.rs % 4 == 0 && c.rs > 0 &&
+      c.stages >= 1 && c.stages <= kMaxStages && c.ctas >= 1 && c.ctas <= 16)
+    return c;
+  return def;
+}
+
+static size_t dep_bulk_smem(int rs, int stages, bool nonuni) {
+  return 128 + (size_t)stages * rs * sizeof(float4) * (nonuni ? 2 : 1) +
+         kMaxStages * sizeof(uint64_t);
+}
+
+template <int DV, bool NONUNI>
+__global__ void __launch_bounds__(kDepThreads) k_deposit_bulk(
+    const float4* __restrict__ xv, const float4* __restrict__ sw,
+    const int32_t* __restrict__ cell_start, int M, int CH, double inv_eta, float uniform_w,
+    double* __restrict__ partials, int rs, int nstages) {
+  extern __shared__ unsigned char s_dyn[];
+  unsigned char* s_base = (unsigned char*)(((uintptr_t)s_dyn + 127) & ~(uintptr_t)127);
+  float4* s_x = reinterpret_cast<float4*>(s_base);                 // [stage][rs]
+  float4* s_w = s_x + (size_t)nstages * rs;                        // [stage][rs] (NONUNI)
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_x + (size_t)nstages * rs * (NONUNI ? 2 : 1));
+  __shared__ double red[(kDepThreads / 32) * 12];
+  const int c = blockIdx.x / CH, k = blockIdx.x % CH;
+  const int cs = cell_start[c], cnt = cell_start[c + 1] - cs;
+  const int p0 = cs + (int)(((long long)cnt * k) / CH);
+  const int p1 = cs + (int)(((long long)cnt * (k + 1)) / CH);
+  const int nrec = p1 - p0, nst = (nrec + rs - 1) / rs;
+  const double cm = (double)c - 0.5;
+  auto issue = [&](int q) {
+    const int st = q % nstages, b = q * rs, m = min(rs, nrec - b);
+    const uint32_t bytes = (uint32_t)m * sizeof(float4);
+    mbar_expect_tx(&s_bar[st], NONUNI ? 2 * bytes : bytes);
+    bulk_g2s(s_x + (size_t)st * rs, xv + p0 + b, bytes, &s_bar[st]);
+    if (NONUNI) bulk_g2s(s_w + (size_t)st * rs, sw + p0 + b, bytes, &s_bar[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < nstages; ++st) mbar_init(&s_bar[st], 1);
+    fence_barrier_init();
+    for (int q = 0; q < min(nst, nstages); ++q) issue(q);
+  }
+  __syncthreads();
+  double a[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) a[q] = 0.0;
+  for (int q = 0; q < nst; ++q) {
+    const int st = q % nstages, m = min(rs, nrec - q * rs);
+    mbar_wait(&s_bar[st], (uint32_t)((q / nstages) & 1));
+    const float4* X = s_x + (size_t)st * rs;
+    const float4* Wr = s_w + (size_t)st * rs;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < m; i += kDepThreads)
+      dep_accum<DV>(a, X[i], NONUNI ? Wr[i].w : 1.f, inv_eta, cm, M);
+    __syncthreads();  // stage st consumed
+    if (threadIdx.x == 0 && q + nstages < nst) {
+      fence_proxy_async();
+      issue(q + nstages);
+    }
+  }
+  if (!NONUNI)
+#pragma unroll
+    for (int q = 0; q < 12; ++q) a[q] *= (double)uniform_w;
+  block_sum<12>(a, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < 12; ++q) partials[(size_t)blockIdx.x * 12 + q] = a[q];
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Deposit partials, v5: v4 with a dedicated producer warp and per-stage "empty" mbarriers in
+// place of the CTA-wide barrier after every stage: the 8 consumer warps release a stage as
+// each finishes it (lane 0 arrives after __syncwarp), and the producer refills it as soon as
+// the last one has, so no warp waits for the slowest before taking the next stage.
+template <int DV, bool NONUNI>
+__global__ void __launch_bounds__(kDepThreads + 32) k_deposit_bulk_ws(
+    const float4* __restrict__ xv, const float4* __restrict__ sw,
+    const int32_t* __restrict__ cell_start, int M, int CH, double inv_eta, float uniform_w,
+    double* __restrict__ partials, int rs, int nstages) {
+  extern __shared__ unsigned char s_dyn[];
+  unsigned char* s_base = (unsigned char*)(((uintptr_t)s_dyn + 127) & ~(uintptr_t)127);
+  float4* s_x = reinterpret_cast<float4*>(s_base);
+  float4* s_w = s_x + (size_t)nstages * rs;
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_x + (size_t)nstages * rs * (NONUNI ? 2 : 1));
+  uint64_t* s_empty = s_full + kMaxStages;
+  __shared__ double red[(kDepThreads / 32) * 12];
+  constexpr int kCW = kDepThreads / 32;  // consumer warps
+  const int c = blockIdx.x / CH, k = blockIdx.x % CH;
+  const int cs = cell_start[c], cnt = cell_start[c + 1] - cs;
+  const int p0 = cs + (int)(((long long)cnt * k) / CH);
+  const int p1 = cs + (int)(((long long)cnt * (k + 1)) / CH);
+  const int nrec = p1 - p0, nst = (nrec + rs - 1) / rs;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < nstages; ++st) {
+      mbar_init(&s_full[st], 1);
+      mbar_init(&s_empty[st], kCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x >= kDepThreads) {  // producer warp
+    if (threadIdx.x == kDepThreads) {
+      for (int q = 0; q < nst; ++q) {
+        const int st = q % nstages;
+        if (q >= nstages) mbar_wait(&s_empty[st], (uint32_t)(((q / nstages) - 1) & 1));
+        const int b = q * rs, m = min(rs, nrec - b);
+        const uint32_t bytes = (uint32_t)m * sizeof(float4);
+        mbar_expect_tx(&s_full[st], NONUNI ? 2 * bytes : bytes);
+        bulk_g2s(s_x + (size_t)st * rs, xv + p0 + b, bytes, &s_full[st]);
+        if (NONUNI) bulk_g2s(s_w + (size_t)st * rs, sw + p0 + b, bytes, &s_full[st]);
+      }
+    }
+  } else {
+    const double cm = (double)c - 0.5;
+    double a[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) a[q] = 0.0;
+    for (int q = 0; q < nst; ++q) {
+      const int st = q % nstages, m = min(rs, nrec - q * rs);
+      mbar_wait(&s_full[st], (uint32_t)((q / nstages) & 1));
+      const float4* X = s_x + (size_t)st * rs;
+      const float4* Wr = s_w + (size_t)st * rs;
+#pragma unroll 4
+      for (int i = threadIdx.x; i < m; i += kDepThreads)
+        dep_accum<DV>(a, X[i], NONUNI ? Wr[i].w : 1.f, inv_eta, cm, M);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s_empty[st]);
+    }
+    if (!NONUNI)
+#pragma unroll
+      for (int q = 0; q < 12; ++q) a[q] *= (double)uniform_w;
+    // fixed-order reduction over the consumer warps (named barrier: the producer is not in it)
+#pragma unroll
+    for (int q = 0; q < 12; ++q) a[q] = warp_sum(a[q]);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 12; ++q) red[wid * 12 + q] = a[q];
+    asm volatile("bar.sync 1, %0;" ::"n"(kDepThreads));
+    if (threadIdx.x < 12) {
+      double t = 0.0;
+      for (int w = 0; w < kCW; ++w) t += red[w * 12 + threadIdx.x];
+      partials[(size_t)blockIdx.x * 12 + threadIdx.x] = t;
+    }
+  }
 }
 
 // Single CTA: node sums (fixed order) -> rho, J; field step; field energies.
@@ -307,8 +532,25 @@ __global__ void k_reduce_rows_pic(const double* __restrict__ part, int rows, int
   }
 }
 
-static int dep_chunks(int M) {
-  int ch = (4 * kNumSMs + M - 1) / M;  // 4x the SM count: more CTAs only grow the finalize
+
+static int dep_variant() {  // SPIC_DEP_VARIANT=1/2/3: register-streaming kernels, 4: bulk (A/B)
+  const char* e = getenv("SPIC_DEP_VARIANT");
+  return e && e[0] ? e[0] - '0' : 5;
+}
+
+// v4 (bulk copies): stage records, stages, target CTAs per SM
+static BulkCfg dep_bulk_cfg(bool nonuni) {
+  return bulk_cfg("SPIC_DEP_CFG", nonuni ? BulkCfg{512, 3, 4} : BulkCfg{1024, 3, 4});
+}
+
+static int dep_chunks(int M, int variant, int64_t n) {
+  (void)n;
+  // v1: 4x the SM count; v2/v3: >= 4 waves of their 3-4 resident CTAs per SM; v4/v5: at most
+  // ctas x SMs CTAs — few long record streams: every CTA pays a pipeline fill (measured at
+  // n = 2^24, M = 1024: 1024 CTAs 0.069 ms, 4096 CTAs 0.108 ms, whatever the wave fill)
+  const int want = variant == 1 ? 4 * kNumSMs
+                   : variant >= 4 ? dep_bulk_cfg(false).ctas * kNumSMs : 16 * kNumSMs;
+  const int ch = variant >= 4 ? want / M : (want + M - 1) / M;
   return std::max(1, std::min(ch, 1024));
 }
 
@@ -343,7 +585,8 @@ extern "C" int spic_push(float* x, float* v, int64_t ldv, int64_t n, int32_t dv,
 
 extern "C" size_t spic_deposit_scratch_bytes(int32_t M, int32_t dv) {
   (void)dv;
-  return sizeof(double) * (size_t)M * dep_chunks(M) * 12 + 64;
+  // sized for any variant / configuration (at most 1024 chunks per cell)
+  return sizeof(double) * (size_t)M * std::min(1024, std::max(16 * kNumSMs / M + 1, 64)) * 12 + 64;
 }
 
 extern "C" int spic_deposit_field(const float* xv, const float* sw, int64_t n, int32_t dv,
@@ -356,9 +599,41 @@ extern "C" int spic_deposit_field(const float* xv, const float* sw, int64_t n, i
     return SPIC_ERR_ARG;
   if (scratch_bytes < spic_deposit_scratch_bytes(M, dv)) return SPIC_ERR_SCRATCH;
   cudaStream_t st = (cudaStream_t)stream;
-  const int CH = dep_chunks(M);
+  const int var = dep_variant();
+  const int CH = dep_chunks(M, var, n);
   double* part = (double*)scratch;
-  if (dv == 3)
+  // v2: two records ahead, four CTAs/SM; v3: four ahead, three CTAs/SM; v4: bulk copies
+  if (var == 5) {
+    const bool nonuni = !(uniform_w > 0.f);
+    const BulkCfg c = dep_bulk_cfg(nonuni);
+    const size_t sm = dep_bulk_smem(c.rs, c.stages, nonuni) + kMaxStages * sizeof(uint64_t);
+    auto kern = dv == 3 ? (nonuni ? k_deposit_bulk_ws<3, true> : k_deposit_bulk_ws<3, false>)
+                        : (nonuni ? k_deposit_bulk_ws<2, true> : k_deposit_bulk_ws<2, false>);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<M * CH, kDepThreads + 32, sm, st>>>((const float4*)xv, (const float4*)sw, cell_start, M,
+                                               CH, 1.0 / eta, uniform_w, part, c.rs, c.stages);
+  } else if (var == 4) {
+    const bool nonuni = !(uniform_w > 0.f);
+    const BulkCfg c = dep_bulk_cfg(nonuni);
+    const size_t sm = dep_bulk_smem(c.rs, c.stages, nonuni);
+    auto kern = dv == 3 ? (nonuni ? k_deposit_bulk<3, true> : k_deposit_bulk<3, false>)
+                        : (nonuni ? k_deposit_bulk<2, true> : k_deposit_bulk<2, false>);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<M * CH, kDepThreads, sm, st>>>((const float4*)xv, (const float4*)sw, cell_start, M, CH,
+                                          1.0 / eta, uniform_w, part, c.rs, c.stages);
+  } else if (var == 2 && dv == 3)
+    k_deposit_partials_v2<3, 2, 4><<<M * CH, kDepThreads, 0, st>>>(
+        (const float4*)xv, (const float4*)sw, cell_start, M, CH, 1.0 / eta, uniform_w, part);
+  else if (var == 2)
+    k_deposit_partials_v2<2, 2, 4><<<M * CH, kDepThreads, 0, st>>>(
+        (const float4*)xv, (const float4*)sw, cell_start, M, CH, 1.0 / eta, uniform_w, part);
+  else if (var == 3 && dv == 3)
+    k_deposit_partials_v2<3, 4, 3><<<M * CH, kDepThreads, 0, st>>>(
+        (const float4*)xv, (const float4*)sw, cell_start, M, CH, 1.0 / eta, uniform_w, part);
+  else if (var == 3)
+    k_deposit_partials_v2<2, 4, 3><<<M * CH, kDepThreads, 0, st>>>(
+        (const float4*)xv, (const float4*)sw, cell_start, M, CH, 1.0 / eta, uniform_w, part);
+  else if (dv == 3)
     k_deposit_partials<3><<<M * CH, kDepThreads, 0, st>>>((const float4*)xv, (const float4*)sw,
                                                           cell_start, M, CH, eta, uniform_w, part);
   else

@@ -905,3 +905,87 @@ def test_pair_paths_nonuniform_weights_and_explicit_splits(spic, nsplit):
         check_field(U.double().cpu().numpy(), ref)
         sb = blob_score(p, ci, grid, 0.4).double().cpu().numpy()
         check_field(sb, O.blob_score(x, v, p.w.double().cpu().numpy(), grid.eta, M, 0.4), tol=2e-4)
+
+
+@pytest.mark.parametrize("n,M,uniform", [(4096, 1, False), (6000, 2, True), (20000, 3, False),
+                                         (1 << 18, 256, True), (1 << 18, 1024, False)])
+def test_deposit_variants_agree_with_oracle(spic, n, M, uniform):
+    """The lighter deposit partials (SPIC_DEP_VARIANT 2, 3: x * (1/eta) instead of x / eta)
+    match the original kernel and the float64 oracle deposit (ref: pic.py:43-58) to 1e-10
+    relative, for M = 1, 2, 3 (coinciding stencil nodes) and large M, with per-particle and
+    uniform weights, including particles at the cell edges and on the x -> L rounding."""
+    import os
+
+    from paper_2603_25832_b200.collision import build_cell_index
+    from paper_2603_25832_b200.pic import Grid, deposit_from_index
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    rng = np.random.default_rng(n + 7 * M)
+    L = 4 * math.pi
+    eta = L / M
+    x = rng.uniform(0, L, n).astype(np.float32)
+    x[: n // 64] = (eta * rng.integers(0, M, n // 64)).astype(np.float32)  # on cell edges
+    x[n // 64: n // 32] = np.nextafter(np.float32(L), np.float32(0))
+    v = rng.normal(size=(n, 3)).astype(np.float32)
+    w = np.full(n, L / n) if uniform else rng.uniform(0.5, 1.5, n) * (L / n)
+    grid = Grid(M, eta)
+
+    def with_env(key, val, fn):
+        old = os.environ.get(key)
+        os.environ[key] = val
+        try:
+            return fn()
+        finally:
+            if old is None:
+                os.environ.pop(key)
+            else:
+                os.environ[key] = old
+
+    p = ParticleEnsemble.from_arrays(x, v, w, device="cuda")
+    ci = build_cell_index(p, grid)
+    outs = {}
+    for val in ("1", "2", "3", "4", "5"):
+        rho, J = with_env("SPIC_DEP_VARIANT", val, lambda: deposit_from_index(ci, p, grid))
+        outs[val] = (rho.cpu().numpy(), J.cpu().numpy())
+    o_rho, o_J = O.deposit(x.astype(np.float64), v.astype(np.float64),
+                           w.astype(np.float32).astype(np.float64), eta, M)
+    for val, (rho, J) in outs.items():
+        assert relL2(rho, o_rho) <= 1e-10, (val, relL2(rho, o_rho))
+        assert relL2(J, o_J) <= 1e-10, (val, relL2(J, o_J))
+
+
+@pytest.mark.parametrize("n,M", [(4096, 1), (1 << 16, 64), (3 * 1024 + 6, 256), (1 << 20, 1024)])
+def test_push_matches_oracle_with_flags(spic, n, M):
+    """The fused push (interpolate + Lorentz + advance + wrap) against the float64 oracle
+    (ref: pic.py:61-93, state.py:14-27) on the 16-B vector path and the scalar path (n not a
+    multiple of 4), positions near 0 and L, and the non-finite velocity flag."""
+    from paper_2603_25832_b200 import _lib
+    from paper_2603_25832_b200.state import ParticleEnsemble, new_flags
+
+    rng = np.random.default_rng(n + M)
+    L = 4 * math.pi
+    eta = L / M
+    x = rng.uniform(0, L, n).astype(np.float32)
+    x[:8] = [0.0, 1e-7, L - 1e-6, np.nextafter(np.float32(L), np.float32(0)), 0.5, 1.0, 2.0, 3.0]
+    v = rng.normal(size=(n, 3)).astype(np.float32)
+    v[4, 0] = np.inf  # non-finite velocity -> flag
+    E = [rng.normal(size=M) * 0.1 for _ in range(3)]
+    Ed = [torch.as_tensor(e, device="cuda") for e in E]
+    dt = 0.05
+    p = ParticleEnsemble.from_arrays(x, v, np.full(n, L / n), device="cuda")
+    fl = new_flags("cuda")
+    _lib.call("spic_push", _lib.ptr(p.x), _lib.ptr(p.vp), n, p.vp.stride(0), 3, _lib.ptr(Ed[0]),
+              _lib.ptr(Ed[1]), _lib.ptr(Ed[2]), M, float(eta), dt, _lib.ptr(fl),
+              _lib.stream_handle())
+    torch.cuda.synchronize()
+    x2, v2, f2 = p.x.cpu().numpy(), p.vp.cpu().numpy(), fl.cpu().numpy()
+    assert f2.any()
+    ok = np.isfinite(v2).all(axis=0)
+    assert not ok[4] and ok.sum() == n - 1
+    assert np.all((x2 >= 0) & (x2 < L))
+    vfin = v.astype(np.float64)
+    vfin[4, 0] = 0.0  # the oracle raises on the non-finite position; row 4 is masked out
+    xo, vo = O.push(x.astype(np.float64), vfin, E[0], E[1], E[2], eta, M, dt)
+    d = np.abs(x2[ok] - xo[ok])
+    assert np.max(np.minimum(d, L - d)) <= 1e-5
+    assert np.max(np.abs(v2.T[ok] - vo[ok])) <= 1e-5
