@@ -25,12 +25,25 @@ namespace spic {
 
 constexpr int kDepThreads = 256;
 
+// node fields (E1, E2, B3) as floats: read from the float64 grid arrays through L1, or from a
+// float4-per-node copy in shared memory (one 16-B load per node instead of three 8-B gathers)
+struct FieldsGlobal {
+  const double* __restrict__ E1;
+  const double* __restrict__ E2;
+  const double* __restrict__ B3;
+  __device__ __forceinline__ float4 operator()(int i) const {
+    return make_float4((float)__ldg(E1 + i), (float)__ldg(E2 + i), (float)__ldg(B3 + i), 0.f);
+  }
+};
+struct FieldsShared {
+  const float4* F;
+  __device__ __forceinline__ float4 operator()(int i) const { return F[i]; }
+};
+
 // one particle of the fused interpolate + Lorentz + advance + wrap
-__device__ __forceinline__ void push_one(float& xi, float& v0, float& v1,
-                                         const double* __restrict__ E1,
-                                         const double* __restrict__ E2,
-                                         const double* __restrict__ B3, int M, float ie, float dt,
-                                         double Ld, bool& badx, bool& badv) {
+template <class Fld>
+__device__ __forceinline__ void push_one(float& xi, float& v0, float& v1, const Fld& fld, int M,
+                                         float ie, float dt, double Ld, bool& badx, bool& badv) {
   // hat weights (ref: pic.py:33-40): g = x/eta - 1/2, i0 = floor(g) mod M, i1 = i0 + 1
   const float g = fmaf(xi, ie, -0.5f);
   const float fl = floorf(g);
@@ -38,9 +51,10 @@ __device__ __forceinline__ void push_one(float& xi, float& v0, float& v1,
   int i0 = (int)fl;
   i0 = i0 < 0 ? i0 + M : (i0 >= M ? i0 - M : i0);
   const int i1 = i0 + 1 == M ? 0 : i0 + 1;
-  const float e1 = f0 * (float)__ldg(E1 + i0) + f1 * (float)__ldg(E1 + i1);
-  const float e2 = f0 * (float)__ldg(E2 + i0) + f1 * (float)__ldg(E2 + i1);
-  const float b3 = f0 * (float)__ldg(B3 + i0) + f1 * (float)__ldg(B3 + i1);
+  const float4 Fa = fld(i0), Fb = fld(i1);
+  const float e1 = f0 * Fa.x + f1 * Fb.x;
+  const float e2 = f0 * Fa.y + f1 * Fb.y;
+  const float b3 = f0 * Fa.z + f1 * Fb.z;
   // Lorentz (ref: pic.py:77-88): dv = (E1 + v2 B3, E2 - v1 B3, 0)
   const float v0n = fmaf(dt, fmaf(v1, b3, e1), v0);
   const float v1n = fmaf(dt, fmaf(-v0, b3, e2), v1);
@@ -63,39 +77,54 @@ __device__ __forceinline__ void push_one(float& xi, float& v0, float& v1,
 
 // Streaming pass over the pid-order planes x, v0, v1 (v2 is untouched by the Lorentz step
 // with B = (0, 0, B3)): 24 B moved per particle. VEC: four particles per thread through
-// 16-B loads/stores (more bytes in flight per thread), planes 16-B aligned.
-template <bool VEC>
+// 16-B loads/stores (more bytes in flight per thread), planes 16-B aligned. SMEM: the node
+// fields staged once per CTA as float4 in shared memory (M <= kPushSmemM; particles are in pid
+// order, so the per-particle node reads are scattered: three 8-B L1 gathers per node cost far
+// more LSU wavefronts than one conflict-light 16-B shared load).
+constexpr int kPushSmemM = 4096;
+template <bool VEC, bool SMEM>
 __global__ void __launch_bounds__(256) k_push(float* __restrict__ x, float* __restrict__ v,
                                               int64_t ldv, int64_t n, const double* __restrict__ E1,
                                               const double* __restrict__ E2,
                                               const double* __restrict__ B3, int M, float ie,
                                               float dt, double Ld, int32_t* flags) {
+  extern __shared__ float4 s_fld[];
   bool badx = false, badv = false;
-  if (VEC) {
-    float4* __restrict__ x4 = reinterpret_cast<float4*>(x);
-    float4* __restrict__ a4 = reinterpret_cast<float4*>(v);
-    float4* __restrict__ b4 = reinterpret_cast<float4*>(v + ldv);
-    const int64_t n4 = n >> 2;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      float4 X = x4[i], A = a4[i], B = b4[i];
-      push_one(X.x, A.x, B.x, E1, E2, B3, M, ie, dt, Ld, badx, badv);
-      push_one(X.y, A.y, B.y, E1, E2, B3, M, ie, dt, Ld, badx, badv);
-      push_one(X.z, A.z, B.z, E1, E2, B3, M, ie, dt, Ld, badx, badv);
-      push_one(X.w, A.w, B.w, E1, E2, B3, M, ie, dt, Ld, badx, badv);
-      x4[i] = X;
-      a4[i] = A;
-      b4[i] = B;
+  auto body = [&](const auto& fld) {
+    if (VEC) {
+      float4* __restrict__ x4 = reinterpret_cast<float4*>(x);
+      float4* __restrict__ a4 = reinterpret_cast<float4*>(v);
+      float4* __restrict__ b4 = reinterpret_cast<float4*>(v + ldv);
+      const int64_t n4 = n >> 2;
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+           i += (int64_t)gridDim.x * blockDim.x) {
+        float4 X = x4[i], A = a4[i], B = b4[i];
+        push_one(X.x, A.x, B.x, fld, M, ie, dt, Ld, badx, badv);
+        push_one(X.y, A.y, B.y, fld, M, ie, dt, Ld, badx, badv);
+        push_one(X.z, A.z, B.z, fld, M, ie, dt, Ld, badx, badv);
+        push_one(X.w, A.w, B.w, fld, M, ie, dt, Ld, badx, badv);
+        x4[i] = X;
+        a4[i] = A;
+        b4[i] = B;
+      }
+    } else {
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+           i += (int64_t)gridDim.x * blockDim.x) {
+        float xi = x[i], v0 = v[i], v1 = v[ldv + i];
+        push_one(xi, v0, v1, fld, M, ie, dt, Ld, badx, badv);
+        x[i] = xi;
+        v[i] = v0;
+        v[ldv + i] = v1;
+      }
     }
+  };
+  if (SMEM) {
+    for (int j = threadIdx.x; j < M; j += blockDim.x)
+      s_fld[j] = make_float4((float)E1[j], (float)E2[j], (float)B3[j], 0.f);
+    __syncthreads();
+    body(FieldsShared{s_fld});
   } else {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      float xi = x[i], v0 = v[i], v1 = v[ldv + i];
-      push_one(xi, v0, v1, E1, E2, B3, M, ie, dt, Ld, badx, badv);
-      x[i] = xi;
-      v[i] = v0;
-      v[ldv + i] = v1;
-    }
+    body(FieldsGlobal{E1, E2, B3});
   }
   if (badx) raise_flag(flags, SPIC_FLAG_NONFINITE_X);
   if (badv) raise_flag(flags, SPIC_FLAG_NONFINITE_V);
@@ -570,14 +599,25 @@ extern "C" int spic_push(float* x, float* v, int64_t ldv, int64_t n, int32_t dv,
   const bool vec = n % 4 == 0 && ldv % 4 == 0 && ((uintptr_t)x & 15) == 0 &&
                    ((uintptr_t)v & 15) == 0;
   const int64_t work = vec ? n / 4 : n;
-  const int blocks = (int)std::min<int64_t>((work + 255) / 256, kNumSMs * 8);
   (void)dv;  // the Lorentz step leaves v2 unchanged: the same kernel serves dv = 2 and 3
-  if (vec)
-    k_push<true><<<blocks, 256, 0, st>>>(x, v, ldv, n, E1, E2, B3, M, (float)(1.0 / eta), dt, Ld,
-                                         flags);
-  else
-    k_push<false><<<blocks, 256, 0, st>>>(x, v, ldv, n, E1, E2, B3, M, (float)(1.0 / eta), dt, Ld,
-                                          flags);
+  const float ie = (float)(1.0 / eta);
+  const char* pe = getenv("SPIC_PUSH_VARIANT");  // "1": fields through L1 (A/B)
+  if (M <= kPushSmemM && !(pe && pe[0] == '1')) {
+    // one resident wave: every CTA stages the fields once
+    auto kern = vec ? k_push<true, true> : k_push<false, true>;
+    const size_t sm = sizeof(float4) * (size_t)M;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, sm);
+    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)kNumSMs * std::max(occ, 1));
+    kern<<<blocks, 256, sm, st>>>(x, v, ldv, n, E1, E2, B3, M, ie, dt, Ld, flags);
+  } else {
+    const int blocks = (int)std::min<int64_t>((work + 255) / 256, kNumSMs * 8);
+    if (vec)
+      k_push<true, false><<<blocks, 256, 0, st>>>(x, v, ldv, n, E1, E2, B3, M, ie, dt, Ld, flags);
+    else
+      k_push<false, false><<<blocks, 256, 0, st>>>(x, v, ldv, n, E1, E2, B3, M, ie, dt, Ld, flags);
+  }
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;

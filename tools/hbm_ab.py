@@ -21,6 +21,33 @@ def main():
     dev = torch.device("cuda", 0)
     sweeps = [a.split("=", 1) for a in sys.argv[1:]] or [["SPIC_PUSH_VARIANT", "2"]]
     peak = bench.hbm_peak_gbs()
+    # practical ceilings at the same byte counts (torch's own vectorised elementwise kernels)
+    import statistics
+
+    n = 1 << 24
+    t = torch.zeros(3, n, device=dev)
+    u = torch.zeros(3, n, device=dev)
+    r = torch.zeros(4 * n, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def timed(fn, reps=9):
+        out = []
+        for _ in range(reps + 1):
+            bench.l2_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return statistics.median(out[1:])
+
+    for name, fn, nbytes in (("inplace_add_24B", lambda: t.add_(1.0), 24 * n),
+                             ("copy_12B_to_12B", lambda: u.copy_(t), 24 * n),
+                             ("read_16B_sum", lambda: r.sum(), 16 * n)):
+        ms = timed(fn)
+        print(json.dumps({"ceiling": name, "ms": ms, "gbs": nbytes / (ms * 1e-3) / 1e9,
+                          "frac": nbytes / (ms * 1e-3) / 1e9 / peak}), flush=True)
     for key, vals in sweeps:
         for val in vals.split("/"):
             os.environ[key] = val
