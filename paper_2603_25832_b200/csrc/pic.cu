@@ -43,11 +43,13 @@ struct FieldsShared {
 // one particle of the fused interpolate + Lorentz + advance + wrap
 template <class Fld>
 __device__ __forceinline__ void push_one(float& xi, float& v0, float& v1, const Fld& fld, int M,
-                                         float ie, float dt, double Ld, bool& badx, bool& badv) {
-  // hat weights (ref: pic.py:33-40): g = x/eta - 1/2, i0 = floor(g) mod M, i1 = i0 + 1
-  const float g = fmaf(xi, ie, -0.5f);
-  const float fl = floorf(g);
-  const float f1 = g - fl, f0 = 1.f - f1;
+                                         double ie, float dt, double Ld, bool& badx, bool& badv) {
+  // hat weights (ref: pic.py:33-40): g = x/eta - 1/2, i0 = floor(g) mod M, i1 = i0 + 1; g in
+  // float64 (one DFMA) so the weights keep full precision at large M (float32 g would carry
+  // an absolute error of ~M * 6e-8 into f1)
+  const double g = fma((double)xi, ie, -0.5);
+  const double fl = floor(g);
+  const float f1 = (float)(g - fl), f0 = 1.f - f1;
   int i0 = (int)fl;
   i0 = i0 < 0 ? i0 + M : (i0 >= M ? i0 - M : i0);
   const int i1 = i0 + 1 == M ? 0 : i0 + 1;
@@ -86,7 +88,7 @@ template <bool VEC, bool SMEM>
 __global__ void __launch_bounds__(256) k_push(float* __restrict__ x, float* __restrict__ v,
                                               int64_t ldv, int64_t n, const double* __restrict__ E1,
                                               const double* __restrict__ E2,
-                                              const double* __restrict__ B3, int M, float ie,
+                                              const double* __restrict__ B3, int M, double ie,
                                               float dt, double Ld, int32_t* flags) {
   extern __shared__ float4 s_fld[];
   bool badx = false, badv = false;
@@ -600,7 +602,7 @@ extern "C" int spic_push(float* x, float* v, int64_t ldv, int64_t n, int32_t dv,
                    ((uintptr_t)v & 15) == 0;
   const int64_t work = vec ? n / 4 : n;
   (void)dv;  // the Lorentz step leaves v2 unchanged: the same kernel serves dv = 2 and 3
-  const float ie = (float)(1.0 / eta);
+  const double ie = 1.0 / eta;
   const char* pe = getenv("SPIC_PUSH_VARIANT");  // "1": fields through L1 (A/B)
   if (M <= kPushSmemM && !(pe && pe[0] == '1')) {
     // one resident wave: every CTA stages the fields once
@@ -737,13 +739,13 @@ namespace spic {
 template <int DV>
 __global__ void k_interpolate(const float* __restrict__ x, int64_t n, const double* __restrict__ E1,
                               const double* __restrict__ E2, const double* __restrict__ B3, int M,
-                              float ie, float* __restrict__ Ep, int64_t lde,
+                              double ie, float* __restrict__ Ep, int64_t lde,
                               float* __restrict__ Bp, int64_t ldb) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float g = fmaf(x[i], ie, -0.5f);
-    const float fl = floorf(g);
-    const float f1 = g - fl, f0 = 1.f - f1;
+    const double g = fma((double)x[i], ie, -0.5);  // as in push_one
+    const double fl = floor(g);
+    const float f1 = (float)(g - fl), f0 = 1.f - f1;
     int i0 = (int)fl;
     i0 = i0 < 0 ? i0 + M : (i0 >= M ? i0 - M : i0);
     const int i1 = i0 + 1 == M ? 0 : i0 + 1;
@@ -781,10 +783,10 @@ extern "C" int spic_interpolate(const float* x, int64_t n, int32_t dv, const dou
   if (n == 0) return SPIC_OK;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
   if (dv == 3)
-    k_interpolate<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, E1, E2, B3, M, (float)(1.0 / eta),
+    k_interpolate<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, E1, E2, B3, M, 1.0 / eta,
                                                                Ep, lde, Bp, ldb);
   else
-    k_interpolate<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, E1, E2, B3, M, (float)(1.0 / eta),
+    k_interpolate<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, E1, E2, B3, M, 1.0 / eta,
                                                                Ep, lde, Bp, ldb);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();

@@ -954,11 +954,17 @@ def test_deposit_variants_agree_with_oracle(spic, n, M, uniform):
         assert relL2(J, o_J) <= 1e-10, (val, relL2(J, o_J))
 
 
-@pytest.mark.parametrize("n,M", [(4096, 1), (1 << 16, 64), (3 * 1024 + 6, 256), (1 << 20, 1024)])
-def test_push_matches_oracle_with_flags(spic, n, M):
+@pytest.mark.parametrize("n,M,l1", [(4096, 1, False), (1 << 16, 64, False), (3 * 1024 + 6, 256, False),
+                                    (1 << 20, 1024, False), (1 << 16, 8192, False),
+                                    (1 << 16, 64, True), (3 * 1024 + 6, 256, True)])
+def test_push_matches_oracle_with_flags(spic, n, M, l1, monkeypatch):
     """The fused push (interpolate + Lorentz + advance + wrap) against the float64 oracle
     (ref: pic.py:61-93, state.py:14-27) on the 16-B vector path and the scalar path (n not a
-    multiple of 4), positions near 0 and L, and the non-finite velocity flag."""
+    multiple of 4), with the node fields staged in shared memory (M <= 4096, default) and read
+    through L1 (M = 8192, or SPIC_PUSH_VARIANT=1), positions near 0 and L, and the non-finite
+    velocity flag."""
+    if l1:
+        monkeypatch.setenv("SPIC_PUSH_VARIANT", "1")
     from paper_2603_25832_b200 import _lib
     from paper_2603_25832_b200.state import ParticleEnsemble, new_flags
 
