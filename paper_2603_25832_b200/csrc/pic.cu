@@ -641,10 +641,7 @@ extern "C" int spic_deposit_field(const float* xv, const float* sw, int64_t n, i
     return SPIC_ERR_ARG;
   if (scratch_bytes < spic_deposit_scratch_bytes(M, dv)) return SPIC_ERR_SCRATCH;
   cudaStream_t st = (cudaStream_t)stream;
-  int var = dep_variant();
-  // the bulk-copy variants need 16-B aligned record arrays (cp.async.bulk); float4 records
-  // from torch / cudaMalloc always are, a caller's offset view may not be
-  if (var >= 4 && ((((uintptr_t)xv) | ((uintptr_t)sw)) & 15)) var = 3;
+  const int var = dep_variant();
   const int CH = dep_chunks(M, var, n);
   double* part = (double*)scratch;
   // v2: two records ahead, four CTAs/SM; v3: four ahead, three CTAs/SM; v4: bulk copies
