@@ -995,3 +995,46 @@ def test_push_matches_oracle_with_flags(spic, n, M, l1, monkeypatch):
     d = np.abs(x2[ok] - xo[ok])
     assert np.max(np.minimum(d, L - d)) <= 1e-5
     assert np.max(np.abs(v2.T[ok] - vo[ok])) <= 1e-5
+
+
+@pytest.mark.parametrize("M,S,L", [(64, 1, 4 * math.pi), (100, 3, 10.0), (1024, 32, 4 * math.pi),
+                                   (256, 16, 2 * math.pi / 1.25), (7, 5, 1.0)])
+@pytest.mark.parametrize("variant", ["c", "r"])
+def test_binning_keys_on_cell_and_subcell_edges(spic, M, S, L, variant, monkeypatch):
+    """Cell and sub-cell keys equal the reference's floor(x / eta) (ref: pic.py:27-30) and the
+    sub-cell floor(frac(x / eta) S) bit for bit, on float32 positions at and one or two ulps either side of every cell and
+    sub-cell edge, for power-of-two and other M, S, eta, through the counting sort and the radix
+    sort: permutation, cell_start and sub_start identical to a numpy stable argsort."""
+    from paper_2603_25832_b200.collision import build_cell_index
+    from paper_2603_25832_b200.pic import Grid
+
+    monkeypatch.setenv("SPIC_BIN_VARIANT", variant)
+    grid = Grid(M, L / M)
+    edges = (np.arange(M * S + 1, dtype=np.float64) * (grid.eta / S)).astype(np.float32)
+    xs = [edges]
+    for k in (1, 2):
+        up, dn = edges.copy(), edges.copy()
+        for _ in range(k):
+            up = np.nextafter(up, np.float32(np.inf))
+            dn = np.nextafter(dn, np.float32(-np.inf))
+        xs += [up, dn]
+    rng = np.random.default_rng(M * S)
+    x = np.concatenate(xs + [rng.uniform(0, L, 4096).astype(np.float32)])
+    x = x[(x >= 0) & (x.astype(np.float64) < L)]
+    x = rng.permutation(x).astype(np.float32)
+    n = x.size
+    p = ens(x.astype(np.float64), np.zeros((n, 3)), np.full(n, L / n))
+    ci = build_cell_index(p, grid, S=S)
+    torch.cuda.synchronize()
+    q = x.astype(np.float64) / grid.eta
+    fl = np.floor(q)
+    cell = np.minimum(fl.astype(np.int64) % M, M - 1)
+    sub = np.clip(((q - fl) * S).astype(np.int64), 0, S - 1) if S > 1 else np.zeros(n, np.int64)
+    key = cell * S + sub
+    order = np.argsort(key, kind="stable")
+    assert np.array_equal(ci.perm.cpu().numpy(), order)
+    starts = np.searchsorted(key[order], np.arange(M + 1) * S)
+    assert np.array_equal(ci.cell_start.cpu().numpy(), starts)
+    if S > 1:
+        sub_starts = np.searchsorted(key[order], np.arange(M * S + 1))
+        assert np.array_equal(ci.sub_start.cpu().numpy(), sub_starts)
