@@ -939,14 +939,47 @@ __global__ void k_silu_reduce_cols(const double* __restrict__ part, const float*
   if (lane == 0) out[col] = s;
 }
 
+// Same column sums with the rows spread over 4 thread groups per column: consecutive threads
+// take consecutive columns (each warp reads one 128/256-B row segment per load instead of 32
+// rows of one column), each group sums rows q, q + 4, ... in order and the four group sums
+// are added in a fixed order: deterministic.
+__global__ void __launch_bounds__(256) k_silu_reduce_cols4(
+    const double* __restrict__ part, const float* __restrict__ pw2, int rows, int64_t width,
+    int64_t oW2, double* __restrict__ out) {
+  __shared__ double red[4][64];
+  const int cl = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int64_t col = blockIdx.x * (int64_t)64 + cl;
+  double s = 0.0;
+  if (col < width) {
+    if (col >= oW2 && col < oW2 + kH * kH) {
+      const float* src = pw2 + (col - oW2);
+#pragma unroll 4
+      for (int r = q; r < rows; r += 4) s += (double)src[(size_t)r * kH * kH];
+    } else {
+      const double* src = part + col;
+#pragma unroll 4
+      for (int r = q; r < rows; r += 4) s += src[(size_t)r * width];
+    }
+  }
+  red[q][cl] = s;
+  __syncthreads();
+  if (q == 0 && col < width) out[col] = (red[0][cl] + red[1][cl]) + (red[2][cl] + red[3][cl]);
+}
+
 static int silu_reduce(int64_t n, void* scratch, cudaStream_t st) {
   const int rows = silu_blocks(n);
   const int64_t width = 1 + silu_params(kH);
   double* part = (double*)scratch;
   const int64_t oW2 = 1 + 4 * kH + kH;
-  k_silu_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(
-      part, (const float*)((char*)scratch + silu_f32_offset(n)), rows, width, oW2,
-      part + (size_t)rows * width);
+  const char* e = getenv("SPIC_SILU_REDUCE");  // "1": one warp per column (A/B)
+  if (e && e[0] == '1')
+    k_silu_reduce_cols<<<(unsigned)((width + 7) / 8), 256, 0, st>>>(
+        part, (const float*)((char*)scratch + silu_f32_offset(n)), rows, width, oW2,
+        part + (size_t)rows * width);
+  else
+    k_silu_reduce_cols4<<<(unsigned)((width + 63) / 64), 256, 0, st>>>(
+        part, (const float*)((char*)scratch + silu_f32_offset(n)), rows, width, oW2,
+        part + (size_t)rows * width);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   return SPIC_OK;
