@@ -1,0 +1,7 @@
+#!/bin/bash
+# bench lines of every workload (no CPU baseline) for profiles/
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for W in c0 c0ss c2ss c2blob c4ss c4blob; do
+  timeout 900 python bench.py --workload $W --no-cpu-baseline > gpurun_out/bench_$W.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$W.log
+done
