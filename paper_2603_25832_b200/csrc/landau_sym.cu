@@ -28,6 +28,18 @@
 
 namespace spic {
 
+// |minimum image of dx| for M <= 2 (ref: collision.py:62-66) from a = |dx| (|dx| < L + ulp:
+// positions lie in [0, L), quirk records at x - L): min(a, |L - a|), where L - a is exact
+// for a >= L/2 (Sterbenz) — one packed subtract instead of the rint-based fold. A NaN
+// padding record stays NaN (both operands NaN), so its weight max(NaN, 0) is still 0.
+__device__ __forceinline__ f2 minimg_abs2(f2 a, f2 L2) {
+  const f2 b = abs2(sub2(L2, a));
+  float a0, a1, b0, b1;
+  un2(a, a0, a1);
+  un2(b, b0, b1);
+  return mk2(fminf(a0, b0), fminf(a1, b1));
+}
+
 __device__ __forceinline__ bool sym_tile_cell(int c, int M, int c_lo, int c_hi, bool partial) {
   if (c >= c_lo && c < c_hi) return true;
   return partial && c == (c_lo - 1 + M) % M;
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(NT, MINB)
   }
   __syncthreads();
   const f2 W1c = mk2(wie, wie), nW2 = mk2(-wie2, -wie2);
-  const f2 invL2 = mk2(1.0f / L, 1.0f / L), negL2 = mk2(-L, -L);
+  const f2 L2 = mk2(L, L);
   int lo = 0, hi = M;  // cell of this tile
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -250,10 +262,10 @@ __global__ void __launch_bounds__(NT, MINB)
         const f2 sj0 = mk2(B.x, B.x), sj1 = mk2(B.y, B.y), sj2 = mk2(B.z, B.z);
 #pragma unroll
         for (int r = 0; r < RP; ++r) {
-          f2 dx = sub2(XA[r], xj);
-          if (MINIMG) dx = fma2(rint2(mul2(dx, invL2)), negL2, dx);
+          f2 adx = abs2(sub2(XA[r], xj));
+          if (MINIMG) adx = minimg_abs2(adx, L2);
           float ce_, co_;
-          un2(fma2(abs2(dx), nW2, W1c), ce_, co_);
+          un2(fma2(adx, nW2, W1c), ce_, co_);
           ce_ = fmaxf(ce_, 0.f);
           co_ = fmaxf(co_, 0.f);
           const f2 z0 = sub2(V0[r], vj0), z1 = sub2(V1[r], vj1), z2 = sub2(V2[r], vj2);
@@ -286,10 +298,10 @@ __global__ void __launch_bounds__(NT, MINB)
           f2 J0, J1, J2;
 #pragma unroll
           for (int r = 0; r < RP; ++r) {
-            f2 dx = sub2(XA[r], xj);
-          if (MINIMG) dx = fma2(rint2(mul2(dx, invL2)), negL2, dx);
+            f2 adx = abs2(sub2(XA[r], xj));
+            if (MINIMG) adx = minimg_abs2(adx, L2);
             float ce_, co_;
-            un2(fma2(abs2(dx), nW2, W1c), ce_, co_);
+            un2(fma2(adx, nW2, W1c), ce_, co_);
             ce_ = fmaxf(ce_, 0.f);
             co_ = fmaxf(co_, 0.f);
             const f2 z0 = sub2(V0[r], vj0), z1 = sub2(V1[r], vj1), z2 = sub2(V2[r], vj2);
