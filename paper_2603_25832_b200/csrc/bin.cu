@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "pairs.cuh"
 
 namespace spic {
 
@@ -536,6 +537,172 @@ __global__ void __launch_bounds__(kRxW * 32) k_radix_scatter_s(
   }
 }
 
+// Bulk-copy variant of the staged scatter: the tile's keys and payload arrive in shared memory
+// by cp.async.bulk (keys on one mbarrier, payload on a second, so the histogram and digit
+// scan run while the payload is still in flight); the ranking only records each tile
+// position's source index, and the write-out gathers the payload from shared memory. No
+// thread waits on a global load (the direct-load form stalls on long scoreboards: 0.78 IPC).
+// Needs 16-B aligned input ranges (the caller checks) and a tile length that is a multiple
+// of 4 records; the partial last tile falls back to plain loads.
+constexpr size_t kRxBulkSmem =
+    128 + (size_t)kRxT * (4 /*key*/ + 4 /*idx or x*/ + 16 /*rec or v0..v2 + pad*/ + 4 /*w*/) +
+    (size_t)kRxT * 2 /*src*/ + sizeof(int) * (kRxW * kRxB + 2 * kRxB + 32) + 2 * sizeof(uint64_t);
+
+template <int MODE>
+__global__ void __launch_bounds__(kRxW * 32) k_radix_scatter_b(
+    const uint32_t* __restrict__ key_in, const int32_t* __restrict__ idx_in,
+    const float4* __restrict__ rec_in, const float* __restrict__ w_in, int64_t n, int shift,
+    int mask, int n_tiles, const int32_t* __restrict__ scanned, uint32_t* __restrict__ key_out,
+    int32_t* __restrict__ idx_out, float4* __restrict__ rec_out, float* __restrict__ w_out,
+    const float* __restrict__ x, const float* __restrict__ v, int64_t ldv,
+    const float* __restrict__ w, int dv, double L) {
+  extern __shared__ unsigned char s_dyn_rb[];
+  unsigned char* sb = (unsigned char*)(((uintptr_t)s_dyn_rb + 127) & ~(uintptr_t)127);
+  uint32_t* s_key = reinterpret_cast<uint32_t*>(sb);                      // [kRxT]
+  int32_t* s_i = reinterpret_cast<int32_t*>(s_key + kRxT);                // idx (1) / x (0, 2)
+  float4* s_rec = reinterpret_cast<float4*>(s_i + kRxT);                  // rec (1)
+  float* s_pl = reinterpret_cast<float*>(s_rec);                          // v0, v1, v2 (0, 2)
+  float* s_w = reinterpret_cast<float*>(s_rec + kRxT);                    // [kRxT]
+  uint16_t* s_src = reinterpret_cast<uint16_t*>(s_w + kRxT);              // [kRxT]
+  int* hist = reinterpret_cast<int*>(s_src + kRxT);                       // [kRxW][kRxB]
+  int* s_lb = hist + kRxW * kRxB;
+  int* s_gb = s_lb + kRxB;
+  int* s_ws = s_gb + kRxB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_ws + 32);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t tbase = (int64_t)blockIdx.x * kRxT;
+  const int cnt = n - tbase < kRxT ? (int)(n - tbase) : kRxT;
+  const bool bulk = (cnt & 3) == 0;
+  if (threadIdx.x == 0 && bulk) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+    const uint32_t b4 = (uint32_t)cnt * 4;
+    mbar_expect_tx(&bar[0], b4);
+    bulk_g2s(s_key, key_in + tbase, b4, &bar[0]);
+    uint32_t tot = 0;
+    if (MODE == 1) {
+      tot = b4 + 4 * b4 + (w_in ? b4 : 0);
+      mbar_expect_tx(&bar[1], tot);
+      bulk_g2s(s_i, idx_in + tbase, b4, &bar[1]);
+      bulk_g2s(s_rec, rec_in + tbase, 4 * b4, &bar[1]);
+      if (w_in) bulk_g2s(s_w, w_in + tbase, b4, &bar[1]);
+    } else {
+      tot = b4 * (1 + 2 + (dv > 2 ? 1 : 0) + (w ? 1 : 0));
+      mbar_expect_tx(&bar[1], tot);
+      bulk_g2s(s_i, x + tbase, b4, &bar[1]);
+      bulk_g2s(s_pl, v + tbase, b4, &bar[1]);
+      bulk_g2s(s_pl + kRxT, v + ldv + tbase, b4, &bar[1]);
+      if (dv > 2) bulk_g2s(s_pl + 2 * kRxT, v + 2 * ldv + tbase, b4, &bar[1]);
+      if (w) bulk_g2s(s_w, w + tbase, b4, &bar[1]);
+    }
+  }
+  for (int k = threadIdx.x; k < kRxW * kRxB; k += blockDim.x) hist[k] = 0;
+  if (!bulk) {  // partial last tile: plain loads into the same staging
+    for (int l = threadIdx.x; l < cnt; l += blockDim.x) {
+      const int64_t i = tbase + l;
+      s_key[l] = key_in[i];
+      if (MODE == 1) {
+        s_i[l] = idx_in[i];
+        s_rec[l] = rec_in[i];
+        if (w_in) s_w[l] = w_in[i];
+      } else {
+        s_i[l] = __float_as_int(x[i]);
+        s_pl[l] = v[i];
+        s_pl[kRxT + l] = v[ldv + i];
+        if (dv > 2) s_pl[2 * kRxT + l] = v[2 * ldv + i];
+        if (w) s_w[l] = w[i];
+      }
+    }
+  }
+  __syncthreads();
+  if (bulk) mbar_wait(&bar[0], 0);
+  const int wl0 = wid * 32 * kRxG;  // this warp's first tile position
+  uint32_t kw[kRxG];
+#pragma unroll
+  for (int g = 0; g < kRxG; ++g) {
+    const int l = wl0 + g * 32 + lane;
+    kw[g] = l < cnt ? s_key[l] : 0u;
+    if (l < cnt) atomicAdd(&hist[wid * kRxB + ((kw[g] >> shift) & mask)], 1);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // blockDim.x == kRxB
+    int tot = 0;
+#pragma unroll
+    for (int q = 0; q < kRxW; ++q) tot += hist[q * kRxB + d];
+    int inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_ws[wid] = inc;
+    __syncthreads();
+    int wpre = 0;
+    for (int q = 0; q < wid; ++q) wpre += s_ws[q];
+    const int lb = wpre + inc - tot;
+    s_lb[d] = lb;
+    s_gb[d] = scanned[(size_t)d * n_tiles + blockIdx.x];
+    int run = lb;
+#pragma unroll
+    for (int q = 0; q < kRxW; ++q) {
+      const int t = hist[q * kRxB + d];
+      hist[q * kRxB + d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  int* my = hist + wid * kRxB;
+#pragma unroll
+  for (int g = 0; g < kRxG; ++g) {
+    const int l = wl0 + g * 32 + lane;
+    const bool valid = l < cnt;
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const int dg = (int)((kw[g] >> shift) & mask);
+      const unsigned peers = __match_any_sync(active, dg);
+      const int rank = __popc(peers & lanemask_lt());
+      const int basepos = my[dg];
+      __syncwarp(active);
+      if (rank == 0) my[dg] = basepos + __popc(peers);
+      s_src[basepos + rank] = (uint16_t)l;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (bulk) mbar_wait(&bar[1], 0);
+  for (int l = threadIdx.x; l < cnt; l += blockDim.x) {
+    const int src = s_src[l];
+    const uint32_t k = s_key[src];
+    const int dg = (int)((k >> shift) & mask);
+    const int pos = s_gb[dg] + (l - s_lb[dg]);
+    key_out[pos] = k;
+    float4 rec;
+    int32_t pid;
+    if (MODE == 1) {
+      pid = s_i[src];
+      rec = s_rec[src];
+    } else {
+      pid = (int32_t)(tbase + src);
+      const float xi = __int_as_float(s_i[src]);
+      rec.x = (k & 0x8000u) ? (float)((double)xi - L) : xi;
+      rec.y = s_pl[src];
+      rec.z = s_pl[kRxT + src];
+      rec.w = dv > 2 ? s_pl[2 * kRxT + src] : 0.f;
+    }
+    const bool has_w = MODE == 1 ? (w_in != nullptr) : (w != nullptr);
+    const float wv = has_w ? s_w[src] : 0.f;
+    if (idx_out) idx_out[pos] = pid;
+    if (rec_out) rec_out[pos] = rec;
+    if (MODE == 0) {
+      if (w_out) w_out[pos] = wv;
+    } else if (w_out) {
+      reinterpret_cast<float4*>(w_out)[pos] = make_float4(0.f, 0.f, 0.f, wv);
+    }
+  }
+}
+
 // cell_start / sub_start from the sorted key words: position k starts every key in
 // (key[k-1], key[k]] (key[-1] = -1, key[n] = K)
 __global__ void k_radix_starts(const uint32_t* __restrict__ key_sorted, int64_t n, int M, int S,
@@ -636,17 +803,27 @@ static int bin_radix(const float* x, const float* v, int64_t ldv, const float* w
     k_scan_apply<<<(unsigned)r.nb_scan, kScanThreads, 0, st>>>(counts, r.counts_elems, bsum);
     for (int k = 0; k < 3; ++k) spic::count_launch();
   };
-  const char* se = getenv("SPIC_RADIX_STAGED");  // "0": the direct-scatter kernels (A/B)
+  // "0": the direct-scatter kernels, "1": staged with plain loads, default: staged with bulk
+  // copies when the input planes are 16-B aligned (A/B)
+  const char* se = getenv("SPIC_RADIX_STAGED");
+  const bool aligned = ((((uintptr_t)x) | ((uintptr_t)v) | ((uintptr_t)w)) & 15) == 0 &&
+                       (ldv & 3) == 0;
+  const bool bulkrx = !(se && (se[0] == '0' || se[0] == '1')) && aligned;
   const bool staged = !(se && se[0] == '0');
   if (staged) {
     cudaFuncSetAttribute(k_radix_scatter_s<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRxStagedSmem);
     cudaFuncSetAttribute(k_radix_scatter_s<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRxStagedSmem);
     cudaFuncSetAttribute(k_radix_scatter_s<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRxStagedSmem);
   }
-  const size_t ssm = staged ? kRxStagedSmem : 0;
-  auto sc0 = staged ? k_radix_scatter_s<0> : k_radix_scatter<0>;
-  auto sc1 = staged ? k_radix_scatter_s<1> : k_radix_scatter<1>;
-  auto sc2 = staged ? k_radix_scatter_s<2> : k_radix_scatter<2>;
+  if (bulkrx) {
+    cudaFuncSetAttribute(k_radix_scatter_b<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRxBulkSmem);
+    cudaFuncSetAttribute(k_radix_scatter_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRxBulkSmem);
+    cudaFuncSetAttribute(k_radix_scatter_b<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRxBulkSmem);
+  }
+  const size_t ssm = bulkrx ? kRxBulkSmem : (staged ? kRxStagedSmem : 0);
+  auto sc0 = bulkrx ? k_radix_scatter_b<0> : (staged ? k_radix_scatter_s<0> : k_radix_scatter<0>);
+  auto sc1 = bulkrx ? k_radix_scatter_b<1> : (staged ? k_radix_scatter_s<1> : k_radix_scatter<1>);
+  auto sc2 = bulkrx ? k_radix_scatter_b<2> : (staged ? k_radix_scatter_s<2> : k_radix_scatter<2>);
   const int lo_bits = r.passes == 1 ? r.bits : 8;
   const int mask0 = (1 << lo_bits) - 1;
   k_radix_count<true><<<nt, 256, 0, st>>>(x, nullptr, key0, n, eta, M, S, 0, mask0, r.n_tiles,
