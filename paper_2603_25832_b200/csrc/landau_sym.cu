@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(NT, MINB)
                  const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
                  const int32_t* __restrict__ tile_start, const SymMeta* __restrict__ meta,
                  const int64_t* __restrict__ off, const int32_t* __restrict__ symflag, int M,
-                 int S, float L, float wie, float wie2, int nsplit, float* __restrict__ Upart,
+                 int S, float L, float wie, float wie2, int nsplit, int split_fast,
+                 float* __restrict__ Upart,
                  float* __restrict__ Jslot, int64_t n) {
   constexpr int TI = NT * 2 * RP;
   constexpr int NW = NT / 32;
@@ -174,7 +175,10 @@ __global__ void __launch_bounds__(NT, MINB)
   auto s_jp = reinterpret_cast<float(*)[NW][kSymTJ * 3]>(s_base + sizeof(float4) * kSymStages * 2 * kSymTJ);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_base + sizeof(float4) * kSymStages * 2 * kSymTJ +
                                                 sizeof(float) * 2 * NW * kSymTJ * 3);
-  const int tile = blockIdx.x, split = blockIdx.y;
+  // split_fast: grid (nsplit, tiles) — a tile's j-splits are dispatched together, tiles in
+  // order, so the long windows (first tiles of a cell) start before the short ones
+  const int tile = split_fast ? blockIdx.y : blockIdx.x;
+  const int split = split_fast ? blockIdx.x : blockIdx.y;
   if (tile >= tile_start[M]) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // zero the stage buffers once (padding records beyond a stage's count must be finite)
@@ -434,7 +438,8 @@ size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit) {
 template <int NT, int RP, int MINB, bool MINIMG>
 static void launch_sym(dim3 grid, cudaStream_t st, const float* xv, const float* sw,
                        const int32_t* cell_start, const int32_t* ssp, const SymScratch& s, int M,
-                       int S, float L, float wie, float wie2, int nsplit, int64_t n) {
+                       int S, float L, float wie, float wie2, int nsplit, int split_fast,
+                       int64_t n) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_landau_sym<NT, RP, MINB, MINIMG>,
@@ -443,7 +448,7 @@ static void launch_sym(dim3 grid, cudaStream_t st, const float* xv, const float*
   }
   k_landau_sym<NT, RP, MINB, MINIMG><<<grid, NT, sym_smem_bytes(NT), st>>>(
       (const float4*)xv, (const float4*)sw, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag,
-      M, S, L, wie, wie2, nsplit, s.Upart, s.Jslot, n);
+      M, S, L, wie, wie2, nsplit, split_fast, s.Upart, s.Jslot, n);
 }
 
 int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32_t* cell_start,
@@ -465,21 +470,25 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
   SPIC_CHECK_LAUNCH();
   const bool partial = (c_hi - c_lo) < M;
   const int64_t ncells = (c_hi - c_lo) + (partial ? 1 : 0);
-  dim3 grid((unsigned)(n / TI + ncells + 1), (unsigned)nsplit);
+  const int64_t ntile_grid = n / TI + ncells + 1;
+  const char* sf = getenv("SPIC_SYM_ORDER");  // "t": tile-fastest grid (A/B)
+  const int split_fast = (ntile_grid <= 65535 && !(sf && sf[0] == 't')) ? 1 : 0;
+  dim3 grid = split_fast ? dim3((unsigned)nsplit, (unsigned)ntile_grid)
+                         : dim3((unsigned)ntile_grid, (unsigned)nsplit);
   const int32_t* ssp = (S > 1 && M >= 3) ? sub_start : nullptr;
   const float Lf = (float)L;
   if (M <= 2)
-    launch_sym<128, 2, 4, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+    launch_sym<128, 2, 4, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.nt == 256)
-    launch_sym<256, 2, 2, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+    launch_sym<256, 2, 2, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.rp == 3 && cfg.minb == 3)
-    launch_sym<128, 3, 3, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+    launch_sym<128, 3, 3, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.rp == 3)
-    launch_sym<128, 3, 2, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+    launch_sym<128, 3, 2, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.minb == 3)
-    launch_sym<128, 2, 3, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+    launch_sym<128, 2, 3, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else
-    launch_sym<128, 2, 4, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, n);
+    launch_sym<128, 2, 4, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
