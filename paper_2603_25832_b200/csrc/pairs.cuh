@@ -3,6 +3,8 @@
 // culled to the sub-cells within eta of the tile), the per-cell target-tile table, and the
 // bulk-copy (cp.async.bulk + mbarrier) helpers that stream j-records into shared memory.
 #pragma once
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace spic {
@@ -194,7 +196,15 @@ static inline int pair_nsplit_slots(int64_t n, int M, int TI, int resident) {
   const double tiles = (double)(n / TI) + 0.5 * M > 1.0 ? (double)(n / TI) + 0.5 * M : 1.0;
   const double slots = (double)resident;
   const int64_t window = 2 * n / (M > 1 ? M : 1);  // records in a culled j-window (approx.)
-  int cap = (int)(window / 1024);
+  // at least min_split j-records per split (SPIC_PAIR_MIN_SPLIT, A/B): 128 lets small cells
+  // (config 0: ~2k-record windows) split far enough to fill the SMs (c0 pair 0.241 -> 0.172 ms
+  // against 1024); windows of the larger configs hit the 16-split cap either way
+  static const int min_split = [] {
+    const char* e = getenv("SPIC_PAIR_MIN_SPLIT");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 128;
+  }();
+  int cap = (int)(window / min_split);
   cap = cap < 1 ? 1 : (cap > 16 ? 16 : cap);
   int best = 1;
   double best_eff = -1.0;
