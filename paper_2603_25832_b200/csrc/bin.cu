@@ -757,14 +757,15 @@ extern "C" int spic_cell_of(const float* x, int64_t n, double eta, int32_t M, in
   return SPIC_OK;
 }
 
-// Path choice: the radix path wins from ~2^21 records (c3: 0.81 -> 0.51 ms, n = 2^24:
-// 5.15 -> 1.93 ms); below that its 11 launches cost more than the single-pass sort saves
-// (equal at 2^20, 0.051 vs 0.074 ms at 2^16). SPIC_BIN_VARIANT=c / r forces a path (A/B tests).
+// Path choice: the radix path (bulk-staged scatters) wins from ~2^20 records (2^20: 0.124 vs
+// 0.138 ms, 2^22: 0.26 vs 0.81 ms, 2^24: 0.86 vs 5.15 ms); below that its 11 launches cost
+// more than the single-pass sort saves (0.070 vs 0.050 ms at 2^16). SPIC_BIN_VARIANT=c / r
+// forces a path (A/B tests).
 static bool bin_use_counting(int64_t n) {
   const char* e = getenv("SPIC_BIN_VARIANT");
   if (e && e[0] == 'c') return true;
   if (e && e[0] == 'r') return false;
-  return n < ((int64_t)1 << 21);
+  return n < ((int64_t)1 << 20);
 }
 
 static size_t radix_scratch_bytes(int64_t n, int32_t M, int32_t S) {
