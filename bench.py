@@ -565,6 +565,18 @@ def build_dist_sim(wl: dict, seed: int, device, world: int):
     return sim
 
 
+def live_pairs(sim, dist_mode: bool) -> float:
+    """Ordered live pairs (|dx| < eta) of this rank's pair kernel. Decomposed runs count the
+    rank's own particles only (pairs with the halo cells left out: a slight undercount)."""
+    from paper_2603_25832_b200.collision import count_live_pairs
+
+    if not dist_mode:
+        return float(count_live_pairs(sim.ci, sim.p, sim.grid))
+    if getattr(sim, "ci_own", None) is None:
+        return 0.0
+    return float(count_live_pairs(sim.ci_own, sim.buf.view(sim.n_own, sim.uniform_w), sim.grid))
+
+
 def main():
     args = parse_args()
     wl = WORKLOADS[args.workload]
@@ -598,20 +610,26 @@ def main():
     import torch
 
     from paper_2603_25832_b200 import _lib
-    from paper_2603_25832_b200.collision import count_live_pairs
-
+    
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # SPIC_FORCE_DIST=1: the decomposed (NCCL) path even at one rank — a one-GPU check of the
+    # multi-GPU bench path (process group, DistSimulation, max-over-ranks timing)
+    dist_mode = world > 1 or os.environ.get("SPIC_FORCE_DIST") == "1"
+    if dist_mode:
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     _lib.load(build_if_missing=False)
 
     # N = 1: the single-GPU engine. N > 1: the cell-range decomposition of a weak-scaled
     # problem (N x particles, cells and domain length) over NCCL.
-    sim = build_dist_sim(wl, args.seed, device, world) if world > 1 else build_sim(wl, args.seed, device)
+    sim = build_dist_sim(wl, args.seed, device, world) if dist_mode else build_sim(wl, args.seed, device)
     n = wl["n"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
 
@@ -621,10 +639,10 @@ def main():
     sim.check()
     # the timed steps replay a CUDA graph of the step (one launch per step; the eager path is
     # identical kernel for kernel, see tests/test_gpu_parity.py::test_cuda_graph_replay_*)
-    use_graph = world == 1 and not os.environ.get("SPIC_NO_GRAPH")
+    use_graph = not dist_mode and not os.environ.get("SPIC_NO_GRAPH")
     if use_graph:
         sim.capture(row=3)
-    live0 = count_live_pairs(sim.ci, sim.p, sim.grid) if world == 1 else 0
+    live0 = live_pairs(sim, dist_mode)
     peak = fp32_peak_tflops(torch, _lib)
 
     if dist:
@@ -661,7 +679,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     coll_ms = [a.elapsed_time(b) for a, b in sim.collision_events]
-    live1 = count_live_pairs(sim.ci, sim.p, sim.grid) if world == 1 else 0
+    live1 = live_pairs(sim, dist_mode)
     live = 0.5 * (live0 + live1)
     t = torch.tensor([total_ms, statistics.mean(coll_ms) if coll_ms else float("nan")],
                      dtype=torch.float64, device=device)
@@ -673,7 +691,7 @@ def main():
 
     # end to end through the public host-buffer API
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not dist_mode:
         dv = sim.p.dv
         xh = torch.empty(n, dtype=torch.float32).pin_memory()
         vh = torch.empty(dv, n, dtype=torch.float32).pin_memory()
@@ -698,6 +716,39 @@ def main():
                "h2d_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4),
                "d2h_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4 + dh.numel() * 8)}
         sim.check()
+    elif not args.no_e2e:
+        # decomposed engine: each rank's particles through DistSimulation.step_host (pinned
+        # host buffers sized with headroom for migration), max over ranks
+        try:
+            dv = sim.dv
+            cap = int(1.5 * sim.n) + 1024
+            xh = torch.empty(cap, dtype=torch.float32).pin_memory()
+            vh = torch.empty(dv, cap, dtype=torch.float32).pin_memory()
+            dh = torch.empty(sim.diag.shape[1], dtype=torch.float64).pin_memory()
+            n0 = sim.n
+            xh[:n0].copy_(sim.buf.x[:n0])
+            vh[:, :n0].copy_(sim.buf.vp[:, :n0])
+            torch.cuda.synchronize()
+            sim.step_host(2, xh, vh, dh)  # warm
+            torch.cuda.synchronize()
+            dist.barrier()
+            counts = []
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                counts.append(sim.step_host(2, xh, vh, dh))
+            e1.record()
+            e1.synchronize()
+            te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            nb = int(statistics.mean(counts)) * 4 * (1 + dv)
+            e2e = {"value": world * n * args.steps / (float(te[0]) * 1e-3),
+                   "unit": "particle-steps/s", "h2d_bytes_per_step": nb,
+                   "d2h_bytes_per_step": nb + dh.numel() * 8,
+                   "note": "per rank: its own particles in and out every step (rank 0's bytes)"}
+            sim.check()
+        except Exception as exc:  # noqa: BLE001
+            e2e = {"error": str(exc)}
 
     flop_launch = pair_flops(live, n)
     achieved = flop_launch / (coll_avg_ms * 1e-3) / 1e12
@@ -725,7 +776,7 @@ def main():
                    "hidden": wl["hidden"], "net": NET_LABEL[wl.get("net", "softsign")],
                    "divergence": wl["divergence"], "sub_cells": sim.S,
                    "l2": "flushed between timed steps (256 MiB write + read-back, outside timed windows)",
-                   "parallelism": ("single GPU" if world == 1 else
+                   "parallelism": ("single GPU" if not dist_mode else
                         f"cell-range decomposition over {world} ranks (NCCL): migration, "
                         "halo, rho/J and ISM-gradient allreduces")},
         "pair_interactions_per_s": world * live / (coll_avg_ms * 1e-3),

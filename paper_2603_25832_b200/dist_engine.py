@@ -156,6 +156,7 @@ class DistSimulation:
         p_own = self.buf.view(n, self.uniform_w)
         # 3. bin own particles, deposit, allreduce the grid moments, field step
         ci = self._bin(n)
+        self.ci_own, self.n_own = ci, n  # own particles only (bench: live-pair count)
         deposit_from_index(ci, p_own, g, fields=FieldState(f.E1, f.E2, f.B3, self.rho, self.J,
                                                            f.rho_ion),
                            field_mode=FIELD_NONE, flags=self.flags)
@@ -239,6 +240,26 @@ class DistSimulation:
         comm.allreduce_(d[3:8])
 
     # ---- host reads -------------------------------------------------------------------------
+    def step_host(self, row: int, x_host: torch.Tensor, v_host: torch.Tensor,
+                  diag_host: torch.Tensor) -> int:
+        """End-to-end step of this rank on HOST buffers (pinned float32 x (cap,), v planes
+        (dv, cap), float64 diag (DIAG_W,), cap >= the rank's particle count): H2D of the rank's
+        current particles, one decomposed step, D2H of its particles after the step (their
+        count changes with migration) and of the step's diagnostics row. Returns the count."""
+        n = self.n
+        if x_host.shape[0] < n or v_host.shape[1] < n:
+            raise ValueError("host buffers smaller than the rank's particle count")
+        self.buf.x[:n].copy_(x_host[:n], non_blocking=True)
+        self.buf.vp[:, :n].copy_(v_host[:, :n], non_blocking=True)
+        self.step(row)
+        n = self.n
+        if x_host.shape[0] < n or v_host.shape[1] < n:
+            raise ValueError("host buffers smaller than the rank's particle count")
+        x_host[:n].copy_(self.buf.x[:n], non_blocking=True)
+        v_host[:, :n].copy_(self.buf.vp[:, :n], non_blocking=True)
+        diag_host.copy_(self.diag[row], non_blocking=True)
+        return n
+
     def check(self) -> None:
         fl = self.flags.clone()
         if self.comm.size > 1:

@@ -463,6 +463,28 @@ def test_dist_engine_single_rank_matches_engine(spic, estimator):
     gid, x2, v2 = s2.gather_state()
     np.testing.assert_allclose(x2, p1.x.double().cpu().numpy()[gid], rtol=0, atol=1e-6)
     np.testing.assert_allclose(v2, p1.v.double().cpu().numpy()[gid], rtol=1e-6, atol=1e-6)
+    # the decomposed engine's host-buffer step (bench e2e at N > 1) equals its device step
+    s4, _ = make("dist")
+    cap = s4.n + 1024
+    xh = torch.empty(cap, dtype=torch.float32).pin_memory()
+    vh = torch.empty(3, cap, dtype=torch.float32).pin_memory()
+    dh = torch.empty(s4.diag.shape[1], dtype=torch.float64).pin_memory()
+    for k in range(1, 4):
+        s4.step(k)
+    n4 = s4.n
+    xh[:n4].copy_(s4.buf.x[:n4])
+    vh[:, :n4].copy_(s4.buf.vp[:, :n4])
+    s5, _ = make("dist")
+    for k in range(1, 4):
+        s5.step(k)
+    s5.step(4)
+    s4.step_host(4, xh, vh, dh)
+    torch.cuda.synchronize()
+    n5 = s5.n
+    assert s4.n == n5
+    assert np.array_equal(xh[:n5].numpy(), s5.buf.x[:n5].cpu().numpy())
+    assert np.array_equal(vh[:, :n5].numpy(), s5.buf.vp[:, :n5].cpu().numpy())
+    assert np.array_equal(dh.numpy(), s5.diag[4].cpu().numpy())
 
 
 # ---------------------------------------------------------------------------- run() end to end
