@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(NT, MINB)
                const int32_t* __restrict__ sub_start, const int32_t* __restrict__ tile_start,
                const SymMeta* __restrict__ meta, const int64_t* __restrict__ off,
                const int32_t* __restrict__ symflag, int M, int S, float L, float wie, float wie2,
-               const float* __restrict__ h_cell, float h_fixed, int nsplit,
+               const float* __restrict__ h_cell, float h_fixed, int nsplit, int split_fast,
                float* __restrict__ Upart, float* __restrict__ Jslot, int64_t n) {
   constexpr int TI = NT * 2 * RP;
   constexpr int NW = NT / 32;
@@ -36,7 +36,9 @@ __global__ void __launch_bounds__(NT, MINB)
   auto s_jp = reinterpret_cast<float(*)[NW][kSymTJ * NC]>(s_base + sizeof(float4) * kSymStages * kSymTJ);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_base + sizeof(float4) * kSymStages * kSymTJ +
                                                 sizeof(float) * 2 * NW * kSymTJ * NC);
-  const int tile = blockIdx.x, split = blockIdx.y;
+  // split_fast: grid (nsplit, tiles), a tile's j-splits dispatched together (as k_landau_sym)
+  const int tile = split_fast ? blockIdx.y : blockIdx.x;
+  const int split = split_fast ? blockIdx.x : blockIdx.y;
   if (tile >= tile_start[M]) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < kSymStages * kSymTJ; k += NT)
@@ -317,7 +319,11 @@ int spic_blob_sym_run(const float4* xv, float4* sw, const int32_t* perm, int64_t
                                   s.meta, s.off, s.flag);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
-  dim3 grid((unsigned)(n / kBlobSymTI + M + 1), (unsigned)nsplit);
+  const int64_t ntile_grid = n / kBlobSymTI + M + 1;
+  const char* sf = getenv("SPIC_SYM_ORDER");  // "t": tile-fastest grid (A/B)
+  const int split_fast = (ntile_grid <= 65535 && !(sf && sf[0] == 't')) ? 1 : 0;
+  dim3 grid = split_fast ? dim3((unsigned)nsplit, (unsigned)ntile_grid)
+                         : dim3((unsigned)ntile_grid, (unsigned)nsplit);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_blob_sym<kBlobSymNT, kBlobSymRP, kBlobSymMinB, false>,
@@ -330,7 +336,7 @@ int spic_blob_sym_run(const float4* xv, float4* sw, const int32_t* perm, int64_t
   k_blob_sym<kBlobSymNT, kBlobSymRP, kBlobSymMinB, MI_><<<grid, kBlobSymNT, blob_sym_smem_bytes(), \
                                                           st>>>(                                 \
       xv, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag, M, S, (float)L, wie, wie2, h_cell, \
-      h_fixed, nsplit, s.Upart, s.Jslot, n)
+      h_fixed, nsplit, split_fast, s.Upart, s.Jslot, n)
   if (M <= 2)
     SPIC_BLOBSYM(true);
   else
