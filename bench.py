@@ -1,24 +1,29 @@
 #!/usr/bin/env python
 """Benchmark of the B200 per-timestep hot path (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4] [--impl ours|reference]
 
-Workload (default c2 = BASELINE config 2): two-stream 1D3V, SBTM, n = 2^20 particles,
-M = 128 cells on L = 10 pi, nu = 0.05, dt = 0.05, K = 10 ISM steps per time step, exact
-divergence, H = 128 (reference softsign architecture), Adam lr 1e-3 (AdamW, wd = 0).
+Workload (default c4 = BASELINE config 4, the largest single-GPU configuration): Landau
+damping 1D3V, SBTM, n = 2^24 particles, M = 1024 cells on L = 4 pi, nu = 0.1, dt = 0.05,
+K = 10 exact-divergence ISM steps per time step with BASELINE's score MLP
+"(x, v) -> 2x128 SiLU -> R^3" (tcgen05 hidden GEMMs), Adam lr 1e-3 (AdamW, wd = 0).
 A step is one full Algorithm-1 step (push, bin, deposit + field, K ISM steps, score, Landau
 collision + push, diagnostics) over the synthetic ensemble (seeded sampler, random-init net).
+The same line carries config 3 (Weibel, full Maxwell VML, n = 2^22) as `config3_vml` and
+config 4 with the reference's own softsign network as `reference_net_variant`.
 
   value  = particle-steps/s, device-timed with CUDA events per step (L2 flushed between
            timed steps by a 256 MiB write outside the timed windows), max over ranks.
+           N > 1: strong scaling — the same n = 2^24 particles split by cell range.
   e2e    = same metric through Simulation.step_host with pinned HOST buffers: H2D of x, v,
-           the step, D2H of x, v and the diagnostics row, every step.
-  roofline: dominant kernel = the Landau pair kernel (spic_landau), 38 FLOP per ordered
-           live pair (|dx| < eta), against the FP32 peak measured in-run by spic_fp32_probe.
+           the step, D2H of x, v, the diagnostics row and the error flags, and the flag check
+           run() does, every step.
+  roofline: the kernel with the largest share of the step (the Landau pair kernel at c4)
+           against the FP32 peak measured in-run by spic_fp32_probe.
   cpu_baseline: the float64 oracle port (oracle/, C + OpenMP) on a bounded sample of the same
            workload, rank 0, N = 1 only.
 `--impl reference` times that CPU port alone (the reference arm; the reference itself is pure
-Python + numba and is not shipped to the GPU box).
+Python + numba and is not shipped to the GPU box), on the same config dict.
 """
 
 from __future__ import annotations
@@ -101,7 +106,7 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -123,11 +128,27 @@ def make_config(wl: dict, seed: int):
 # CPU baseline: the oracle port on a bounded sample
 # ------------------------------------------------------------------------------------------
 
-def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_stride: int = 16,
-                    seed: int = 0):
-    """Seconds for one full step of the workload on the host cores, measured on a bounded
-    sample: push/deposit/field/bin/forward on all n; K ISM steps on n/ism_sub particles
-    (x ism_sub); the pair kernel on every cell_stride-th cell (x cell_stride)."""
+def cpu_sample_plan(wl: dict) -> dict:
+    """Bounded CPU sample of one step of the workload (about 10-30 s on 16 host cores):
+    the pair kernels on every `cell_stride`-th cell (about 1.3e10 stencil pairs), the SiLU ISM
+    on `ism_particles` particles (numpy float64), the softsign ISM on up to 65 536; everything
+    else (push, deposit, field, bin, softsign forward) on all n. Each sampled stage is scaled
+    up by its factor."""
+    n, M = wl["n"], wl["M"]
+    stencil_pairs = 3.0 * n * n / M if M >= 3 else float(n) * n
+    cell_stride = int(max(1, min(M, round(stencil_pairs / 1.3e10))))
+    if wl.get("net") == "silu":
+        ism = min(n, 16384)
+        fwd_stride = max(1, n // (1 << 18))
+    else:
+        ism = min(n, 65536)
+        fwd_stride = 1
+    return {"cell_stride": cell_stride, "ism_particles": ism, "forward_stride": fwd_stride}
+
+
+def cpu_sample_step(wl: dict, host_state: dict, plan: dict, *, seed: int = 0):
+    """Seconds for one full step of the workload on the host cores, measured on the bounded
+    sample of cpu_sample_plan() and scaled up stage by stage."""
     from oracle import oracle as O
 
     x, v, w = host_state["x"], host_state["v"], host_state["w"]
@@ -135,6 +156,7 @@ def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_strid
     M, L = wl["M"], wl["L"]
     eta = L / M
     n = x.shape[0]
+    cell_stride = plan["cell_stride"]
     t = {}
     t0 = time.perf_counter()
     x1, v1 = O.push(x, v, E1, E2, B3, eta, M, wl["dt"])
@@ -143,11 +165,12 @@ def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_strid
     O.build_cell_index(x1, eta, M)
     t["push_deposit_field_bin"] = time.perf_counter() - t0
     rng = np.random.default_rng(seed)
+    sub = np.sort(rng.choice(n, size=plan["ism_particles"], replace=False)) \
+        if plan["ism_particles"] < n else np.arange(n)
     if wl["estimator"] == "sbtm" and wl.get("net") == "silu":
         from oracle import silu_oracle as SO
 
         params = SO.glorot(128, rng)
-        sub = rng.choice(n, size=max(1, n // (4 * ism_sub)), replace=False)
         u = SO.inputs(x1[sub], v1[sub], L)
         m, v2 = np.zeros_like(params), np.zeros_like(params)
         t0 = time.perf_counter()
@@ -157,13 +180,12 @@ def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_strid
                                           weight_decay=wl["weight_decay"])
         t["ism"] = (time.perf_counter() - t0) * (n / len(sub))
         t0 = time.perf_counter()
-        fsub = np.arange(0, n, ism_sub)
+        fsub = np.arange(0, n, plan["forward_stride"])
         s = np.zeros_like(v1)
         s[fsub] = SO.forward(params, SO.inputs(x1[fsub], v1[fsub], L), 128, with_div=False)[0]
         t["forward"] = (time.perf_counter() - t0) * (n / len(fsub))
     elif wl["estimator"] == "sbtm":
         net = O.Net.glorot(v.shape[1], wl["hidden"], rng)
-        sub = rng.choice(n, size=max(1, n // ism_sub), replace=False)
         opt = O.AdamW(lr=wl["lr"], weight_decay=wl["weight_decay"])
         t0 = time.perf_counter()
         O.sbtm_update(net, opt, x1[sub], v1[sub], w[sub], wl["K"], L=L, divergence=wl["divergence"])
@@ -181,9 +203,27 @@ def cpu_sample_step(wl: dict, host_state: dict, *, ism_sub: int = 16, cell_strid
     return sum(t.values()), t
 
 
+_SAMPLE_CACHE: dict = {}
+
+
 def sample_workload(wl: dict, cfg, rng):
     """Initial particles of a workload: the reference's preset sampler, or BASELINE config 3's
-    anisotropic Maxwellian; plus the seeded B3 noise (None unless the workload has one)."""
+    anisotropic Maxwellian; plus the seeded B3 noise (None unless the workload has one).
+    Memoised per (workload sampling parameters, seed): a variant line of the same config (e.g.
+    the softsign network) reuses the ensemble and continues from the same rng state."""
+    key = (wl["preset"], wl["n"], wl["M"], wl["L"], wl.get("sampler"), wl.get("b3_noise"),
+           cfg.seed)
+    hit = _SAMPLE_CACHE.get(key)
+    if hit is not None:
+        rng.bit_generator.state = hit[1]
+        return hit[0]
+    res = _sample_workload(wl, cfg, rng)
+    _SAMPLE_CACHE.clear()
+    _SAMPLE_CACHE[key] = (res, rng.bit_generator.state)
+    return res
+
+
+def _sample_workload(wl: dict, cfg, rng):
     from paper_2603_25832_b200.sampling import anisotropic_ensemble, sample_arrays, seeded_b3_noise
 
     if wl.get("sampler") == "anisotropic":
@@ -213,26 +253,54 @@ def cpu_baseline_line(wl: dict, seed: int, reps: int = 1, warm: int = 0):
     from oracle import oracle as O
 
     st = host_initial_state(wl, seed)
+    plan = cpu_sample_plan(wl)
     for _ in range(warm):
-        cpu_sample_step(wl, st, seed=seed)
+        cpu_sample_step(wl, st, plan, seed=seed)
     times, parts = [], None
+    wall0 = time.perf_counter()
     for _ in range(reps):
-        T, parts = cpu_sample_step(wl, st, seed=seed)
+        T, parts = cpu_sample_step(wl, st, plan, seed=seed)
         times.append(T)
+    sample_seconds = (time.perf_counter() - wall0) / max(reps, 1)
     T = statistics.mean(times)
     n = wl["n"]
-    live = O.count_live_pairs(st["x"], wl["L"] / wl["M"], wl["M"]) if wl["n"] <= (1 << 21) else None
+    live = O.count_live_pairs(st["x"], wl["L"] / wl["M"], wl["M"]) if n <= (1 << 21) else None
+    net = wl.get("net")
+    sample = (f"oracle/ float64 C+OpenMP port of the reference path; per step: push/deposit/"
+              f"field/bin on all n; the pair kernel on every {plan['cell_stride']}-th cell "
+              f"(x{plan['cell_stride']}); ")
+    if wl["estimator"] == "blob":
+        sample += f"the blob score on the same cells (x{plan['cell_stride']})"
+    elif net == "silu":
+        sample += (f"the SiLU 2x128 score net as the float64 numpy restatement "
+                   f"oracle/silu_oracle.py (the reference has no such network): K ISM steps on "
+                   f"{plan['ism_particles']} particles (x{n / plan['ism_particles']:.0f}), "
+                   f"forward on every {plan['forward_stride']}-th particle "
+                   f"(x{plan['forward_stride']})")
+    else:
+        sample += (f"the reference's softsign score net: K ISM steps on "
+                   f"{plan['ism_particles']} particles (x{n / plan['ism_particles']:.0f}), "
+                   f"forward on all n")
+    scale = {"pair_cells": plan["cell_stride"], "ism": n / plan["ism_particles"],
+             "forward": plan["forward_stride"] if net == "silu" else 1}
     return dict(value=n / T, unit="particle-steps/s", cores=O.num_threads(), kind="port",
-                sample=("oracle/ float64 C+OpenMP port; per step: push/deposit/field/bin on "
-                        "all n, the pair kernel on every 16th cell (x16), and "
-                        + ("the SiLU 2x128 score net as the float64 numpy restatement "
-                           "oracle/silu_oracle.py (the reference has no such network): K ISM "
-                           "steps on n/64 particles (x64), forward on every 16th particle (x16)"
-                           if wl.get("net") == "silu" else
-                           "the reference's softsign score net: K ISM steps on n/16 particles "
-                           "(x16), forward on all n")),
-                seconds_per_step=T, stage_seconds=parts,
+                sample=sample, extrapolated=True, sample_seconds=sample_seconds,
+                scale_factors=scale, seconds_per_step=T, stage_seconds=parts,
                 pair_interactions_per_s=(live / parts["collision"]) if live else None)
+
+
+def bench_config(wl: dict, world: int) -> dict:
+    """The `config` dict of a bench line; identical for the GPU arm and the reference arm."""
+    return {"workload": wl["workload"], "n": wl["n"], "M": wl["M"], "L": wl["L"],
+            "mode": wl["mode"], "estimator": wl["estimator"], "K_ism": wl["K"],
+            "hidden": wl["hidden"], "net": NET_LABEL[wl.get("net", "softsign")]
+            if wl["estimator"] == "sbtm" else None,
+            "bandwidth": wl.get("bandwidth"), "divergence": wl["divergence"],
+            "nu": wl["nu"], "dt": wl["dt"],
+            "l2": "flushed between timed steps (256 MiB write + read-back, outside timed windows)",
+            "parallelism": ("single GPU" if world == 1 else
+                            f"cell-range decomposition of the same n over {world} ranks (NCCL): "
+                            "migration, halo, rho/J and ISM-gradient allreduces")}
 
 
 # ------------------------------------------------------------------------------------------
@@ -531,22 +599,23 @@ def hbm_microbench(torch, device, peak_gbs: float, n: int = 1 << 24, M: int = 10
 
 
 def build_dist_sim(wl: dict, seed: int, device, world: int):
-    """Weak-scaled decomposed problem: world x (n, M, L) of the workload, cell ranges per rank."""
+    """The workload's own problem (n, M, L fixed: strong scaling, as BASELINE configs 3 and 4
+    define their 2/4/8-GPU runs) decomposed into cell ranges, one per rank; the ranges are
+    balanced on the initial cell counts."""
     from paper_2603_25832_b200.dist_engine import DistSimulation
     from paper_2603_25832_b200.parallel import CellPartition, Comm
     from paper_2603_25832_b200.pic import Grid, deposit
     from paper_2603_25832_b200.run import initial_fields
     from paper_2603_25832_b200.state import ParticleEnsemble
 
-    wl = dict(wl, n=wl["n"] * world, M=wl["M"] * world, L=wl["L"] * world)
     cfg = make_config(wl, seed)
     rng = np.random.default_rng(seed)
     x, v, w, b3 = sample_workload(wl, cfg, rng)
     grid = Grid(cfg.M, cfg.eta)
     comm = Comm()
-    part = CellPartition.equal(cfg.M, world)
     cell = np.minimum(np.floor(x.astype(np.float32).astype(np.float64) / grid.eta).astype(np.int64) % cfg.M,
                       cfg.M - 1)
+    part = CellPartition.balanced(np.bincount(cell, minlength=cfg.M), world)
     lo, hi = part.owned(comm.rank)
     own = np.nonzero((cell >= lo) & (cell < hi))[0]
     # global initial fields from the full ensemble (identical on every rank)
@@ -595,11 +664,13 @@ def main():
                "impl": "reference", "n_gpus": args.gpus, "steps": reps, "warmup": warm,
                "requested_steps": args.steps, "requested_warmup": args.warmup,
                "ms_per_step": 1e3 * line["seconds_per_step"], "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": wl["workload"], "n": wl["n"], "M": wl["M"], "K": wl["K"],
-                          "hidden": wl["hidden"], "net": NET_LABEL[wl.get("net", "softsign")]},
-               "cpu_baseline": {"value": line["value"], "unit": "particle-steps/s",
-                                "cores": line["cores"], "kind": "port", "sample": line["sample"]},
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": bench_config(wl, 1),
+               "cpu_baseline": {k: line[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                     "extrapolated", "sample_seconds",
+                                                     "scale_factors")},
+               "extrapolated": True, "sample_seconds": line["sample_seconds"],
+               "scale_factors": line["scale_factors"],
                "e2e": {"value": line["value"], "unit": "particle-steps/s",
                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                "pair_interactions_per_s": line["pair_interactions_per_s"],
@@ -627,8 +698,8 @@ def main():
     device = torch.device("cuda", local)
     _lib.load(build_if_missing=False)
 
-    # N = 1: the single-GPU engine. N > 1: the cell-range decomposition of a weak-scaled
-    # problem (N x particles, cells and domain length) over NCCL.
+    # N = 1: the single-GPU engine. N > 1: the cell-range decomposition of the same problem
+    # (strong scaling) over NCCL.
     sim = build_dist_sim(wl, args.seed, device, world) if dist_mode else build_sim(wl, args.seed, device)
     n = wl["n"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
@@ -687,7 +758,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     total_ms, coll_avg_ms = float(t[0]), float(t[1])
-    value = world * n * args.steps / (total_ms * 1e-3)
+    value = n * args.steps / (total_ms * 1e-3)  # n = the whole job's particles (strong scaling)
 
     # end to end through the public host-buffer API
     e2e = None
@@ -696,25 +767,31 @@ def main():
         xh = torch.empty(n, dtype=torch.float32).pin_memory()
         vh = torch.empty(dv, n, dtype=torch.float32).pin_memory()
         dh = torch.empty(sim.diag.shape[1], dtype=torch.float64).pin_memory()
+        fh = torch.empty(sim.flags.shape[0], dtype=torch.int32).pin_memory()
         xh.copy_(sim.p.x)
         vh.copy_(sim.p.vp)
         torch.cuda.synchronize()
-        sim.step_host(2, xh, vh, dh)  # warm
+        sim.step_host(2, xh, vh, dh, fh)  # warm
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+        stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            sim.step_host(2, xh, vh, dh)
+            sim.step_host(2, xh, vh, dh, fh)
+            stream.synchronize()       # the per-step flag read run() does (ref: run.py:107-108)
+            sim.check_host(fh.numpy())
         e1.record()
         e1.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n * args.steps / (float(te[0]) * 1e-3), "unit": "particle-steps/s",
+        e2e = {"value": n * args.steps / (float(te[0]) * 1e-3), "unit": "particle-steps/s",
                "h2d_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4),
-               "d2h_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4 + dh.numel() * 8)}
+               "d2h_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4 + dh.numel() * 8
+                                         + fh.numel() * 4),
+               "flags_checked_every_step": True}
         sim.check()
     elif not args.no_e2e:
         # decomposed engine: each rank's particles through DistSimulation.step_host (pinned
@@ -742,7 +819,7 @@ def main():
             te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
             nb = int(statistics.mean(counts)) * 4 * (1 + dv)
-            e2e = {"value": world * n * args.steps / (float(te[0]) * 1e-3),
+            e2e = {"value": n * args.steps / (float(te[0]) * 1e-3),
                    "unit": "particle-steps/s", "h2d_bytes_per_step": nb,
                    "d2h_bytes_per_step": nb + dh.numel() * 8,
                    "note": "per rank: its own particles in and out every step (rank 0's bytes)"}
@@ -769,16 +846,10 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded reference sampler; random-init score net, no pretraining)",
-        "config": {"workload": wl["workload"], "n_per_gpu": n, "M": wl["M"], "L": wl["L"],
-                   "mode": wl["mode"], "estimator": wl["estimator"], "K_ism": wl["K"],
-                   "hidden": wl["hidden"], "net": NET_LABEL[wl.get("net", "softsign")],
-                   "divergence": wl["divergence"], "sub_cells": sim.S,
-                   "l2": "flushed between timed steps (256 MiB write + read-back, outside timed windows)",
-                   "parallelism": ("single GPU" if not dist_mode else
-                        f"cell-range decomposition over {world} ranks (NCCL): migration, "
-                        "halo, rho/J and ISM-gradient allreduces")},
+        "config": bench_config(wl, world),
+        "engine": {"sub_cells": sim.S, "cuda_graph": use_graph, "dist_path": dist_mode},
         "pair_interactions_per_s": world * live / (coll_avg_ms * 1e-3),
         "live_pairs_per_step": live,
         "collision_ms": coll_avg_ms,
@@ -813,6 +884,13 @@ def main():
             out["hbm_kernels"] = hbm_microbench(torch, device, hbm_peak_gbs())
         except Exception as exc:  # noqa: BLE001
             out["hbm_kernels"] = {"error": str(exc)}
+    if world == 1 and args.workload == "c4":
+        # BASELINE config 3 (the VML config: Weibel, full Maxwell) in the same run
+        try:
+            out["config3_vml"] = variant_line(torch, device, WORKLOADS["c3"], args.seed)
+            out["config3_vml"]["config"] = bench_config(WORKLOADS["c3"], 1)
+        except Exception as exc:  # noqa: BLE001
+            out["config3_vml"] = {"error": str(exc)}
     if world == 1 and args.workload + "ss" in WORKLOADS:
         # the same config with the reference's own softsign network (like-for-like with the
         # reference arm, which has no SiLU network)
@@ -824,7 +902,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line = cpu_baseline_line(wl, args.seed)
-            out["cpu_baseline"] = {k: line[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"] = {k: line[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                        "extrapolated", "sample_seconds",
+                                                        "scale_factors")}
             out["cpu_baseline"]["pair_interactions_per_s"] = line["pair_interactions_per_s"]
         except Exception as exc:  # noqa: BLE001
             out["cpu_baseline"] = {"error": str(exc)}

@@ -1037,9 +1037,25 @@ extern "C" int spic_silu_finalize(void* scratch, int64_t n, int32_t H, int32_t m
                                         grads_out, loss_out, row + 1 + P, flags);
   } else {
     cudaMemsetAsync(sync, 0, sizeof(int32_t), st);  // the barrier ticket
-    k_silu_finalize_mc<<<kSiluFinCTAs, 256, 0, st>>>(
-        row, P, mse != 0, params64, m, v2, opt_state, beta1, beta2, eps, weight_decay, reset_lr,
-        apply_step, params32, grads_out, loss_out, row + 1 + P, flags, sync);
+    // cooperative launch: the runtime guarantees the kSiluFinCTAs CTAs are co-resident (or
+    // fails the launch) so the spin barrier cannot deadlock behind other work holding SMs;
+    // cudaLaunchKernelEx with the cooperative attribute is stream-capturable
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kSiluFinCTAs);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const bool mse_b = mse != 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_silu_finalize_mc, row, P, mse_b, params64, m, v2,
+                                       opt_state, beta1, beta2, eps, weight_decay, (int)reset_lr,
+                                       (int)apply_step, params32, grads_out, loss_out,
+                                       row + 1 + P, flags, sync);
+    if (e != cudaSuccess) return SPIC_ERR_CUDA - (int)e;
   }
   spic::count_launch();
   SPIC_CHECK_LAUNCH();

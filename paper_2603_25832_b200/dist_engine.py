@@ -270,7 +270,7 @@ class DistSimulation:
         if f[_lib.FLAG_ISOLATED]:
             idx = int(self.bad_pid.item()) & 0xFFFFFFFF
             raise ValueError(f"isolated particle in velocity space (particle {idx})")
-        raise_for_flags(fl)
+        raise_for_flags(fl, self.f)
 
     def records(self, rows, steps, times) -> list:
         D = self.diag[list(rows)].cpu().numpy()

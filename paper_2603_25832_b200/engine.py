@@ -126,16 +126,20 @@ class Simulation:
                       _lib.ptr(d[4:9]), _lib.ptr(self.flags), _lib.ptr(buf), nb, st)
 
     def step_host(self, row: int, x_host: torch.Tensor, v_host: torch.Tensor,
-                  diag_host: torch.Tensor) -> None:
+                  diag_host: torch.Tensor, flags_host: torch.Tensor | None = None) -> None:
         """Public end-to-end step on HOST buffers (pinned float32 x (n,), v planes (dv, n),
-        float64 diag (DIAG_W,)): H2D of the state, one device step, D2H of the updated state
-        and of the step's diagnostics row — all enqueued on the current stream."""
+        float64 diag (DIAG_W,)): H2D of the state, one device step, D2H of the updated state,
+        of the step's diagnostics row and (if given, pinned int32 (8,)) of the error flags —
+        all enqueued on the current stream; check_host(flags_host) after a sync raises the
+        reference's exception for the step, as run() does once per step."""
         self.p.x.copy_(x_host, non_blocking=True)
         self.p.vp.copy_(v_host, non_blocking=True)
         self.step(row)
         x_host.copy_(self.p.x, non_blocking=True)
         v_host.copy_(self.p.vp, non_blocking=True)
         diag_host.copy_(self.diag[row], non_blocking=True)
+        if flags_host is not None:
+            flags_host.copy_(self.flags, non_blocking=True)
 
     # ---- host reads -------------------------------------------------------------------------
     def check(self) -> None:
@@ -144,7 +148,13 @@ class Simulation:
         if f[_lib.FLAG_ISOLATED]:
             idx = int(self.bad_pid.item()) & 0xFFFFFFFF
             raise ValueError(f"isolated particle in velocity space (particle {idx})")
-        raise_for_flags(self.flags)
+        raise_for_flags(self.flags, self.f)
+
+    def check_host(self, flags_host) -> None:
+        """check() on a host copy of the flags (e.g. the one step_host() fills), no D2H read."""
+        if flags_host[_lib.FLAG_ISOLATED]:
+            self.check()
+        raise_for_flags(flags_host, self.f)
 
     def lr_halvings(self) -> int:
         return int(self.flags[_lib.FLAG_LR_HALVINGS].item())

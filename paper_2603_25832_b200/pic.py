@@ -41,9 +41,11 @@ class Grid:
         return out
 
 
-def raise_for_flags(flags: torch.Tensor) -> None:
-    """Map device flags to the reference's exceptions (one D2H read)."""
-    f = flags.cpu().numpy()
+def raise_for_flags(flags, fields=None) -> None:
+    """Map device flags (a device tensor, or a host copy of it) to the reference's exceptions.
+    With `fields` given, a non-finite field is named as in FieldState.validate
+    (ref: state.py:75-78: "non-finite field state: {name}", first of E1, E2, B3, rho, J)."""
+    f = flags.cpu().numpy() if isinstance(flags, torch.Tensor) else np.asarray(flags)
     if f[_lib.FLAG_NONFINITE_X]:
         raise ValueError("non-finite position")
     if f[_lib.FLAG_NON_NEUTRAL]:
@@ -55,7 +57,14 @@ def raise_for_flags(flags: torch.Tensor) -> None:
     if f[_lib.FLAG_NONFINITE_V]:
         raise ValueError("non-finite particle state")
     if f[_lib.FLAG_NONFINITE_FIELD]:
-        raise ValueError("non-finite field state")
+        name = "E1"
+        if fields is not None:
+            for nm in ("E1", "E2", "B3", "rho", "J"):
+                a = getattr(fields, nm, None)
+                if a is not None and not bool(torch.isfinite(a).all()):
+                    name = nm
+                    break
+        raise ValueError(f"non-finite field state: {name}")
 
 
 def push_particles(particles: ParticleEnsemble, fields: FieldState, grid: Grid, dt: float,

@@ -1,0 +1,247 @@
+"""GPU parity at the sizes the bench reports (BASELINE configs 1-4), per particle, against the
+float64 oracle (oracle/, pinned to the reference by tests/test_oracle_golden.py).
+
+Tolerances (float32 product vs float64 reference):
+  * collision velocities U: relative L2 <= 1e-4 and per particle |err| <= 1e-4 * max|U_ref|
+    over every target of the sampled cells (the oracle evaluates every `stride`-th cell in
+    full: all targets of the cell against its whole 3-cell stencil,
+    ref: collision.py:49-110);
+  * SiLU ISM loss <= 1e-4 relative and gradients <= 1e-4 relative L2 per parameter tensor
+    (split-BF16 tensor-core products, see tests/test_gpu_silu.py);
+  * 100 full config-0 steps (softsign SBTM net, the reference's network) against
+    oracle.full_step on the same float32 initial state: conservation and field-energy traces
+    within the bands stated in test_config0_100_steps_traces_match_oracle.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2603_25832_b200 import _lib
+
+    _lib.load()
+    return _lib
+
+
+def relL2(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def bench_ensemble(tag: str, seed: int = 0):
+    """The bench's own initial ensemble of BASELINE config `tag` (seeded reference sampler /
+    config-3 anisotropic sampler), rounded to float32 once."""
+    import bench
+
+    wl = bench.WORKLOADS[tag]
+    cfg = bench.make_config(wl, seed)
+    x, v, w, _ = bench.sample_workload(wl, cfg, np.random.default_rng(seed))
+    return f32(x), f32(v), f32(w), wl
+
+
+def sampled_cell_mask(x, eta, M, stride):
+    cell = O.cell_of(x, eta, M)
+    return (cell % stride) == 0
+
+
+@pytest.mark.parametrize("tag,stride", [("c2", 8), ("c3", 16), ("c4", 64)])
+def test_collision_per_particle_at_bench_size(lib, tag, stride):
+    """Configs 2 (n = 2^20, M = 128), 3 (n = 2^22, M = 256, Weibel velocities) and 4
+    (n = 2^24, M = 1024): U from the device path the engine runs (antisymmetric pair kernel,
+    sub-cell culling, cell-sorted records) against the oracle on every `stride`-th cell.
+    Scores are non-Maxwellian so U is O(1): config 2 the exact two-stream mixture score,
+    config 3 the anisotropic Maxwellian's exact score -v_k / T_k, config 4 -v plus a smooth
+    perturbation."""
+    from paper_2603_25832_b200.collision import auto_sub_cells, build_cell_index, collision_force
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    x, v, w, wl = bench_ensemble(tag)
+    n, M, L = wl["n"], wl["M"], wl["L"]
+    if tag == "c2":
+        s = -v.copy()
+        s[:, 0] = -v[:, 0] + wl["c"] * np.tanh(wl["c"] * v[:, 0])
+    elif tag == "c3":
+        s = -v / np.asarray(wl["temps"])[None, :]
+    else:
+        s = -v + 0.5 * np.sin(2.0 * v[:, [1, 2, 0]])
+    s = f32(s)
+    grid = Grid(M, L / M)
+    p = ParticleEnsemble.from_arrays(x, v, w)
+    ci = build_cell_index(p, grid, auto_sub_cells(n, M))
+    U = collision_force(p, s, ci, grid, -3.0).double().cpu().numpy()
+    ref = O.collision_force(x, v, p.w.double().cpu().numpy(), s, grid.eta, M, -3.0,
+                            cell_stride=stride)
+    mask = sampled_cell_mask(x, grid.eta, M, stride)
+    assert mask.sum() > n // (2 * stride)
+    got, want = U[mask], ref[mask]
+    err = relL2(got, want)
+    worst = float(np.max(np.abs(got - want)) / np.max(np.abs(want)))
+    print(f"{tag}: {int(mask.sum())} targets, relL2 {err:.2e}, worst/max {worst:.2e}")
+    assert err <= 1e-4, err
+    assert worst <= 1e-4, worst
+    assert np.all(np.isfinite(U))
+
+
+def test_config1_n131072_per_particle(lib):
+    """BASELINE config 1 at its largest n = 131 072: one cell, co-located x, two-stream
+    mixture velocities with the exact mixture score; all n^2 ordered pairs live. Every
+    particle against the oracle, plus momentum / energy conservation <= 1e-5 (A1 metric,
+    ref: tests/test_acceptance.py:62-77)."""
+    from paper_2603_25832_b200.collision import build_cell_index, collision_force
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    n, L = 131072, 2.0
+    rng = np.random.default_rng(1)
+    v = rng.normal(size=(n, 3))
+    v[:, 0] += np.where(rng.random(n) < 0.5, 1.5, -1.5)
+    v = f32(v)
+    s = -v.copy()
+    s[:, 0] = -v[:, 0] + 1.5 * np.tanh(1.5 * v[:, 0])
+    s = f32(s)
+    x = np.full(n, 1.0)
+    p = ParticleEnsemble.from_arrays(x, v, np.full(n, L / n))
+    grid = Grid(1, L)
+    U = collision_force(p, s, build_cell_index(p, grid), grid, -3.0).double().cpu().numpy()
+    w64 = p.w.double().cpu().numpy()
+    ref = O.collision_force(x, v, w64, s, L, 1, -3.0)
+    err = relL2(U, ref)
+    worst = float(np.max(np.abs(U - ref)) / np.max(np.abs(ref)))
+    print(f"config1 n=131072: relL2 {err:.2e}, worst/max {worst:.2e}")
+    assert err <= 1e-4 and worst <= 1e-4, (err, worst)
+    wU = w64[:, None] * U
+    mom = np.max(np.abs(wU.sum(0))) / (np.max(np.abs(wU)) * n)
+    en = abs(float(np.sum(w64 * np.einsum("ij,ij->i", v, U))))
+    en /= float(np.sum(w64 * np.linalg.norm(v, axis=1) * np.linalg.norm(U, axis=1)))
+    assert mom <= 1e-5 and en <= 1e-5, (mom, en)
+
+
+def _silu_oracle_chunked(params, x, v, w, L, chunk=1 << 17):
+    """Float64 ISM loss and gradient of the SiLU net summed over particle chunks (the loss
+    and every gradient are sums over particles)."""
+    from oracle import silu_oracle as so
+
+    loss, grad = 0.0, None
+    for a in range(0, x.shape[0], chunk):
+        b = min(a + chunk, x.shape[0])
+        l, g = so.ism_loss_and_grad(params, so.inputs(x[a:b], v[a:b], L), w[a:b], 128)
+        loss += l
+        grad = g if grad is None else grad + g
+    return loss, grad
+
+
+@pytest.mark.parametrize("tag", ["c2", "c3"])
+def test_silu_ism_at_bench_size(lib, tag):
+    """The SiLU ISM kernel at the bench's own sizes (config 2: n = 2^20 two-stream; config 3:
+    n = 2^22 Weibel velocities): one persistent CTA per SM accumulates ~150 (2^20) to ~600
+    (2^22) 48-particle chunks in float32 TMEM before its float64 partial row; loss and every
+    gradient tensor against the float64 oracle."""
+    from oracle import silu_oracle as so
+    from paper_2603_25832_b200.silu_net import SiluScoreNet, silu_ism_loss_and_grad
+
+    x, v, w, wl = bench_ensemble(tag)
+    L = wl["L"]
+    rng = np.random.default_rng(5)
+    params = so.glorot(128, rng)
+    params[4 * 128:5 * 128] = rng.normal(0, 0.3, 128)
+    params[-3:] = rng.normal(0, 0.3, 3)
+    params = f32(params)
+    net = SiluScoreNet()
+    net.set_flat(params)
+    loss, g = silu_ism_loss_and_grad(net, x, v, w, L)
+    g = g.cpu().numpy()
+    ref_loss, ref_g = _silu_oracle_chunked(params, x, v, w, L)
+    print(f"{tag}: loss {loss:.8e} vs {ref_loss:.8e}")
+    assert abs(loss - ref_loss) <= 1e-4 * abs(ref_loss), (loss, ref_loss)
+    for (a, b, _), name in zip(net._slices(), ("W1", "b1", "W2", "b2", "W3", "b3")):
+        e = relL2(g[a:b], ref_g[a:b])
+        print(f"  {name}: relL2 {e:.2e}")
+        assert e <= 1e-4, (name, e)
+
+
+def test_config0_100_steps_traces_match_oracle(lib):
+    """BASELINE config 0 (Landau damping, n = 65 536, M = 64, L = 4 pi, nu = 0.1, dt = 0.05,
+    K = 10 exact-divergence ISM steps, H = 128 softsign net — the reference's network —, Adam
+    lr 1e-3, no pretraining) for 100 steps on the device engine and in oracle.full_step from
+    the same float32 initial state and the same initial network. Particle trajectories are
+    chaotic in the float32 / float64 difference, so the run is compared
+    through conservation and traces:
+      * energy drift |E_tot(t) / E_tot(0) - 1| of the device run <= 1e-4 at every step, and
+        within 1e-5 of the oracle's drift;
+      * momentum |P(t)| <= 1e-5 * sum w |v| (conserved by push (E only) + Landau);
+      * field-energy traces: max_t |E_E - E_E_ref| <= 2e-2 * max_t E_E_ref, same for E_l2.
+    H_dot (depends on the trained net) is printed, not asserted.
+    Measured values are printed (DESIGN.md section 5 records them)."""
+    import bench
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
+    from paper_2603_25832_b200.score import MlpScoreNet, SbtmEstimator
+    from paper_2603_25832_b200.state import FieldState, ParticleEnsemble
+
+    steps, dt, nu, K = 100, 0.05, 0.1, 10
+    wl = bench.WORKLOADS["c0ss"]
+    cfg = bench.make_config(wl, 0)
+    rng = np.random.default_rng(0)
+    x, v, w, _ = bench.sample_workload(wl, cfg, rng)
+    x, v = f32(x), f32(v)
+    n, M, L = wl["n"], wl["M"], wl["L"]
+    grid = Grid(M, L / M)
+    p = ParticleEnsemble.from_arrays(x, v, w)
+    w64 = p.w.double().cpu().numpy()
+    rho, _ = deposit(p, grid)
+    rho_ion = float(rho.sum()) * grid.eta / L
+    f = FieldState.zeros(M, 3, rho_ion)
+    f.E1.copy_(poisson_solve(rho, rho_ion, grid))
+    E1_0 = f.E1.cpu().numpy().copy()
+    net = MlpScoreNet.init_glorot(3, 128, rng)
+    onet = O.Net(*[a.cpu().numpy().astype(np.float64).copy() for a in net.params()])
+    est = SbtmEstimator(net, L, K, rng, lr=1e-3, weight_decay=0.0, divergence="exact")
+    sim = Simulation(p, f, grid, dt=dt, nu=nu, mode="VPL", gamma=-3.0, estimator=est,
+                     max_rows=steps + 1)
+    for k in range(1, steps + 1):
+        sim.step(k)
+    sim.check()
+    got = sim.records(range(1, steps + 1), range(1, steps + 1), [dt * k for k in range(1, steps + 1)])
+
+    st = dict(x=x.copy(), v=v.copy(), w=w64, E1=E1_0.copy(), E2=np.zeros(M), B3=np.zeros(M))
+    d0 = O.diagnostics(v, w64, E1_0, np.zeros(M), np.zeros(M), grid.eta)
+    opt = O.AdamW(lr=1e-3, weight_decay=0.0)
+    ref = [O.full_step(st, eta=grid.eta, M=M, dt=dt, nu=nu, mode="VPL", gamma=-3.0, net=onet,
+                       opt=opt, K=K, divergence="exact") for _ in range(steps)]
+
+    E0 = d0["E_total"]
+    drift_g = np.array([r.E_total / E0 - 1.0 for r in got])
+    drift_r = np.array([r["E_total"] / E0 - 1.0 for r in ref])
+    EE_g, EE_r = np.array([r.E_E for r in got]), np.array([r["E_E"] for r in ref])
+    El_g, El_r = np.array([r.E_l2 for r in got]), np.array([r["E_l2"] for r in ref])
+    P_g = np.array([r.P for r in got])
+    HD_g, HD_r = np.array([r.H_dot for r in got]), np.array([r["H_dot"] for r in ref])
+    pscale = float(np.sum(w64 * np.linalg.norm(v, axis=1)))
+    ee = float(np.max(np.abs(EE_g - EE_r)) / np.max(EE_r))
+    el = float(np.max(np.abs(El_g - El_r)) / np.max(El_r))
+    print(f"config0 100 steps: max drift device {np.max(np.abs(drift_g)):.3e}, oracle "
+          f"{np.max(np.abs(drift_r)):.3e}, max |drift diff| {np.max(np.abs(drift_g - drift_r)):.3e}; "
+          f"E_E trace {ee:.3e}, E_l2 trace {el:.3e}; max |P|/scale "
+          f"{np.max(np.abs(P_g)) / pscale:.3e}; min H_dot device {HD_g.min():.3e} oracle "
+          f"{HD_r.min():.3e}; E_E(0..100) device {EE_g[0]:.4e}..{EE_g[-1]:.4e} oracle "
+          f"{EE_r[0]:.4e}..{EE_r[-1]:.4e}")
+    assert np.max(np.abs(drift_g)) <= 1e-4
+    assert np.max(np.abs(drift_g - drift_r)) <= 1e-5
+    assert np.max(np.abs(P_g)) <= 1e-5 * pscale
+    assert ee <= 2e-2 and el <= 2e-2, (ee, el)

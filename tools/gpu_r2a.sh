@@ -1,0 +1,8 @@
+#!/bin/bash
+# round-2 first pass: gpu tests (incl. the at-size parity) + the default bench line
+cd $GRAFT_REPO_ROOT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
+timeout 2400 python -m pytest tests -m gpu -x -q -s -p no:cacheprovider > gpurun_out/r2a_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2a_pytest.log
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/r2a_bench.json 2> gpurun_out/r2a_bench.err
+echo "bench rc=$?" >> gpurun_out/r2a_bench.err
