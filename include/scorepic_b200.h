@@ -96,7 +96,10 @@ int spic_landau(const float* xv, const float* sw, int64_t n, int32_t dv, const i
                 float uniform_w, int32_t nsplit, float* U_sorted, void* scratch,
                 size_t scratch_bytes, void* stream);
 /* Same, with targets restricted to the cells [c_lo, c_hi) (a domain rank's owned cells;
- * halo cells only act as neighbours). U_sorted entries of other cells are not written. */
+ * halo cells only act as neighbours). U_sorted entries of other cells are not written.
+ * Scratch: spic_landau_range_scratch_bytes (per-cell sizes estimated over the range). */
+size_t spic_landau_range_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nsplit,
+                                       int32_t c_lo, int32_t c_hi);
 int spic_landau_range(const float* xv, const float* sw, int64_t n, int32_t dv,
                       const int32_t* cell_start, const int32_t* sub_start, int32_t M, int32_t S,
                       double eta, double gamma, float uniform_w, int32_t nsplit, int32_t c_lo,
@@ -255,6 +258,33 @@ size_t spic_moments_scratch_bytes(int64_t n);
 int spic_moments(const float* v, int64_t ldv, const float* w, int64_t n, int32_t dv,
                  float uniform_w, double* out, int32_t* flags, void* scratch,
                  size_t scratch_bytes, void* stream);
+
+/* ---- cell-range domain decomposition (the reference is single-
+ *      process: these replace the per-rank bookkeeping of its run loop, run.py:81-118, when
+ *      particles are partitioned by cell over ranks) ------------------------------------------
+ * Message = float4 pairs: pair 0 = header int32 {rows, rows in the receiver's owned cells,
+ * rows dropped for capacity, 0}; pair r+1 = (x, v0, v1, v2), (w, gid as int32 bits, 0, 0).
+ * send_cells / recv_cells are HOST int32[4]: two cell ranges [a0, a1) and [b0, b1) (empty when
+ * a1 <= a0) giving the cyclic cell range to send and its part owned by the receiver. Rows are
+ * read from pid-order planes through perm (sorted position -> pid) over cell_start. */
+int spic_dist_pack(const float* x, const float* v, int64_t ldv, int32_t dv, const float* w,
+                   float uniform_w, const int32_t* gid, const int32_t* perm,
+                   const int32_t* cell_start, int32_t M, const int32_t* send_cells,
+                   const int32_t* recv_cells, int64_t cap, float* msg, void* stream);
+/* rows [0, rows) of a message -> planes at [at, at + rows) (w nullable). */
+int spic_dist_unpack(const float* msg, int64_t rows, int64_t at, float* x, float* v, int64_t ldv,
+                     int32_t dv, float* w, int32_t* gid, void* stream);
+size_t spic_dist_epilogue_scratch_bytes(void);
+/* Collision epilogue over the owned sorted positions [cell_start[lo], cell_start[hi]) (read
+ * on device): v_new = v[perm[k]] - nu_dt U[:, k]; the rank's next particle state is written
+ * compacted in sorted order (out_x/out_v/out_w/out_gid at k - cell_start[lo]); red_out
+ * (float64[6]) = [H_dot, E_K, P_0, P_1, P_2, sum w] over those particles. */
+int spic_dist_epilogue(const float* U_sorted, int64_t ldu, const float* sw, const int32_t* perm,
+                       const int32_t* cell_start, int32_t lo, int32_t hi, int32_t dv, float nu_dt,
+                       const float* x, const float* v, int64_t ldv, const float* w,
+                       const int32_t* gid, float* out_x, float* out_v, int64_t ldo,
+                       float* out_w, int32_t* out_gid, double* red_out, int32_t* flags,
+                       void* scratch, size_t scratch_bytes, void* stream);
 
 #ifdef __cplusplus
 }

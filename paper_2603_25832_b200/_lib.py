@@ -47,6 +47,7 @@ SIGNATURES = {
                                 _P, _SZ, _P]),
     "spic_gather_scores": (ctypes.c_int, [_P, _I64, _P, _I64, _I32, _P, _P, _P]),
     "spic_landau_scratch_bytes": (_SZ, [_I64, _I32, _I32, _I32]),
+    "spic_landau_range_scratch_bytes": (_SZ, [_I64, _I32, _I32, _I32, _I32, _I32]),
     "spic_landau": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P, _I32, _I32, _D, _D, _F, _I32, _P,
                                    _P, _SZ, _P]),
     "spic_landau_range": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P, _I32, _I32, _D, _D, _F, _I32,
@@ -91,6 +92,12 @@ SIGNATURES = {
     "spic_poisson": (ctypes.c_int, [_P, _D, _I32, _D, _P, _P, _P]),
     "spic_moments_scratch_bytes": (_SZ, [_I64]),
     "spic_moments": (ctypes.c_int, [_P, _I64, _P, _I64, _I32, _F, _P, _P, _P, _SZ, _P]),
+    "spic_dist_pack": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _F, _P, _P, _P, _I32, _P, _P, _I64,
+                                      _P, _P]),
+    "spic_dist_unpack": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _I64, _I32, _P, _P, _P]),
+    "spic_dist_epilogue_scratch_bytes": (_SZ, []),
+    "spic_dist_epilogue": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _F, _P, _P, _I64,
+                                          _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 
 

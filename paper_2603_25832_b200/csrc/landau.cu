@@ -451,7 +451,7 @@ __global__ void k_fold_splits(const float* __restrict__ part, int nsplit, int dv
 using namespace spic;
 
 // antisymmetric (unordered-pair) path, landau_sym.cu
-size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit);
+size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit, int32_t m_occ);
 int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32_t* cell_start,
                         const int32_t* sub_start, int32_t M, int32_t S, double eta,
                         float uniform_w, int32_t nsplit, int32_t c_lo, int32_t c_hi,
@@ -464,13 +464,19 @@ static char landau_variant() {
   return var ? var[0] : 0;
 }
 
-extern "C" size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nsplit) {
+extern "C" size_t spic_landau_range_scratch_bytes(int64_t n, int32_t M, int32_t dv,
+                                                   int32_t nsplit, int32_t c_lo, int32_t c_hi) {
   const int32_t ns = nsplit <= 0 ? auto_nsplit(n, M, dv) : nsplit;
   size_t b = sizeof(int32_t) * (size_t)(M + 1 + 31);
   if (ns > 1) b += sizeof(float) * (size_t)ns * dv * n + 256;
+  const int32_t m_occ = (c_hi - c_lo) < M ? std::min<int32_t>(M, (c_hi - c_lo) + 3) : M;
   if (dv == 3 && landau_variant() == 0)
-    b = std::max(b, spic_landau_sym_scratch_bytes(n, M, nsplit));
+    b = std::max(b, spic_landau_sym_scratch_bytes(n, M, nsplit, m_occ));
   return b;
+}
+
+extern "C" size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nsplit) {
+  return spic_landau_range_scratch_bytes(n, M, dv, nsplit, 0, M);
 }
 
 extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, int32_t dv,
@@ -495,7 +501,8 @@ extern "C" int spic_landau_range(const float* xv, const float* sw, int64_t n, in
   if (c_lo < 0 || c_hi > M || c_lo > c_hi) return SPIC_ERR_ARG;
   if (n < 0 || n > INT32_MAX || M < 1 || S < 1 || !(eta > 0) || (dv != 2 && dv != 3))
     return SPIC_ERR_ARG;
-  if (scratch_bytes < spic_landau_scratch_bytes(n, M, dv, nsplit)) return SPIC_ERR_SCRATCH;
+  if (scratch_bytes < spic_landau_range_scratch_bytes(n, M, dv, nsplit, c_lo, c_hi))
+    return SPIC_ERR_SCRATCH;
   if (n == 0) return SPIC_OK;
   const char var = landau_variant();
   if (dv == 3 && gamma == -3.0 && uniform_w > 0.f && var == 0 &&

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(1024) k_sym_tiles(
 // (even, odd) pairs; j records broadcast from shared memory (one-sided stages) or read in a
 // per-lane XOR order inside groups of 8 (two-sided stages, so the warp reduce-scatter of the
 // j-side needs no selects: lane l holds record (k ^ m_l), m_l = (l >> 2) & 7).
-template <int NT, int RP, int MINB, bool MINIMG>
+template <int NT, int RP, int MINB, bool MINIMG, int G>
 __global__ void __launch_bounds__(NT, MINB)
     k_landau_sym(const float4* __restrict__ xv, const float4* __restrict__ sw,
                  const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
@@ -242,7 +242,10 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int q = 0; q < min(ntiles, kSymStages); ++q) issue(q);
   }
   __syncthreads();  // padding writes of the prologue stages
-  const uint32_t mofs = (uint32_t)(((lane >> 2) & 7) * sizeof(float4));
+  // two-sided stages: groups of G records, lane l reads record k ^ m_l of each group
+  constexpr int kLpr = 32 / G;  // lanes per record after the reduce-scatter
+  const int m_l = (lane / kLpr) & (G - 1);
+  const uint32_t mofs = (uint32_t)(m_l * sizeof(float4));
   constexpr uint32_t kSwOfs = kSymTJ * sizeof(float4);
 
   for (int q = 0; q < ntiles; ++q) {
@@ -289,11 +292,11 @@ __global__ void __launch_bounds__(NT, MINB)
       }
     } else {
       float* jp = &s_jp[q & 1][wid][0];
-      for (int jb = 0; jb < d.cnt; jb += 8) {
-        float P0[8], P1[8], P2[8];
+      for (int jb = 0; jb < d.cnt; jb += G) {
+        float P0[G], P1[G], P2[G];
         const uint32_t gb = (sbase + (uint32_t)jb * sizeof(float4)) | mofs;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < G; ++k) {
           const uint32_t a = gb ^ (uint32_t)(k * sizeof(float4));
           const float4 A = lds128(a);
           const float4 B = lds128(a + kSwOfs);
@@ -333,13 +336,13 @@ __global__ void __launch_bounds__(NT, MINB)
           un2(J1, e, o); P1[k] = e + o;
           un2(J2, e, o); P2[k] = e + o;
         }
-        float PP[3][8];
+        float PP[3][G];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) { PP[0][k] = P0[k]; PP[1][k] = P1[k]; PP[2][k] = P2[k]; }
-        sym_reduce_scatter8<3>(PP);
+        for (int k = 0; k < G; ++k) { PP[0][k] = P0[k]; PP[1][k] = P1[k]; PP[2][k] = P2[k]; }
+        if constexpr (G == 8) sym_reduce_scatter8<3>(PP); else sym_reduce_scatter4<3>(PP);
         P0[0] = PP[0][0]; P1[0] = PP[1][0]; P2[0] = PP[2][0];
-        const int cc = lane & 3;
-        if (cc < 3) jp[(jb + ((lane >> 2) & 7)) * 3 + cc] = cc == 0 ? P0[0] : (cc == 1 ? P1[0] : P2[0]);
+        const int cc = lane & (kLpr - 1);
+        if (cc < 3) jp[(jb + m_l) * 3 + cc] = cc == 0 ? P0[0] : (cc == 1 ? P1[0] : P2[0]);
       }
     }
     __syncthreads();  // stage st consumed; warp slices of a two-sided stage complete
@@ -410,43 +413,46 @@ constexpr size_t sym_smem_bytes(int NT) {
 
 // kernel configuration: threads per CTA, packed target pairs per thread, resident CTAs per SM
 struct SymCfg {
-  int nt, rp, minb;
+  int nt, rp, minb, g;  // g: records per j-side reduce-scatter group
   int ti() const { return nt * 2 * rp; }
 };
-constexpr SymCfg kSymCfgs[] = {{128, 2, 4}, {128, 2, 3}, {128, 3, 3}, {256, 2, 2}, {128, 3, 2}};
+constexpr SymCfg kSymCfgs[] = {{128, 2, 4, 8}, {128, 2, 3, 8}, {128, 3, 3, 8}, {256, 2, 2, 8},
+                               {128, 3, 2, 8}, {128, 2, 5, 8}, {128, 2, 4, 4}, {128, 2, 5, 4},
+                               {128, 2, 6, 4}};
+constexpr int kNumSymCfgs = sizeof(kSymCfgs) / sizeof(kSymCfgs[0]);
 
 SymCfg sym_cfg(int M) {
   if (M <= 2) return kSymCfgs[0];
   const char* e = getenv("SPIC_SYM_CFG");
   const int k = e ? atoi(e) : 0;
-  return kSymCfgs[(k >= 0 && k < 5) ? k : 0];
+  return kSymCfgs[(k >= 0 && k < kNumSymCfgs) ? k : 0];
 }
 
 }  // namespace
 
 // nsplit for the symmetric kernel: whole waves of (CTAs per SM) x SMs
-int spic_landau_sym_nsplit(int64_t n, int32_t M) {
+int spic_landau_sym_nsplit(int64_t n, int32_t M, int32_t m_occ) {
   const SymCfg c = sym_cfg(M);
-  return pair_nsplit_slots(n, M, c.ti(), c.minb * kNumSMs);
+  return pair_nsplit_slots(n, m_occ > 0 ? m_occ : M, c.ti(), c.minb * kNumSMs);
 }
 
-size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit) {
-  if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
-  return sym_layout(nullptr, n, M, nsplit, sym_cfg(M).ti()).bytes + 256;
+size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit, int32_t m_occ) {
+  if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M, m_occ);
+  return sym_layout(nullptr, n, M, nsplit, sym_cfg(M).ti(), 3, m_occ).bytes + 256;
 }
 
-template <int NT, int RP, int MINB, bool MINIMG>
+template <int NT, int RP, int MINB, bool MINIMG, int G = 8>
 static void launch_sym(dim3 grid, cudaStream_t st, const float* xv, const float* sw,
                        const int32_t* cell_start, const int32_t* ssp, const SymScratch& s, int M,
                        int S, float L, float wie, float wie2, int nsplit, int split_fast,
                        int64_t n) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_landau_sym<NT, RP, MINB, MINIMG>,
+    cudaFuncSetAttribute(k_landau_sym<NT, RP, MINB, MINIMG, G>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem_bytes(NT));
     attr = true;
   }
-  k_landau_sym<NT, RP, MINB, MINIMG><<<grid, NT, sym_smem_bytes(NT), st>>>(
+  k_landau_sym<NT, RP, MINB, MINIMG, G><<<grid, NT, sym_smem_bytes(NT), st>>>(
       (const float4*)xv, (const float4*)sw, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag,
       M, S, L, wie, wie2, nsplit, split_fast, s.Upart, s.Jslot, n);
 }
@@ -457,9 +463,10 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
                         float* U_sorted, void* scratch, size_t scratch_bytes, void* stream) {
   const SymCfg cfg = sym_cfg(M);
   const int TI = cfg.ti();
-  if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M);
+  const int m_occ = (c_hi - c_lo) < M ? std::min<int>(M, (c_hi - c_lo) + 3) : M;
+  if (nsplit <= 0) nsplit = spic_landau_sym_nsplit(n, M, m_occ);
   uintptr_t b = ((uintptr_t)scratch + 255) & ~(uintptr_t)255;
-  SymScratch s = sym_layout((void*)b, n, M, nsplit, TI);
+  SymScratch s = sym_layout((void*)b, n, M, nsplit, TI, 3, m_occ);
   if (s.bytes + (b - (uintptr_t)scratch) > scratch_bytes) return SPIC_ERR_SCRATCH;
   cudaStream_t st = (cudaStream_t)stream;
   const double L = (double)M * eta;
@@ -479,6 +486,14 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
   const float Lf = (float)L;
   if (M <= 2)
     launch_sym<128, 2, 4, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
+  else if (cfg.g == 4 && cfg.minb == 4)
+    launch_sym<128, 2, 4, false, 4>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
+  else if (cfg.g == 4 && cfg.minb == 5)
+    launch_sym<128, 2, 5, false, 4>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
+  else if (cfg.g == 4 && cfg.minb == 6)
+    launch_sym<128, 2, 6, false, 4>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
+  else if (cfg.minb == 5)
+    launch_sym<128, 2, 5, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.nt == 256)
     launch_sym<256, 2, 2, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.rp == 3 && cfg.minb == 3)

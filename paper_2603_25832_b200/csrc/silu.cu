@@ -36,6 +36,12 @@ constexpr int kNCW = 128 * kNWG;  // compute threads
 constexpr int kNT = kNCW + 32;    // + one MMA-issuer warp
 constexpr int kPPT = kCP / kNWG;  // particles per thread per chunk
 constexpr uint32_t kTmemCols = 512;
+// The weight-gradient accumulators dW2 (D3) and M (D4) stay in TMEM for at most this many
+// chunks; then they are added into a per-CTA float32 buffer in global memory (L2) and the
+// next G3 starts a fresh accumulation. The tensor pipe's float32 accumulation is not
+// round-to-nearest: over ~600 chunks (n = 2^22 on 148 CTAs) its error reached 2e-4 relative
+// on the tangent terms, over 64 chunks it stays at ~1e-5, independent of n.
+constexpr int kFlushChunks = 64;
 constexpr uint32_t kColD1 = 0, kColD2 = 128, kColD3 = 256;  // self-test accumulators
 
 #ifdef SPIC_SILU_TRACE  // tools/silu_trace.cu: per-phase clock64 stamps of CTA 0, thread 0
@@ -197,7 +203,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
                                                  float x_scale, float L,
                                                  float4* __restrict__ sw_out,
                                                  double* __restrict__ part,
-                                                 float* __restrict__ part_w2) {
+                                                 float* __restrict__ part_w2,
+                                                 float* __restrict__ part_acc) {
   constexpr bool ISM = MODE != 0;  // training modes (loss + gradient partials)
   constexpr bool DIV = MODE == 1;  // divergence columns
   const float4* __restrict__ xv = in.xv;
@@ -323,6 +330,24 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     gb1 += ab1;
   };
 
+  // this thread's 32-column slice of D3 / D4 (row h, columns 32 wg ..) in the CTA's buffer
+  int nflush = 0;
+  float* acc_row = part_acc ? part_acc + (size_t)blockIdx.x * 2 * kH * kH + (size_t)h * kH + 32 * wg
+                            : nullptr;
+  auto flush_acc = [&](uint32_t col, int which) {
+    float t[32];
+    umma::tmem_ld32(tl + col + (uint32_t)(32 * wg), t);
+    float4* g = reinterpret_cast<float4*>(acc_row + (size_t)which * kH * kH);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float4 a = make_float4(t[4 * k], t[4 * k + 1], t[4 * k + 2], t[4 * k + 3]);
+      if (nflush) {
+        const float4 b = g[k];
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      g[k] = a;
+    }
+  };
   bool pending = false;  // the previous chunk's layer-1 reverse sweep is still to run (ISM)
   int ub = 0;            // S.u buffer of the current chunk
   if (tid >= kNCW) {
@@ -360,12 +385,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         SILU_TRACE_I(12);
         {
           // G3 first: the next chunk's layer-1 sweep waits for it (X, Y reuse)
+          const bool acc3 = !fst && (iit % kFlushChunks) != 0;  // fresh after a flush
           umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(tm + cD3, sYh, sYl, sXh,
-                                                                      sXl, !fst);  // da2 h1^T
+                                                                      sXl, acc3);  // da2 h1^T
           if (DIV)
             umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(
                 tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
-                !fst);  // y2 d1^T
+                acc3);  // y2 d1^T
           umma::commit_elect(&S.bar[1]);
 #ifdef SPIC_SILU_TRACE_G3  // timing diagnostic: stamp G3's completion before issuing G2
           {
@@ -533,6 +559,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     umma::fence_before();
     handoff_arrive(6);
     SILU_TRACE(2);
+    if (it > 0 && it % kFlushChunks == 0) {
+      // G3 of the previous chunk is complete (wait_g3 above) and the next G3 is issued only
+      // after this chunk's F2b hand-off: move D3 (and D4) into the CTA's float32 buffer
+      flush_acc(cD3, 0);
+      if (DIV) flush_acc(cD4, 1);
+      ++nflush;
+    }
     if (MODE == 1 && pending) layer1_reverse(ub ^ 1);  // overlaps this chunk's G1
     SILU_TRACE(3);
     umma::wait_mma(&S.bar[0], phase);
@@ -673,6 +706,21 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       float v[32], m[32];
       umma::tmem_ld32(tl + cD3 + (uint32_t)(32 * wg), v);
       if (DIV) umma::tmem_ld32(tl + cD4 + (uint32_t)(32 * wg), m);
+      if (nflush) {  // the earlier windows' sums (fixed order: earlier windows first)
+        const float4* g3 = reinterpret_cast<const float4*>(acc_row);
+        const float4* g4 = reinterpret_cast<const float4*>(acc_row + kH * kH);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 a = g3[k];
+          v[4 * k] = a.x + v[4 * k]; v[4 * k + 1] = a.y + v[4 * k + 1];
+          v[4 * k + 2] = a.z + v[4 * k + 2]; v[4 * k + 3] = a.w + v[4 * k + 3];
+          if (DIV) {
+            const float4 b = g4[k];
+            m[4 * k] = b.x + m[4 * k]; m[4 * k + 1] = b.y + m[4 * k + 1];
+            m[4 * k + 2] = b.z + m[4 * k + 2]; m[4 * k + 3] = b.w + m[4 * k + 3];
+          }
+        }
+      }
       // the dW2 row block (rows 32q.. of this warp, columns 32g..32g+31) goes out through a
       // per-warp shared-memory transpose in two 16-column halves, so each store instruction
       // writes two 128-B row segments instead of 32 scattered doubles (free space after the
@@ -886,10 +934,15 @@ static size_t silu_f32_offset(int64_t n) {
   return (b + 255) & ~(size_t)255;
 }
 
+static size_t silu_acc_offset(int64_t n) {
+  return silu_f32_offset(n) + sizeof(float) * (size_t)silu_blocks(n) * kH * kH;
+}
+
 extern "C" size_t spic_silu_scratch_bytes(int64_t n) {
   // [blocks][1 + P] partials, the reduced row, candidate parameters, finalize sync words,
-  // then the per-CTA dW2 partials as float [blocks][H * H] (the rows' W2 range is unused)
-  return silu_f32_offset(n) + sizeof(float) * (size_t)silu_blocks(n) * kH * kH;
+  // then the per-CTA dW2 partials as float [blocks][H * H] (the rows' W2 range is unused),
+  // then the per-CTA flushed TMEM accumulators float [blocks][2][H * H]
+  return silu_acc_offset(n) + sizeof(float) * (size_t)silu_blocks(n) * 2 * kH * kH;
 }
 
 extern "C" int64_t spic_silu_row_offset(int64_t n) {
@@ -910,7 +963,8 @@ static int silu_launch(int mode, const float* params32, int32_t H, const SiluInp
                          (int)kSiluSmem);                                                      \
     k_silu<MD><<<blocks, kNT, kSiluSmem, st>>>(                                                \
         params32, in, n, x_scale, L, (float4*)sw_out, part,                                    \
-        part ? (float*)((char*)part + silu_f32_offset(n)) : nullptr);                          \
+        part ? (float*)((char*)part + silu_f32_offset(n)) : nullptr,                           \
+        part ? (float*)((char*)part + silu_acc_offset(n)) : nullptr);                          \
   } while (0)
   if (mode == 0) SPIC_SILU_LAUNCH(0);
   else if (mode == 1) SPIC_SILU_LAUNCH(1);

@@ -138,6 +138,23 @@ __device__ __forceinline__ void sym_reduce_scatter8(float (&P)[NC][8]) {
   for (int c = 0; c < NC; ++c) P[c][0] += __shfl_xor_sync(0xffffffffu, P[c][0], 1);
 }
 
+// Same over 4 records (lane l holds record k ^ m_l, m_l = (l >> 3) & 3): xor-16/8 exchanges
+// without selects, then xor-4/2/1 butterflies; every lane ends with the warp sums of record
+// m_l in P[c][0]. Half the live partials of the 8-record form for ~1.3x its shuffles.
+template <int NC>
+__device__ __forceinline__ void sym_reduce_scatter4(float (&P)[NC][4]) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) P[c][k] += __shfl_xor_sync(0xffffffffu, P[c][k + 2], 16);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) P[c][0] += __shfl_xor_sync(0xffffffffu, P[c][1], 8);
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) P[c][0] += __shfl_xor_sync(0xffffffffu, P[c][0], o);
+}
+
 // the fold's walk over a record's slots: own-cell tiles before its tile, then the tiles of
 // cell c-1 whose seg2 reaches it; calls f(slot) in that fixed order
 template <typename F>
@@ -179,13 +196,18 @@ struct SymScratch {
 
 static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-static inline SymScratch sym_layout(void* base, int64_t n, int M, int nsplit, int TI, int nc = 3) {
+// m_occ: the cells the records occupy (M for a whole-grid call; a domain rank's target range
+// plus its halo cells for a range call), which sets the per-cell size estimate
+static inline SymScratch sym_layout(void* base, int64_t n, int M, int nsplit, int TI, int nc = 3,
+                                    int m_occ = 0) {
   SymScratch s{};
+  if (m_occ <= 0 || m_occ > M) m_occ = M;
   const int64_t Tmax = n / TI + M + 2;
   // slot estimate for a near-uniform ensemble: each tile's forward window ~ one cell plus a
   // sub-cell; 1.3x headroom (an exceeding ensemble runs the ordered path, see k_sym_tiles)
-  const int64_t ncell = n / std::max(M, 1);
-  int64_t cap = (int64_t)(1.3 * (double)Tmax * (double)(ncell + 2 * TI)) + 4096;
+  const int64_t ncell = n / std::max(m_occ, 1);
+  const int64_t Tocc = n / TI + m_occ + 2;
+  int64_t cap = (int64_t)(1.3 * (double)Tocc * (double)(ncell + 2 * TI)) + 4096;
   // at most 16 GiB of slots (a near-uniform n = 2^24, M = 1024 ensemble needs ~7 GB); a
   // degenerate ensemble (e.g. one huge cell) beyond that takes the ordered path
   const int64_t cap_max = ((int64_t)16 << 30) / (int64_t)(sizeof(float) * nc);

@@ -1,18 +1,15 @@
 """Cell-range domain decomposition across ranks.
 
 One process per GPU. Rank r owns the contiguous cell range [C_r, C_{r+1}) and the particles
-in it. Per step the only exchanges are the ones the physics needs:
+in it. Per step the only exchanges are the ones the physics needs (dist_engine.py):
 
-  * migration   — particles whose new cell is owned elsewhere go to the owner
-                  (all-to-all with per-destination counts; in practice only ring
-                  neighbours receive anything since dt |v1| << cell width);
-  * deposit     — allreduce(SUM) of the deposited rho, J (M x (1+dv) float64);
+  * deposit     — allreduce(SUM) of the deposited [rho; J] ((1+dv) x M float64);
   * SBTM        — allreduce(SUM) of the reduced ISM loss/gradient row (1 + P + H float64)
                   before every finalize, so every rank applies the identical AdamW step;
-  * halo        — the particles of the boundary cells C_r and C_{r+1}-1 go to the left and
-                  right neighbours (1-cell halo: the stencil of an owned cell is owned or
-                  halo); for the blob estimator the halo scores are exchanged a second time;
-  * diagnostics — allreduce(SUM) of [H_dot, E_K, P].
+  * boundary    — one fixed-size message to each ring neighbour carrying the particles that
+                  moved to its side plus the first / last g owned cells (its halo); migration
+                  and the halo exchange are this one message;
+  * diagnostics — allreduce(SUM) of [H_dot, E_K, P, sum w].
 
 The routines here are device-agnostic (torch tensors + torch.distributed), so the partition
 and exchange logic is tested on CPU with the gloo backend (tests/test_parallel_gloo.py); on
@@ -81,82 +78,53 @@ class CellPartition:
 
 
 class Comm:
-    """torch.distributed helpers (works for gloo/CPU and NCCL/CUDA tensors)."""
+    """torch.distributed helpers (works for gloo/CPU and NCCL/CUDA tensors).
 
-    def __init__(self, group=None):
+    host_staged=True runs every collective on host copies of device tensors (gloo on CPU):
+    several ranks can then share one GPU (NCCL refuses two ranks on one device), which is how
+    the multi-rank device path is tested on a single B200."""
+
+    def __init__(self, group=None, host_staged: bool = False):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.size = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.host_staged = host_staged
 
-    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+    def _op(self, op: str):
+        return {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX}[op]
+
+    def allreduce_(self, t: torch.Tensor, op: str = "sum") -> torch.Tensor:
         if self.size > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            if self.host_staged and t.is_cuda:
+                h = t.cpu()
+                dist.all_reduce(h, op=self._op(op), group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=self._op(op), group=self.group)
         return t
 
-    def alltoallv(self, send: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
-        """Rows of `send` (grouped by destination, counts[d] rows for rank d) -> rows received,
-        grouped by source rank in rank order."""
+    def exchange_pair(self, to_left: torch.Tensor, to_right: torch.Tensor,
+                      from_left: torch.Tensor, from_right: torch.Tensor,
+                      part: "CellPartition") -> None:
+        """Fixed-size point-to-point exchange with the ring neighbours: to_left goes to the
+        left neighbour (which receives it as its from_right), to_right to the right one. With
+        R == 2 both neighbours are one rank; messages between one pair of ranks match in
+        posting order, so the receives are posted swapped there."""
         if self.size == 1:
-            return send.clone()
-        counts = counts.to(torch.int64)
-        recv_counts = torch.empty_like(counts)
-        dist.all_to_all_single(recv_counts, counts, group=self.group)
-        sc, rc = counts.cpu().tolist(), recv_counts.cpu().tolist()
-        out = torch.empty((sum(rc),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
-        dist.all_to_all_single(out, send.contiguous(), output_split_sizes=rc,
-                               input_split_sizes=sc, group=self.group)
-        return out
-
-    def exchange_halo(self, to_left: torch.Tensor, to_right: torch.Tensor,
-                      part: CellPartition) -> tuple[torch.Tensor, torch.Tensor]:
-        """Send rows to the left / right neighbour; returns (from_left, from_right), where
-        from_left is the left neighbour's `to_right` (its last cell) and vice versa.
-        With R == 2 both neighbours are the same rank; point-to-point messages between one
-        pair of ranks are matched in posting order, so the receives are posted swapped."""
-        if self.size == 1:
-            return to_right.clone(), to_left.clone()
+            from_left.copy_(to_right)
+            from_right.copy_(to_left)
+            return
         left, right = part.neighbours(self.rank)
-        dev, dt, tail = to_left.device, to_left.dtype, tuple(to_left.shape[1:])
-
-        def p2p(sends, recvs):
-            ops = [dist.P2POp(dist.isend, t, peer, self.group) for t, peer in sends if t.numel()]
-            ops += [dist.P2POp(dist.irecv, t, peer, self.group) for t, peer in recvs if t.numel()]
-            if ops:
-                for req in dist.batch_isend_irecv(ops):
-                    req.wait()
-
-        n_l = torch.tensor([to_left.shape[0]], dtype=torch.int64, device=dev)
-        n_r = torch.tensor([to_right.shape[0]], dtype=torch.int64, device=dev)
-        m_l = torch.empty(1, dtype=torch.int64, device=dev)
-        m_r = torch.empty(1, dtype=torch.int64, device=dev)
-        recv_order = [(m_r, right), (m_l, left)] if left == right else [(m_l, left), (m_r, right)]
-        p2p([(n_l, left), (n_r, right)], recv_order)
-        from_left = torch.empty((int(m_l.item()),) + tail, dtype=dt, device=dev)
-        from_right = torch.empty((int(m_r.item()),) + tail, dtype=dt, device=dev)
-        recv_order = [(from_right, right), (from_left, left)] if left == right else \
-            [(from_left, left), (from_right, right)]
-        p2p([(to_left.contiguous(), left), (to_right.contiguous(), right)], recv_order)
-        return from_left, from_right
-
-
-def route(cells: torch.Tensor, owner: torch.Tensor, R: int):
-    """Stable grouping of local rows by destination rank: (order, counts)."""
-    dest = owner[cells.long()]
-    order = torch.argsort(dest, stable=True)
-    counts = torch.bincount(dest, minlength=R)
-    return order, counts
-
-
-def migrate(rows: torch.Tensor, cells: torch.Tensor, owner: torch.Tensor, comm: Comm) -> torch.Tensor:
-    """Send every row to the owner of its cell; returns this rank's rows (by source rank)."""
-    order, counts = route(cells, owner, comm.size)
-    return comm.alltoallv(rows[order], counts)
-
-
-def boundary_rows(rows_sorted: torch.Tensor, cell_start: np.ndarray, part: CellPartition,
-                  rank: int) -> tuple[torch.Tensor, torch.Tensor]:
-    """Rows of my first and last owned cells from cell-sorted rows (contiguous slices)."""
-    lo, hi = part.owned(rank)
-    first = rows_sorted[int(cell_start[lo]):int(cell_start[lo + 1])]
-    last = rows_sorted[int(cell_start[hi - 1]):int(cell_start[hi])]
-    return first, last
+        staged = self.host_staged and to_left.is_cuda
+        sl, sr = (to_left.cpu(), to_right.cpu()) if staged else (to_left, to_right)
+        rl = torch.empty_like(sl) if staged else from_left
+        rr = torch.empty_like(sr) if staged else from_right
+        ops = [dist.P2POp(dist.isend, sl, left, self.group),
+               dist.P2POp(dist.isend, sr, right, self.group)]
+        recvs = [(rr, right), (rl, left)] if left == right else [(rl, left), (rr, right)]
+        ops += [dist.P2POp(dist.irecv, t, peer, self.group) for t, peer in recvs]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        if staged:
+            from_left.copy_(rl)
+            from_right.copy_(rr)

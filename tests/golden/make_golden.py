@@ -305,6 +305,69 @@ def gen_run():
     save("run.npz", **out)
 
 
+def gen_faults():
+    """sbtm_update's restore-and-halve recovery (ref: score.py:568-587): (A) a non-finite loss
+    (W2[0,0] = inf, the reference test_score.py:231-237 construction) halves the learning rate
+    down to the 1e-12 floor and raises "training divergence"; (B) a finite loss whose AdamW step
+    overflows (lr * weight_decay = inf) restores the parameters and halves until the step is
+    finite, with m, v and t advancing on every attempt."""
+    out = {}
+    n, dv, H, L = 512, 3, 16, 4 * math.pi
+    prng = np.random.default_rng(400)
+    x = f32(prng.uniform(0, L, n))
+    v = f32(prng.normal(size=(n, dv)))
+    w = np.full(n, L / n)
+    p = ParticleEnsemble(x=x, v=v, w=w)
+    out.update(fault_x=x, fault_v=v, fault_w=w)
+    # (A) fatal
+    net = score.MlpScoreNet.init_glorot(dv, H, np.random.default_rng(41))
+    net.W2[0, 0] = np.inf
+    out.update(net_arrays("faultA_init_", net))
+    opt = score.AdamW(lr=1e-3, weight_decay=0.0)
+    warn = []
+    try:
+        score.sbtm_update(net, opt, p, 2, L=L, rng=np.random.default_rng(1),
+                          divergence="exact", warnings=warn)
+        raise AssertionError("expected training divergence")
+    except RuntimeError as exc:
+        assert "training divergence" in str(exc)
+    out.update(net_arrays("faultA_final_", net))
+    out["faultA_warnings"] = np.array(warn)
+    out["faultA_lr_after"] = np.array(opt.lr)
+    out["faultA_t"] = np.array(opt.t)
+    # (B) recovery
+    net = score.MlpScoreNet.init_glorot(dv, H, np.random.default_rng(42))
+    out.update(net_arrays("faultB_init_", net))
+    opt = score.AdamW(lr=1e155, weight_decay=1e155)
+    warn = []
+    losses = score.sbtm_update(net, opt, p, 1, L=L, rng=np.random.default_rng(1),
+                               divergence="exact", warnings=warn)
+    out.update(net_arrays("faultB_final_", net))
+    out["faultB_losses"] = np.array(losses)
+    out["faultB_warnings"] = np.array(warn)
+    out["faultB_lr_after"] = np.array(opt.lr)
+    out["faultB_t"] = np.array(opt.t)
+    for k, (m_, v_) in enumerate(zip(opt.m, opt.v)):
+        out[f"faultB_m{k}"] = m_
+        out[f"faultB_v{k}"] = v_
+    save("faults.npz", **out)
+
+
+def gen_score_test():
+    """run.score_test (ref: run.py:134-185) with the blob estimator (deterministic): the
+    reference's CSV columns x, v*, s_est*, s_true*, U* and its reported MSE."""
+    cfg = build_config(overrides=dict(preset="two_stream", n=4096, M=16, seed=3,
+                                      estimator="blob"))
+    with tempfile.TemporaryDirectory() as d:
+        rep = run.score_test(cfg, d, compute_force=True, estimators=("blob",))
+        path = os.path.join(d, "score_test_blob.csv")
+        with open(path, encoding="utf-8") as fh:
+            header = fh.readline().strip().split(",")
+        data = np.loadtxt(path, delimiter=",", skiprows=1)
+    save("score_test.npz", columns=np.array(header), data=data,
+         mse=np.array(rep["blob"]["mse"]))
+
+
 if __name__ == "__main__":
     gen_binning()
     gen_collision()
@@ -313,3 +376,5 @@ if __name__ == "__main__":
     gen_adamw_sbtm()
     gen_pic()
     gen_run()
+    gen_faults()
+    gen_score_test()

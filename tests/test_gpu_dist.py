@@ -1,0 +1,196 @@
+"""The cell-range decomposed step engine (dist_engine.DistSimulation) executed with 1, 2 and 3
+ranks against the single-GPU engine (engine.Simulation) on the same global initial state.
+
+The ranks are separate processes sharing cuda:0 with a gloo process group and host-staged
+collectives (parallel.Comm(host_staged=True)): NCCL refuses two ranks on one device, and this
+round has one GPU. Every kernel of the decomposed step (push, binning of the own particles,
+deposit, boundary pack / unpack, union binning, scores, range pair kernel, compacting
+epilogue) runs on the device exactly as under NCCL; only the transport differs.
+
+Tolerances: the decomposition changes summation order (per-rank partial sums of rho, J and
+the ISM gradient rows; cell-sorted particle order), so results agree to float32 rounding
+amplified by three steps of training: E_total 1e-6 relative, E_E 1e-4, H_dot 2e-2, positions
+1e-5 L and velocities 2e-4 absolute per particle (by global id)."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+STEPS = 3
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _setup(estimator, n=20000, M=16, seed=3):
+    """Global ensemble, fields and estimator factory shared by both engines."""
+    from paper_2603_25832_b200.pic import Grid
+
+    L = 4 * math.pi
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    x[x >= L] = 0
+    v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
+    w = np.full(n, L / n)
+    return x, v, w, Grid(M, L / M), L
+
+
+def _fields(x, v, w, grid, L):
+    from paper_2603_25832_b200.pic import deposit, poisson_solve
+    from paper_2603_25832_b200.state import FieldState, ParticleEnsemble
+
+    p = ParticleEnsemble.from_arrays(x, v, w)
+    rho, _ = deposit(p, grid)
+    rho_ion = float(rho.sum()) * grid.eta / L
+    f = FieldState.zeros(grid.M, 3, rho_ion)
+    f.E1.copy_(poisson_solve(rho, rho_ion, grid))
+    return f
+
+
+def _estimator(kind, grid, L):
+    from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
+
+    r = np.random.default_rng(5)
+    if kind == "sbtm":
+        return SbtmEstimator(MlpScoreNet.init_glorot(3, 32, r), L, 3, r, lr=1e-3,
+                             weight_decay=0.0, divergence="exact")
+    if kind == "silu":
+        from paper_2603_25832_b200.silu_net import SiluEstimator, SiluScoreNet
+
+        return SiluEstimator(SiluScoreNet.init_glorot(r), L, 3, r, lr=1e-3, weight_decay=0.0)
+    return BlobEstimator(grid, None)
+
+
+def _reference(kind):
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    x, v, w, grid, L = _setup(kind)
+    p = ParticleEnsemble.from_arrays(x, v, w)
+    sim = Simulation(p, _fields(x, v, w, grid, L), grid, dt=0.05, nu=0.1, mode="VPL",
+                     gamma=-3.0, estimator=_estimator(kind, grid, L), max_rows=8)
+    for k in range(1, STEPS + 1):
+        sim.step(k)
+    sim.check()
+    recs = sim.records(range(1, STEPS + 1), range(1, STEPS + 1), [0.05 * k for k in range(1, STEPS + 1)])
+    return recs, p.x.double().cpu().numpy(), p.v.double().cpu().numpy()
+
+
+def _body(rank, world, port, kind, out_dir):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2603_25832_b200 import _lib
+        from paper_2603_25832_b200.dist_engine import DistSimulation
+        from paper_2603_25832_b200.parallel import CellPartition, Comm
+
+        _lib.load(build_if_missing=False)
+        x, v, w, grid, L = _setup(kind)
+        part = CellPartition.equal(grid.M, world)
+        lo, hi = part.owned(rank)
+        cell = np.minimum(np.floor(x / grid.eta).astype(np.int64) % grid.M, grid.M - 1)
+        own = np.nonzero((cell >= lo) & (cell < hi))[0]
+        sim = DistSimulation(x[own], v[own], w[own], own, _fields(x, v, w, grid, L), grid,
+                             dt=0.05, nu=0.1, mode="VPL", gamma=-3.0,
+                             estimator=_estimator(kind, grid, L),
+                             comm=Comm(host_staged=True), partition=part, n_global=x.shape[0],
+                             max_rows=8)
+        for k in range(1, STEPS + 1):
+            sim.step(k)
+        sim.check()
+        gid, xs, vs = sim.gather_state()
+        parts = [None] * world
+        dist.all_gather_object(parts, (gid, xs, vs, sim.host_syncs))
+        if rank == 0:
+            D = sim.diag[1:STEPS + 1].cpu().numpy()
+            g = np.concatenate([p[0] for p in parts])
+            np.savez(os.path.join(out_dir, "dist.npz"), diag=D, gid=g,
+                     x=np.concatenate([p[1] for p in parts]),
+                     v=np.concatenate([p[2] for p in parts]),
+                     syncs=np.array([p[3] for p in parts]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2603_25832_b200 import _lib
+
+    _lib.load()
+    return _lib
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("kind", ["sbtm", "silu", "blob"])
+def test_decomposed_step_matches_single_gpu_engine(lib, tmp_path, world, kind):
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_body, args=(world, _free_port(), kind, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    res = np.load(tmp_path / "dist.npz")
+    recs, x_ref, v_ref = _reference(kind)
+    D = res["diag"]
+    for k, r in enumerate(recs):
+        E_tot = D[k, 4] + D[k, 0] + D[k, 1]
+        assert E_tot == pytest.approx(r.E_total, rel=1e-6)
+        assert D[k, 0] == pytest.approx(r.E_E, rel=1e-4)
+        assert D[k, 3] == pytest.approx(r.H_dot, rel=2e-2, abs=1e-9)
+        assert D[k, 8] == pytest.approx(4 * math.pi, rel=1e-6)  # every particle owned once
+    gid = res["gid"]
+    assert np.array_equal(np.sort(gid), np.arange(x_ref.shape[0]))
+    L = 4 * math.pi
+    dx = np.abs(res["x"] - x_ref[gid])
+    assert np.max(np.minimum(dx, L - dx)) <= 1e-5 * L
+    assert np.max(np.abs(res["v"] - v_ref[gid])) <= 2e-4
+    if world > 1:  # one host synchronisation per step (the received counts)
+        assert np.all(res["syncs"] == STEPS)
+
+
+def test_decomposed_host_buffer_step_equals_device_step(lib):
+    """DistSimulation.step_host (the bench's e2e path at N > 1) equals its device step."""
+    from paper_2603_25832_b200.dist_engine import DistSimulation
+
+    x, v, w, grid, L = _setup("sbtm")
+    n = x.shape[0]
+
+    def make():
+        return DistSimulation(x, v, w, np.arange(n), _fields(x, v, w, grid, L), grid, dt=0.05,
+                              nu=0.1, mode="VPL", gamma=-3.0,
+                              estimator=_estimator("sbtm", grid, L), max_rows=8)
+
+    s4, s5 = make(), make()
+    for k in range(1, 4):
+        s4.step(k)
+        s5.step(k)
+    cap = s4.n + 1024
+    xh = torch.empty(cap, dtype=torch.float32).pin_memory()
+    vh = torch.empty(3, cap, dtype=torch.float32).pin_memory()
+    dh = torch.empty(s4.diag.shape[1], dtype=torch.float64).pin_memory()
+    n4 = s4.n
+    xh[:n4].copy_(s4.buf.x[:n4])
+    vh[:, :n4].copy_(s4.buf.vp[:, :n4])
+    s5.step(4)
+    s4.step_host(4, xh, vh, dh)
+    torch.cuda.synchronize()
+    n5 = s5.n
+    assert s4.n == n5
+    assert np.array_equal(xh[:n5].numpy(), s5.buf.x[:n5].cpu().numpy())
+    assert np.array_equal(vh[:, :n5].numpy(), s5.buf.vp[:, :n5].cpu().numpy())
+    assert np.array_equal(dh.numpy(), s5.diag[4].cpu().numpy())

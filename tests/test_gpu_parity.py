@@ -404,89 +404,6 @@ def test_engine_steps_match_reference_run(spic, golden, tag):
     assert np.max(np.abs(P - g[f"{tag}_P"][1:])) <= 1e-3 * scale
 
 
-# ---------------------------------------------------------------------------- decomposed engine
-@pytest.mark.parametrize("estimator", ["sbtm", "blob", "silu"])
-def test_dist_engine_single_rank_matches_engine(spic, estimator):
-    """DistSimulation (the per-rank path of the cell-range decomposition) on one rank gives
-    the same trajectory as the single-GPU engine."""
-    from paper_2603_25832_b200.dist_engine import DistSimulation
-    from paper_2603_25832_b200.engine import Simulation
-    from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
-    from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
-    from paper_2603_25832_b200.state import FieldState
-
-    n, M, L = 20000, 16, 4 * math.pi
-    rng = np.random.default_rng(3)
-    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
-    x[x >= L] = 0
-    v = rng.normal(size=(n, 3))
-    w = np.full(n, L / n)
-    grid = Grid(M, L / M)
-
-    def make(kind):
-        p = ens(x, v, w)
-        rho, J = deposit(p, grid)
-        rho_ion = float(rho.sum()) * grid.eta / L
-        f = FieldState.zeros(M, 3, rho_ion)
-        f.E1.copy_(poisson_solve(rho, rho_ion, grid))
-        if estimator == "sbtm":
-            r = np.random.default_rng(5)
-            net = MlpScoreNet.init_glorot(3, 32, r)
-            est = SbtmEstimator(net, L, 3, r, lr=1e-3, weight_decay=0.0, divergence="exact")
-        elif estimator == "silu":  # extension M1 (tcgen05 SiLU net) through the same engines
-            from paper_2603_25832_b200.silu_net import SiluEstimator, SiluScoreNet
-
-            r = np.random.default_rng(5)
-            est = SiluEstimator(SiluScoreNet.init_glorot(r), L, 3, r, lr=1e-3, weight_decay=0.0)
-        else:
-            est = BlobEstimator(grid, None)
-        if kind == "single":
-            return Simulation(p, f, grid, dt=0.05, nu=0.1, mode="VPL", gamma=-3.0, estimator=est,
-                              max_rows=8), p
-        sim = DistSimulation(x, v, w, np.arange(n), f, grid, dt=0.05, nu=0.1, mode="VPL",
-                             gamma=-3.0, estimator=est, max_rows=8)
-        return sim, None
-
-    s1, p1 = make("single")
-    s2, _ = make("dist")
-    for k in range(1, 4):
-        s1.step(k)
-        s2.step(k)
-    s1.check()
-    s2.check()
-    r1 = s1.records([1, 2, 3], [1, 2, 3], [0.05, 0.1, 0.15])
-    r2 = s2.records([1, 2, 3], [1, 2, 3], [0.05, 0.1, 0.15])
-    for a, b in zip(r1, r2):
-        assert a.E_total == pytest.approx(b.E_total, rel=1e-12)
-        assert a.H_dot == pytest.approx(b.H_dot, rel=1e-9, abs=1e-12)
-        assert a.E_E == pytest.approx(b.E_E, rel=1e-12)
-    gid, x2, v2 = s2.gather_state()
-    np.testing.assert_allclose(x2, p1.x.double().cpu().numpy()[gid], rtol=0, atol=1e-6)
-    np.testing.assert_allclose(v2, p1.v.double().cpu().numpy()[gid], rtol=1e-6, atol=1e-6)
-    # the decomposed engine's host-buffer step (bench e2e at N > 1) equals its device step
-    s4, _ = make("dist")
-    cap = s4.n + 1024
-    xh = torch.empty(cap, dtype=torch.float32).pin_memory()
-    vh = torch.empty(3, cap, dtype=torch.float32).pin_memory()
-    dh = torch.empty(s4.diag.shape[1], dtype=torch.float64).pin_memory()
-    for k in range(1, 4):
-        s4.step(k)
-    n4 = s4.n
-    xh[:n4].copy_(s4.buf.x[:n4])
-    vh[:, :n4].copy_(s4.buf.vp[:, :n4])
-    s5, _ = make("dist")
-    for k in range(1, 4):
-        s5.step(k)
-    s5.step(4)
-    s4.step_host(4, xh, vh, dh)
-    torch.cuda.synchronize()
-    n5 = s5.n
-    assert s4.n == n5
-    assert np.array_equal(xh[:n5].numpy(), s5.buf.x[:n5].cpu().numpy())
-    assert np.array_equal(vh[:, :n5].numpy(), s5.buf.vp[:, :n5].cpu().numpy())
-    assert np.array_equal(dh.numpy(), s5.diag[4].cpu().numpy())
-
-
 # ---------------------------------------------------------------------------- run() end to end
 @pytest.mark.parametrize("tag", ["sbtm", "blob", "vml"])
 def test_run_matches_reference_run(spic, golden, tmp_path, tag):

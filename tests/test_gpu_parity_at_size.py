@@ -183,10 +183,13 @@ def test_config0_100_steps_traces_match_oracle(lib):
     chaotic in the float32 / float64 difference, so the run is compared
     through conservation and traces:
       * energy drift |E_tot(t) / E_tot(0) - 1| of the device run <= 1e-4 at every step, and
-        within 1e-5 of the oracle's drift;
-      * momentum |P(t)| <= 1e-5 * sum w |v| (conserved by push (E only) + Landau);
-      * field-energy traces: max_t |E_E - E_E_ref| <= 2e-2 * max_t E_E_ref, same for E_l2.
-    H_dot (depends on the trained net) is printed, not asserted.
+        within 1e-7 of the oracle's drift (measured: drift 5.2e-5 on both, difference 2.8e-9);
+      * field-energy traces: max_t |E_E - E_E_ref| <= 1e-3 * max_t E_E_ref, same for E_l2
+        (measured 2.7e-5 and 2.6e-5);
+      * momentum: the P trace (P_x changes through the field force) within 1e-4 * sum w|v| of
+        the oracle's, P_y and P_z (no force, Landau conserves momentum) constant to 1e-6;
+      * entropy production H_dot (depends on the trained net): trace within 5e-2 of the
+        oracle's (measured minima 5.760e-3 vs 5.741e-3).
     Measured values are printed (DESIGN.md section 5 records them)."""
     import bench
     from paper_2603_25832_b200.engine import Simulation
@@ -230,18 +233,22 @@ def test_config0_100_steps_traces_match_oracle(lib):
     drift_r = np.array([r["E_total"] / E0 - 1.0 for r in ref])
     EE_g, EE_r = np.array([r.E_E for r in got]), np.array([r["E_E"] for r in ref])
     El_g, El_r = np.array([r.E_l2 for r in got]), np.array([r["E_l2"] for r in ref])
-    P_g = np.array([r.P for r in got])
+    P_g, P_r = np.array([r.P for r in got]), np.array([r["P"] for r in ref])
     HD_g, HD_r = np.array([r.H_dot for r in got]), np.array([r["H_dot"] for r in ref])
     pscale = float(np.sum(w64 * np.linalg.norm(v, axis=1)))
     ee = float(np.max(np.abs(EE_g - EE_r)) / np.max(EE_r))
     el = float(np.max(np.abs(El_g - El_r)) / np.max(El_r))
+    P0 = w64 @ v
+    pt = float(np.max(np.abs(P_g - P_r)) / pscale)
+    pyz = float(np.max(np.abs(P_g[:, 1:] - P0[None, 1:])) / pscale)
+    hd = float(np.max(np.abs(HD_g - HD_r)) / np.max(np.abs(HD_r)))
     print(f"config0 100 steps: max drift device {np.max(np.abs(drift_g)):.3e}, oracle "
           f"{np.max(np.abs(drift_r)):.3e}, max |drift diff| {np.max(np.abs(drift_g - drift_r)):.3e}; "
-          f"E_E trace {ee:.3e}, E_l2 trace {el:.3e}; max |P|/scale "
-          f"{np.max(np.abs(P_g)) / pscale:.3e}; min H_dot device {HD_g.min():.3e} oracle "
-          f"{HD_r.min():.3e}; E_E(0..100) device {EE_g[0]:.4e}..{EE_g[-1]:.4e} oracle "
+          f"E_E trace {ee:.3e}, E_l2 trace {el:.3e}; P trace {pt:.3e}, P_yz drift {pyz:.3e}; "
+          f"H_dot trace {hd:.3e}; E_E(1..100) device {EE_g[0]:.4e}..{EE_g[-1]:.4e} oracle "
           f"{EE_r[0]:.4e}..{EE_r[-1]:.4e}")
     assert np.max(np.abs(drift_g)) <= 1e-4
-    assert np.max(np.abs(drift_g - drift_r)) <= 1e-5
-    assert np.max(np.abs(P_g)) <= 1e-5 * pscale
-    assert ee <= 2e-2 and el <= 2e-2, (ee, el)
+    assert np.max(np.abs(drift_g - drift_r)) <= 1e-7
+    assert ee <= 1e-3 and el <= 1e-3, (ee, el)
+    assert pt <= 1e-4 and pyz <= 1e-6, (pt, pyz)
+    assert hd <= 5e-2, hd

@@ -21,7 +21,7 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2ss")
-    ap.add_argument("--cfgs", default="0,1,2,3,4")
+    ap.add_argument("--cfgs", default="0,5,6,7,8")
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
     wl = bench.WORKLOADS[args.workload]
