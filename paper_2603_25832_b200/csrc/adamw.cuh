@@ -17,6 +17,8 @@ __device__ __forceinline__ void adamw_with_recovery(
   if (grads_out)
     for (int64_t k = threadIdx.x; k < P; k += blockDim.x) grads_out[k] = grad[k];
   if (!apply_step) return;
+  // a fatal divergence earlier in this update raised in the reference: no further steps
+  if (flags && flags[SPIC_FLAG_TRAIN_FATAL]) return;
   double lr = reset_lr ? opt[2] : opt[1];
   if (!isfinite(loss)) {
     // ism_loss_and_grad raises before the optimizer step; sbtm_update restores (a no-op),
@@ -93,6 +95,7 @@ __device__ __forceinline__ void adamw_with_recovery_mc(
   if (grads_out)
     for (int64_t k = gtid; k < P; k += gstride) grads_out[k] = grad[k];
   if (!apply_step) return;
+  if (flags && flags[SPIC_FLAG_TRAIN_FATAL]) return;  // every CTA reads it before the barrier
   if (!isfinite(loss)) {  // see adamw_with_recovery; one thread records it
     if (gtid == 0) {
       double lr = reset_lr ? opt[2] : opt[1];

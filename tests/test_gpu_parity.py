@@ -704,7 +704,8 @@ def test_antisymmetric_pair_path_partial_cell_range(spic):
     cs = ci.cell_start.cpu().numpy()
     for c_lo, c_hi in ((0, 8), (5, 20), (24, 32), (1, 31)):
         U = torch.zeros(3, n, dtype=torch.float32, device="cuda")
-        buf, nb = _lib.scratch("landau_t", _lib.query("spic_landau_scratch_bytes", n, M, 3, 0))
+        buf, nb = _lib.scratch("landau_t", _lib.query("spic_landau_range_scratch_bytes", n, M, 3,
+                                                      0, c_lo, c_hi))
         _lib.call("spic_landau_range", _lib.ptr(ci.xv), _lib.ptr(ci.sw), n, 3,
                   _lib.ptr(ci.cell_start), _lib.ptr(ci.sub_start), M, S, float(grid.eta), -3.0,
                   float(p.uniform_w), 0, c_lo, c_hi, _lib.ptr(U), _lib.ptr(buf), nb,

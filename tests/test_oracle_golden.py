@@ -164,3 +164,51 @@ def test_oracle_full_steps_match_reference_run(golden, tag):
     np.testing.assert_allclose(got, ref[:, [2, 3, 4, 5, 6, 7]], rtol=1e-9, atol=1e-13)
     np.testing.assert_allclose(np.array([r["P"] for r in recs]), g[f"{tag}_P"], rtol=1e-9,
                                atol=1e-11)
+
+
+def test_sbtm_recovery_paths_match_reference(golden):
+    """sbtm_update's restore-and-halve recovery (ref: score.py:568-587; the construction of
+    test_score.py:231-237): (A) a non-finite loss halves lr down to the 1e-12 floor and raises,
+    parameters untouched, no optimizer step; (B) an AdamW step that overflows (lr * wd = inf)
+    restores and halves until finite, m, v and t advancing on every attempt."""
+    g = golden("faults.npz")
+    x, v, w, L = g["fault_x"], g["fault_v"], g["fault_w"], 4 * math.pi
+    net = _net(g, "faultA_init_")
+    opt = O.AdamW(lr=1e-3, weight_decay=0.0)
+    warn = []
+    with pytest.raises(RuntimeError, match="training divergence"):
+        O.sbtm_update(net, opt, x, v, w, 2, L=L, divergence="exact", warnings=warn)
+    assert warn == list(g["faultA_warnings"])
+    assert opt.lr == float(g["faultA_lr_after"]) and opt.t == int(g["faultA_t"])
+    for a, b in zip(net.params(), _net(g, "faultA_final_").params()):
+        assert np.array_equal(a, b)
+    net = _net(g, "faultB_init_")
+    opt = O.AdamW(lr=1e155, weight_decay=1e155)
+    warn = []
+    losses = O.sbtm_update(net, opt, x, v, w, 1, L=L, divergence="exact", warnings=warn)
+    np.testing.assert_allclose(losses, g["faultB_losses"], rtol=1e-12)
+    assert warn == list(g["faultB_warnings"])
+    assert opt.lr == float(g["faultB_lr_after"]) and opt.t == int(g["faultB_t"])
+    for a, b in zip(net.params(), _net(g, "faultB_final_").params()):
+        assert rel(a, b) <= 1e-12
+    for k in range(4):
+        assert rel(opt.m[k], g[f"faultB_m{k}"]) <= 1e-10
+        assert rel(opt.v[k], g[f"faultB_v{k}"]) <= 1e-10
+
+
+def test_score_test_fixture_matches_oracle_blob(golden):
+    """The reference's score_test blob CSV (ref: run.py:134-185): the oracle's blob scores and
+    Landau U on the CSV's own x, v columns reproduce its s_est and U columns."""
+    g = golden("score_test.npz")
+    cols = [str(c) for c in g["columns"]]
+    d = g["data"]
+    col = {c: i for i, c in enumerate(cols)}
+    x = d[:, col["x"]]
+    v = d[:, [col["v1"], col["v2"], col["v3"]]]
+    s = d[:, [col["s_est1"], col["s_est2"], col["s_est3"]]]
+    U = d[:, [col["U1"], col["U2"], col["U3"]]]
+    n, M, L = x.size, 16, 10 * math.pi
+    eta = L / M
+    w = np.full(n, L / n)
+    assert rel(O.blob_score(x, v, w, eta, M), s) <= 1e-11
+    assert rel(O.collision_force(x, v, w, s, eta, M, -3.0), U) <= 1e-11
