@@ -54,4 +54,15 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   return o;
 }
 
+// c - a*b as one FFMA2 with a negated operand: the product and the subtraction are written
+// without .rn so ptxas contracts them (same single rounding as fma(-a, b, c)); saves the two
+// LOP3s of an explicit sign flip
+__device__ __forceinline__ f2 fnms2(f2 a, f2 b, f2 c) {
+  f2 o;
+  asm("{\n.reg .b64 t;\nmul.ftz.f32x2 t, %1, %2;\nsub.ftz.f32x2 %0, %3, t;\n}"
+      : "=l"(o.r)
+      : "l"(a.r), "l"(b.r), "l"(c.r));
+  return o;
+}
+
 }  // namespace spic

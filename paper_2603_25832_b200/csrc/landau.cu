@@ -277,10 +277,10 @@ __global__ void __launch_bounds__(kLandauNT, MINB)
           // 1/|z|, or 0 for the eps2-skipped pairs (incl. the self pair)
           const f2 rp = mk2(zze > kEps2 ? qe : 0.f, zzo > kEps2 ? qo : 0.f);
           const f2 cw = mul2(mk2(ce, co), rp);           // w psi / |z|
-          const f2 nq = neg2(mul2(mul2(rp, rp), zu));    // -(z.u)/|z|^2
-          A0[r] = fma2(cw, fma2(nq, z0, u0), A0[r]);
-          A1[r] = fma2(cw, fma2(nq, z1, u1), A1[r]);
-          A2[r] = fma2(cw, fma2(nq, z2, u2), A2[r]);
+          const f2 q = mul2(mul2(rp, rp), zu);    // -(z.u)/|z|^2
+          A0[r] = fma2(cw, fnms2(q, z0, u0), A0[r]);
+          A1[r] = fma2(cw, fnms2(q, z1, u1), A1[r]);
+          A2[r] = fma2(cw, fnms2(q, z2, u2), A2[r]);
         }
       }
       __syncthreads();

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(1024) k_sym_tiles(
 // (even, odd) pairs; j records broadcast from shared memory (one-sided stages) or read in a
 // per-lane XOR order inside groups of 8 (two-sided stages, so the warp reduce-scatter of the
 // j-side needs no selects: lane l holds record (k ^ m_l), m_l = (l >> 2) & 7).
-template <int NT, int RP, int MINB, bool MINIMG, int G, bool PR>
+template <int NT, int RP, int MINB, bool MINIMG, int G>
 __global__ void __launch_bounds__(NT, MINB)
     k_landau_sym(const float4* __restrict__ xv, const float4* __restrict__ sw,
                  const int32_t* __restrict__ cell_start, const int32_t* __restrict__ sub_start,
@@ -284,22 +284,19 @@ __global__ void __launch_bounds__(NT, MINB)
           const float qe = rsqrtf(zze), qo = rsqrtf(zzo);
           const f2 rp = mk2(zze > kEps2 ? qe : 0.f, zzo > kEps2 ? qo : 0.f);
           const f2 cw = mul2(mk2(ce_, co_), rp);
-          const f2 nq = neg2(mul2(mul2(rp, rp), zu));
-          A0[r] = fma2(cw, fma2(nq, z0, u0), A0[r]);
-          A1[r] = fma2(cw, fma2(nq, z1, u1), A1[r]);
-          A2[r] = fma2(cw, fma2(nq, z2, u2), A2[r]);
+          const f2 q = mul2(mul2(rp, rp), zu);
+          A0[r] = fma2(cw, fnms2(q, z0, u0), A0[r]);
+          A1[r] = fma2(cw, fnms2(q, z1, u1), A1[r]);
+          A2[r] = fma2(cw, fnms2(q, z2, u2), A2[r]);
         }
       }
     } else {
       float* jp = &s_jp[q & 1][wid][0];
       for (int jb = 0; jb < d.cnt; jb += G) {
         float P0[G], P1[G], P2[G];
-        f2 PJ[3][4];
         const uint32_t gb = (sbase + (uint32_t)jb * sizeof(float4)) | mofs;
 #pragma unroll
-        for (int kq = 0; kq < G; ++kq) {
-          // PR: slots in the order 0, 4, 1, 5, ... so the xor-16 exchange folds each pair at once
-          const int k = PR ? ((kq >> 1) | ((kq & 1) << 2)) : kq;
+        for (int k = 0; k < G; ++k) {
           const uint32_t a = gb ^ (uint32_t)(k * sizeof(float4));
           const float4 A = lds128(a);
           const float4 B = lds128(a + kSwOfs);
@@ -323,8 +320,8 @@ __global__ void __launch_bounds__(NT, MINB)
             const float qe = rsqrtf(zze), qo = rsqrtf(zzo);
             const f2 rp = mk2(zze > kEps2 ? qe : 0.f, zzo > kEps2 ? qo : 0.f);
             const f2 cw = mul2(mk2(ce_, co_), rp);
-            const f2 nq = neg2(mul2(mul2(rp, rp), zu));
-            const f2 d0 = fma2(nq, z0, u0), d1 = fma2(nq, z1, u1), d2 = fma2(nq, z2, u2);
+            const f2 q = mul2(mul2(rp, rp), zu);
+            const f2 d0 = fnms2(q, z0, u0), d1 = fnms2(q, z1, u1), d2 = fnms2(q, z2, u2);
             A0[r] = fma2(cw, d0, A0[r]);
             A1[r] = fma2(cw, d1, A1[r]);
             A2[r] = fma2(cw, d2, A2[r]);
@@ -334,34 +331,16 @@ __global__ void __launch_bounds__(NT, MINB)
               J0 = fma2(cw, d0, J0); J1 = fma2(cw, d1, J1); J2 = fma2(cw, d2, J2);
             }
           }
-          if constexpr (PR) {
-            if ((kq & 1) == 0) {
-              PJ[0][kq >> 1] = J0; PJ[1][kq >> 1] = J1; PJ[2][kq >> 1] = J2;
-            } else {
-              PJ[0][kq >> 1] = add2(PJ[0][kq >> 1], shfl_xor2(J0, 16));
-              PJ[1][kq >> 1] = add2(PJ[1][kq >> 1], shfl_xor2(J1, 16));
-              PJ[2][kq >> 1] = add2(PJ[2][kq >> 1], shfl_xor2(J2, 16));
-            }
-          } else {
-            float e, o;
-            un2(J0, e, o); P0[k] = e + o;
-            un2(J1, e, o); P1[k] = e + o;
-            un2(J2, e, o); P2[k] = e + o;
-          }
-        }
-        if constexpr (PR) {
-          sym_reduce_scatter8_x2_tail<3>(PJ);
           float e, o;
-          un2(PJ[0][0], e, o); P0[0] = e + o;
-          un2(PJ[1][0], e, o); P1[0] = e + o;
-          un2(PJ[2][0], e, o); P2[0] = e + o;
-        } else {
-          float PP[3][G];
-#pragma unroll
-          for (int k = 0; k < G; ++k) { PP[0][k] = P0[k]; PP[1][k] = P1[k]; PP[2][k] = P2[k]; }
-          if constexpr (G == 8) sym_reduce_scatter8<3>(PP); else sym_reduce_scatter4<3>(PP);
-          P0[0] = PP[0][0]; P1[0] = PP[1][0]; P2[0] = PP[2][0];
+          un2(J0, e, o); P0[k] = e + o;
+          un2(J1, e, o); P1[k] = e + o;
+          un2(J2, e, o); P2[k] = e + o;
         }
+        float PP[3][G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) { PP[0][k] = P0[k]; PP[1][k] = P1[k]; PP[2][k] = P2[k]; }
+        if constexpr (G == 8) sym_reduce_scatter8<3>(PP); else sym_reduce_scatter4<3>(PP);
+        P0[0] = PP[0][0]; P1[0] = PP[1][0]; P2[0] = PP[2][0];
         const int cc = lane & (kLpr - 1);
         if (cc < 3) jp[(jb + m_l) * 3 + cc] = cc == 0 ? P0[0] : (cc == 1 ? P1[0] : P2[0]);
       }
@@ -435,12 +414,11 @@ constexpr size_t sym_smem_bytes(int NT) {
 // kernel configuration: threads per CTA, packed target pairs per thread, resident CTAs per SM
 struct SymCfg {
   int nt, rp, minb, g;  // g: records per j-side reduce-scatter group
-  bool pr = false;      // packed (f32x2) j-side reduce-scatter (g = 8)
   int ti() const { return nt * 2 * rp; }
 };
 constexpr SymCfg kSymCfgs[] = {{128, 2, 4, 8}, {128, 2, 3, 8}, {128, 3, 3, 8}, {256, 2, 2, 8},
                                {128, 3, 2, 8}, {128, 2, 5, 8}, {128, 2, 4, 4}, {128, 2, 5, 4},
-                               {128, 2, 6, 4}, {128, 2, 4, 8, true}, {128, 2, 5, 8, true}};
+                               {128, 2, 6, 4}};
 constexpr int kNumSymCfgs = sizeof(kSymCfgs) / sizeof(kSymCfgs[0]);
 
 SymCfg sym_cfg(int M) {
@@ -463,18 +441,18 @@ size_t spic_landau_sym_scratch_bytes(int64_t n, int32_t M, int32_t nsplit, int32
   return sym_layout(nullptr, n, M, nsplit, sym_cfg(M).ti(), 3, m_occ).bytes + 256;
 }
 
-template <int NT, int RP, int MINB, bool MINIMG, int G = 8, bool PR = false>
+template <int NT, int RP, int MINB, bool MINIMG, int G = 8>
 static void launch_sym(dim3 grid, cudaStream_t st, const float* xv, const float* sw,
                        const int32_t* cell_start, const int32_t* ssp, const SymScratch& s, int M,
                        int S, float L, float wie, float wie2, int nsplit, int split_fast,
                        int64_t n) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_landau_sym<NT, RP, MINB, MINIMG, G, PR>,
+    cudaFuncSetAttribute(k_landau_sym<NT, RP, MINB, MINIMG, G>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem_bytes(NT));
     attr = true;
   }
-  k_landau_sym<NT, RP, MINB, MINIMG, G, PR><<<grid, NT, sym_smem_bytes(NT), st>>>(
+  k_landau_sym<NT, RP, MINB, MINIMG, G><<<grid, NT, sym_smem_bytes(NT), st>>>(
       (const float4*)xv, (const float4*)sw, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag,
       M, S, L, wie, wie2, nsplit, split_fast, s.Upart, s.Jslot, n);
 }
@@ -508,10 +486,6 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
   const float Lf = (float)L;
   if (M <= 2)
     launch_sym<128, 2, 4, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
-  else if (cfg.pr && cfg.minb == 5)
-    launch_sym<128, 2, 5, false, 8, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
-  else if (cfg.pr)
-    launch_sym<128, 2, 4, false, 8, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.g == 4 && cfg.minb == 4)
     launch_sym<128, 2, 4, false, 4>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.g == 4 && cfg.minb == 5)

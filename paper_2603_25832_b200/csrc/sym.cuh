@@ -138,30 +138,6 @@ __device__ __forceinline__ void sym_reduce_scatter8(float (&P)[NC][8]) {
   for (int c = 0; c < NC; ++c) P[c][0] += __shfl_xor_sync(0xffffffffu, P[c][0], 1);
 }
 
-// Packed form of sym_reduce_scatter8 for (even target, odd target) partial pairs, reduced as
-// f32x2 (FADD2, two SHFLs per exchange); the caller folds the two halves of P[c][0] at the
-// end — 3 scalar FADDs per 8 records instead of 24 (the FMA pipe is the bound, SHFLs are not).
-// The xor-16 step is done by the caller as the records are produced (slot k += partner's slot
-// k + 4), so only 4 packed slots per component stay live; this is the rest (xor-8 ... xor-1).
-__device__ __forceinline__ f2 shfl_xor2(f2 a, int m) {
-  float lo, hi;
-  un2(a, lo, hi);
-  return mk2(__shfl_xor_sync(0xffffffffu, lo, m), __shfl_xor_sync(0xffffffffu, hi, m));
-}
-template <int NC>
-__device__ __forceinline__ void sym_reduce_scatter8_x2_tail(f2 (&P)[NC][4]) {
-#pragma unroll
-  for (int k = 0; k < 2; ++k)
-#pragma unroll
-    for (int c = 0; c < NC; ++c) P[c][k] = add2(P[c][k], shfl_xor2(P[c][k + 2], 8));
-#pragma unroll
-  for (int c = 0; c < NC; ++c) P[c][0] = add2(P[c][0], shfl_xor2(P[c][1], 4));
-#pragma unroll
-  for (int c = 0; c < NC; ++c) P[c][0] = add2(P[c][0], shfl_xor2(P[c][0], 2));
-#pragma unroll
-  for (int c = 0; c < NC; ++c) P[c][0] = add2(P[c][0], shfl_xor2(P[c][0], 1));
-}
-
 // Same over 4 records (lane l holds record k ^ m_l, m_l = (l >> 3) & 3): xor-16/8 exchanges
 // without selects, then xor-4/2/1 butterflies; every lane ends with the warp sums of record
 // m_l in P[c][0]. Half the live partials of the 8-record form for ~1.3x its shuffles.
