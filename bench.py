@@ -598,7 +598,7 @@ def hbm_microbench(torch, device, peak_gbs: float, n: int = 1 << 24, M: int = 10
     return res
 
 
-def build_dist_sim(wl: dict, seed: int, device, world: int):
+def build_dist_sim(wl: dict, seed: int, device, world: int, host_staged: bool = False):
     """The workload's own problem (n, M, L fixed: strong scaling, as BASELINE configs 3 and 4
     define their 2/4/8-GPU runs) decomposed into cell ranges, one per rank; the ranges are
     balanced on the initial cell counts."""
@@ -612,7 +612,7 @@ def build_dist_sim(wl: dict, seed: int, device, world: int):
     rng = np.random.default_rng(seed)
     x, v, w, b3 = sample_workload(wl, cfg, rng)
     grid = Grid(cfg.M, cfg.eta)
-    comm = Comm()
+    comm = Comm(host_staged=host_staged)
     cell = np.minimum(np.floor(x.astype(np.float32).astype(np.float64) / grid.eta).astype(np.int64) % cfg.M,
                       cfg.M - 1)
     part = CellPartition.balanced(np.bincount(cell, minlength=cfg.M), world)
@@ -644,6 +644,44 @@ def live_pairs(sim, dist_mode: bool) -> float:
     if getattr(sim, "ci_own", None) is None:
         return 0.0
     return float(count_live_pairs(sim.ci_own, sim.buf.view(sim.n_own, sim.uniform_w), sim.grid))
+
+
+def allreduce_max(dist, t, host_staged: bool):
+    """MAX over ranks of a small device tensor (host-staged for the gloo test backend)."""
+    if host_staged:
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t
+
+
+def evaluated_pairs(cell_start, sub_start, M: int, S: int, TI: int = 512) -> float:
+    """Unordered pairs the antisymmetric kernel evaluates in one launch ("count
+    41 FLOP per evaluated unordered pair"): per target tile [t0, t1) of a cell, its forward
+    window (the rest of the cell, len1, plus the culled prefix of the next cell, len2 — the
+    k_sym_tiles rule, landau_sym.cu) and the tile's own unordered pairs (the diagonal block,
+    counted once although the kernel evaluates it one-sided in both orders). Host numpy on
+    the cell / sub-cell starts; M >= 3."""
+    cs = np.asarray(cell_start, dtype=np.int64)
+    ss = np.asarray(sub_start, dtype=np.int64) if S > 1 else None
+    total = 0.0
+    for c in range(M):
+        a, e = int(cs[c]), int(cs[c + 1])
+        cn = (c + 1) % M
+        for t0 in range(a, e, TI):
+            t1 = min(t0 + TI, e)
+            tl = t1 - t0
+            if ss is not None:
+                sub = ss[c * S:(c + 1) * S]
+                b = int(np.searchsorted(sub, t1 - 1, side="right")) - 1
+                hs = min(S - 1, b + 1)
+                len2 = int(ss[cn * S + hs + 1] - cs[cn])
+            else:
+                len2 = int(cs[cn + 1] - cs[cn])
+            total += tl * ((e - t1) + len2) + tl * (tl - 1) / 2.0
+    return total
 
 
 def main():
@@ -682,6 +720,13 @@ def main():
 
     from paper_2603_25832_b200 import _lib
     
+    # SPIC_DIST_BACKEND=gloo (test only): every rank on cuda:0 with host-staged collectives, so
+    # the multi-rank bench path can be exercised on one GPU (NCCL refuses two ranks per device);
+    # its timings are not bench numbers
+    backend = os.environ.get("SPIC_DIST_BACKEND", "nccl")
+    share_gpu = backend == "gloo"
+    if share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     # SPIC_FORCE_DIST=1: the decomposed (NCCL) path even at one rank — a one-GPU check of the
@@ -694,13 +739,17 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     _lib.load(build_if_missing=False)
 
     # N = 1: the single-GPU engine. N > 1: the cell-range decomposition of the same problem
     # (strong scaling) over NCCL.
-    sim = build_dist_sim(wl, args.seed, device, world) if dist_mode else build_sim(wl, args.seed, device)
+    sim = (build_dist_sim(wl, args.seed, device, world, host_staged=share_gpu) if dist_mode
+           else build_sim(wl, args.seed, device))
     n = wl["n"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
 
@@ -752,10 +801,17 @@ def main():
     coll_ms = [a.elapsed_time(b) for a, b in sim.collision_events]
     live1 = live_pairs(sim, dist_mode)
     live = 0.5 * (live0 + live1)
+    evald = None
+    if not dist_mode and not os.environ.get("SPIC_LANDAU_VARIANT") and sim.grid.M >= 3:
+        try:
+            evald = evaluated_pairs(sim.ci.cell_start.cpu().numpy(), sim.ci.sub_start.cpu().numpy(),
+                                    sim.grid.M, sim.S)
+        except Exception:  # noqa: BLE001
+            evald = None
     t = torch.tensor([total_ms, statistics.mean(coll_ms) if coll_ms else float("nan")],
                      dtype=torch.float64, device=device)
     if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce_max(dist, t, share_gpu)
         dist.barrier()
     total_ms, coll_avg_ms = float(t[0]), float(t[1])
     value = n * args.steps / (total_ms * 1e-3)  # n = the whole job's particles (strong scaling)
@@ -786,7 +842,7 @@ def main():
         e1.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
         if dist:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            allreduce_max(dist, te, share_gpu)
         e2e = {"value": n * args.steps / (float(te[0]) * 1e-3), "unit": "particle-steps/s",
                "h2d_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4),
                "d2h_bytes_per_step": int(xh.numel() * 4 + vh.numel() * 4 + dh.numel() * 8
@@ -817,7 +873,7 @@ def main():
             e1.record()
             e1.synchronize()
             te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            allreduce_max(dist, te, share_gpu)
             nb = int(statistics.mean(counts)) * 4 * (1 + dv)
             e2e = {"value": n * args.steps / (float(te[0]) * 1e-3),
                    "unit": "particle-steps/s", "h2d_bytes_per_step": nb,
@@ -834,7 +890,7 @@ def main():
         silu_rf = silu_kernel_roofline(torch, device, sim, wl, args.workload)
         t = torch.tensor([silu_rf["launch_ms"]], dtype=torch.float64, device=device)
         if dist:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            allreduce_max(dist, t, share_gpu)
         silu_rf["launch_ms"] = float(t[0])
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "landau_traffic.json")
@@ -849,7 +905,8 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded reference sampler; random-init score net, no pretraining)",
         "config": bench_config(wl, world),
-        "engine": {"sub_cells": sim.S, "cuda_graph": use_graph, "dist_path": dist_mode},
+        "engine": {"sub_cells": sim.S, "cuda_graph": use_graph, "dist_path": dist_mode,
+                   "backend": (backend if dist_mode else None)},
         "pair_interactions_per_s": world * live / (coll_avg_ms * 1e-3),
         "live_pairs_per_step": live,
         "collision_ms": coll_avg_ms,
@@ -858,6 +915,9 @@ def main():
                           "frac": achieved / peak, "traffic": traffic,
                           "ordered_equivalent_frac": FLOP_PER_PAIR * live / (coll_avg_ms * 1e-3)
                           / 1e12 / peak,
+                          "evaluated_unordered_pairs": evald,
+                          "frac_evaluated": (FLOP_PER_UPAIR * evald / (coll_avg_ms * 1e-3) / 1e12
+                                             / peak) if evald else None,
                           "flop_per_launch": flop_launch, "launch_ms": coll_avg_ms,
                           "launches_per_step": 1,
                           "peak_source": "measured in-run: spic_fp32_probe (FFMA2 chains, "

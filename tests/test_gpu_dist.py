@@ -34,12 +34,19 @@ def _free_port():
 
 
 def _setup(estimator, n=20000, M=16, seed=3):
-    """Global ensemble, fields and estimator factory shared by both engines."""
+    """Global ensemble, fields and estimator factory shared by both engines. Kinds ending in
+    "-rebal" draw the density 1 + 0.6 sin(2 pi x / L) (crowded in the first half of the box),
+    so an equal-cell partition is unbalanced and the ranks' rebalancing moves the boundaries."""
     from paper_2603_25832_b200.pic import Grid
 
     L = 4 * math.pi
     rng = np.random.default_rng(seed)
-    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    u = rng.uniform(0, 1, n)
+    if estimator.endswith("-rebal"):  # rejection sampling, first n accepted of 3n candidates
+        c = rng.uniform(0, 1, 3 * n)
+        keep = rng.uniform(0, 1.6, 3 * n) < 1.0 + 0.6 * np.sin(2 * np.pi * c)
+        u = c[keep][:n]
+    x = (L * u).astype(np.float32).astype(np.float64)
     x[x >= L] = 0
     v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
     w = np.full(n, L / n)
@@ -61,6 +68,7 @@ def _fields(x, v, w, grid, L):
 def _estimator(kind, grid, L):
     from paper_2603_25832_b200.score import BlobEstimator, MlpScoreNet, SbtmEstimator
 
+    kind = kind.replace("-rebal", "")
     r = np.random.default_rng(5)
     if kind == "sbtm":
         return SbtmEstimator(MlpScoreNet.init_glorot(3, 32, r), L, 3, r, lr=1e-3,
@@ -109,20 +117,20 @@ def _body(rank, world, port, kind, out_dir):
                              dt=0.05, nu=0.1, mode="VPL", gamma=-3.0,
                              estimator=_estimator(kind, grid, L),
                              comm=Comm(host_staged=True), partition=part, n_global=x.shape[0],
-                             max_rows=8)
+                             max_rows=8, rebalance_every=1 if kind.endswith("-rebal") else 0)
         for k in range(1, STEPS + 1):
             sim.step(k)
         sim.check()
         gid, xs, vs = sim.gather_state()
         parts = [None] * world
-        dist.all_gather_object(parts, (gid, xs, vs, sim.host_syncs))
+        dist.all_gather_object(parts, (gid, xs, vs, sim.host_syncs, sim.part.bounds.tolist()))
         if rank == 0:
             D = sim.diag[1:STEPS + 1].cpu().numpy()
             g = np.concatenate([p[0] for p in parts])
             np.savez(os.path.join(out_dir, "dist.npz"), diag=D, gid=g,
                      x=np.concatenate([p[1] for p in parts]),
                      v=np.concatenate([p[2] for p in parts]),
-                     syncs=np.array([p[3] for p in parts]))
+                     syncs=np.array([p[3] for p in parts]), bounds=np.array(parts[0][4]))
     finally:
         dist.destroy_process_group()
 
@@ -137,8 +145,8 @@ def lib():
     return _lib
 
 
-@pytest.mark.parametrize("world", [1, 2, 3])
-@pytest.mark.parametrize("kind", ["sbtm", "silu", "blob"])
+@pytest.mark.parametrize("world,kind", [(w, k) for k in ("sbtm", "silu", "blob") for w in (1, 2, 3)]
+                         + [(2, "sbtm-rebal"), (3, "sbtm-rebal")])
 def test_decomposed_step_matches_single_gpu_engine(lib, tmp_path, world, kind):
     import torch.multiprocessing as mp
 
@@ -161,6 +169,10 @@ def test_decomposed_step_matches_single_gpu_engine(lib, tmp_path, world, kind):
     assert np.max(np.abs(res["v"] - v_ref[gid])) <= 2e-4
     if world > 1:  # one host synchronisation per step (the received counts)
         assert np.all(res["syncs"] == STEPS)
+    if kind.endswith("-rebal"):  # the skewed ensemble moved the equal-cell boundaries
+        from paper_2603_25832_b200.parallel import CellPartition
+
+        assert not np.array_equal(res["bounds"], CellPartition.equal(16, world).bounds)
 
 
 def test_decomposed_host_buffer_step_equals_device_step(lib):
