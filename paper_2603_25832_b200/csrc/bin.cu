@@ -285,7 +285,7 @@ static RadixPlan radix_plan(int64_t n, int M, int S) {
   r.passes = r.bits <= 8 ? 1 : 2;
   r.n_tiles = (int)std::max<int64_t>(1, (n + kRxT - 1) / kRxT);
   r.counts_elems = (size_t)kRxB * r.n_tiles;
-  r.nb_scan = (r.counts_elems + kScanChunk - 1) / kScanChunk;
+  r.nb_scan = (size_t)kRxB * ((r.n_tiles + 63) / 64);  // column-scan block sums (kRxR = 64)
   return r;
 }
 
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) k_radix_count(const float* __restrict__ x
   }
   __syncthreads();
   for (int k = threadIdx.x; k < kRxB; k += blockDim.x)
-    counts[(size_t)k * n_tiles + blockIdx.x] = hist[k];
+    counts[(size_t)blockIdx.x * kRxB + k] = hist[k];  // tile-major row: one coalesced store
 }
 
 // Stable scatter of one digit pass: warp w of a tile owns records [32 G w, 32 G (w+1)); per-warp
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kRxW * 32) k_radix_scatter(
     if (wbase + g * 32 + lane < n) atomicAdd(&hist[wid][(kw[g] >> shift) & mask], 1);
   __syncthreads();
   for (int k = threadIdx.x; k < kRxB; k += blockDim.x) {
-    int run = scanned[(size_t)k * n_tiles + blockIdx.x];
+    int run = scanned[(size_t)blockIdx.x * kRxB + k];
 #pragma unroll
     for (int q = 0; q < kRxW; ++q) {
       const int t = hist[q][k];
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kRxW * 32) k_radix_scatter_s(
     for (int q = 0; q < wid; ++q) wpre += s_ws[q];
     const int lb = wpre + inc - tot;
     s_lb[d] = lb;
-    s_gb[d] = scanned[(size_t)d * n_tiles + blockIdx.x];
+    s_gb[d] = scanned[(size_t)blockIdx.x * kRxB + d];
     int run = lb;
 #pragma unroll
     for (int q = 0; q < kRxW; ++q) {
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kRxW * 32) k_radix_scatter_b(
     const float* __restrict__ x, const float* __restrict__ v, int64_t ldv,
     const float* __restrict__ w, int dv, double L) {
   extern __shared__ unsigned char s_dyn_rb[];
-  unsigned char* sb = (unsigned char*)(((uintptr_t)s_dyn_rb + 127) & ~(uintptr_t)127);
+  unsigned char* sb = s_dyn_rb + ((128u - (uint32_t)((uintptr_t)s_dyn_rb & 127u)) & 127u);
   uint32_t* s_key = reinterpret_cast<uint32_t*>(sb);                      // [kRxT]
   int32_t* s_i = reinterpret_cast<int32_t*>(s_key + kRxT);                // idx (1) / x (0, 2)
   float4* s_rec = reinterpret_cast<float4*>(s_i + kRxT);                  // rec (1)
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(kRxW * 32) k_radix_scatter_b(
     for (int q = 0; q < wid; ++q) wpre += s_ws[q];
     const int lb = wpre + inc - tot;
     s_lb[d] = lb;
-    s_gb[d] = scanned[(size_t)d * n_tiles + blockIdx.x];
+    s_gb[d] = scanned[(size_t)blockIdx.x * kRxB + d];
     int run = lb;
 #pragma unroll
     for (int q = 0; q < kRxW; ++q) {
@@ -699,6 +699,65 @@ __global__ void __launch_bounds__(kRxW * 32) k_radix_scatter_b(
       if (w_out) w_out[pos] = wv;
     } else if (w_out) {
       reinterpret_cast<float4*>(w_out)[pos] = make_float4(0.f, 0.f, 0.f, wv);
+    }
+  }
+}
+
+// Exclusive (digit, tile)-order scan of the tile-major radix count table c[tile][digit]:
+//   offset[t][d] = sum_{d' < d} total[d'] + sum_{t' < t} c[t'][d].
+// Two launches, every table access a coalesced 1-KB row: column sums per block of kRxR tiles,
+// then per block the apply, which first derives its own prefix and the digit totals from all
+// block sums (L2-resident, nb x 1 KB) and scans the totals over the digits in the CTA.
+constexpr int kRxR = 64;  // tiles per column-scan block
+__global__ void __launch_bounds__(kRxB) k_rx_colsum(const int32_t* __restrict__ c, int n_tiles,
+                                                   int32_t* __restrict__ bsum) {
+  const int d = threadIdx.x, t0 = blockIdx.x * kRxR, t1 = min(t0 + kRxR, n_tiles);
+  int s = 0;
+  for (int tb = t0; tb < t1; tb += 16) {
+    int v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = tb + i < t1 ? c[(size_t)(tb + i) * kRxB + d] : 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += v[i];
+  }
+  bsum[(size_t)blockIdx.x * kRxB + d] = s;
+}
+__global__ void __launch_bounds__(kRxB) k_rx_colscan_apply(int32_t* __restrict__ c, int n_tiles,
+                                                          const int32_t* __restrict__ bsum,
+                                                          int nb) {
+  __shared__ int ws[kRxB / 32];
+  const int d = threadIdx.x, lane = d & 31, wid = d >> 5;
+  int pre = 0, tot = 0;
+  for (int bb = 0; bb < nb; bb += 16) {
+    int v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = bb + i < nb ? bsum[(size_t)(bb + i) * kRxB + d] : 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      pre += bb + i < (int)blockIdx.x ? v[i] : 0;
+      tot += v[i];
+    }
+  }
+  int inc = tot;  // exclusive scan of the digit totals across the CTA
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) ws[wid] = inc;
+  __syncthreads();
+  int wpre = 0;
+  for (int q = 0; q < wid; ++q) wpre += ws[q];
+  int run = wpre + inc - tot + pre;
+  const int t0 = blockIdx.x * kRxR, t1 = min(t0 + kRxR, n_tiles);
+  for (int tb = t0; tb < t1; tb += 16) {  // 16 independent loads in flight, then the stores
+    int v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = tb + i < t1 ? c[(size_t)(tb + i) * kRxB + d] : 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (tb + i < t1) c[(size_t)(tb + i) * kRxB + d] = run;
+      run += v[i];
     }
   }
 }
@@ -798,11 +857,11 @@ static int bin_radix(const float* x, const float* v, int64_t ldv, const float* w
   int32_t* bsum = counts + r.counts_elems;
   const double L = (double)M * eta;
   const unsigned nt = (unsigned)r.n_tiles;
+  const int nbk = (r.n_tiles + kRxR - 1) / kRxR;
   auto scan = [&]() {
-    k_scan_reduce<<<(unsigned)r.nb_scan, kScanThreads, 0, st>>>(counts, r.counts_elems, bsum);
-    k_scan_blocksums<<<1, kScanThreads, 0, st>>>(bsum, r.nb_scan);
-    k_scan_apply<<<(unsigned)r.nb_scan, kScanThreads, 0, st>>>(counts, r.counts_elems, bsum);
-    for (int k = 0; k < 3; ++k) spic::count_launch();
+    k_rx_colsum<<<(unsigned)nbk, kRxB, 0, st>>>(counts, r.n_tiles, bsum);
+    k_rx_colscan_apply<<<(unsigned)nbk, kRxB, 0, st>>>(counts, r.n_tiles, bsum, nbk);
+    for (int k = 0; k < 2; ++k) spic::count_launch();
   };
   // "0": the direct-scatter kernels, "1": staged with plain loads, default: staged with bulk
   // copies when the input planes are 16-B aligned (A/B)

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr int NW = NT / 32;
   constexpr int NC = kBlobNC;
   extern __shared__ unsigned char s_dyn[];
-  unsigned char* s_base = (unsigned char*)(((uintptr_t)s_dyn + 127) & ~(uintptr_t)127);
+  unsigned char* s_base = s_dyn + ((128u - (uint32_t)((uintptr_t)s_dyn & 127u)) & 127u);
   auto s_rec = reinterpret_cast<float4(*)[kSymTJ]>(s_base);
   auto s_jp = reinterpret_cast<float(*)[NW][kSymTJ * NC]>(s_base + sizeof(float4) * kSymStages * kSymTJ);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_base + sizeof(float4) * kSymStages * kSymTJ +

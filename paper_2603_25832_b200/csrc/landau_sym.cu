@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(NT, MINB)
   // dynamic shared memory (128-aligned by hand): stages of [xv records | sw records] (the sw
   // half at a fixed byte offset), the double-buffered per-warp j-side sums, the mbarriers
   extern __shared__ unsigned char s_dyn[];
-  unsigned char* s_base = (unsigned char*)(((uintptr_t)s_dyn + 127) & ~(uintptr_t)127);
+  unsigned char* s_base = s_dyn + ((128u - (uint32_t)((uintptr_t)s_dyn & 127u)) & 127u);
   auto s_rec = reinterpret_cast<float4(*)[2][kSymTJ]>(s_base);
   auto s_jp = reinterpret_cast<float(*)[NW][kSymTJ * 3]>(s_base + sizeof(float4) * kSymStages * 2 * kSymTJ);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_base + sizeof(float4) * kSymStages * 2 * kSymTJ +

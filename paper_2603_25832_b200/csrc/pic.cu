@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kDepThreads) k_deposit_bulk(
     const int32_t* __restrict__ cell_start, int M, int CH, double inv_eta, float uniform_w,
     double* __restrict__ partials, int rs, int nstages) {
   extern __shared__ unsigned char s_dyn[];
-  unsigned char* s_base = (unsigned char*)(((uintptr_t)s_dyn + 127) & ~(uintptr_t)127);
+  unsigned char* s_base = s_dyn + ((128u - (uint32_t)((uintptr_t)s_dyn & 127u)) & 127u);
   float4* s_x = reinterpret_cast<float4*>(s_base);                 // [stage][rs]
   float4* s_w = s_x + (size_t)nstages * rs;                        // [stage][rs] (NONUNI)
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_x + (size_t)nstages * rs * (NONUNI ? 2 : 1));
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kDepThreads + 32) k_deposit_bulk_ws(
     const int32_t* __restrict__ cell_start, int M, int CH, double inv_eta, float uniform_w,
     double* __restrict__ partials, int rs, int nstages) {
   extern __shared__ unsigned char s_dyn[];
-  unsigned char* s_base = (unsigned char*)(((uintptr_t)s_dyn + 127) & ~(uintptr_t)127);
+  unsigned char* s_base = s_dyn + ((128u - (uint32_t)((uintptr_t)s_dyn & 127u)) & 127u);
   float4* s_x = reinterpret_cast<float4*>(s_base);
   float4* s_w = s_x + (size_t)nstages * rs;
   uint64_t* s_full = reinterpret_cast<uint64_t*>(s_x + (size_t)nstages * rs * (NONUNI ? 2 : 1));
