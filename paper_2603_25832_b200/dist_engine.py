@@ -39,6 +39,7 @@ import torch
 from . import _lib
 from .collision import CellIndex, auto_sub_cells
 from .config import DeviceOptions
+from .engine import nvtx
 from .parallel import CellPartition, Comm
 from .pic import FIELD_NONE, FIELD_VML, FIELD_VPL, Grid, deposit_from_index, raise_for_flags
 from .score import BlobEstimator, SbtmEstimator, blob_sorted
@@ -254,10 +255,16 @@ class DistSimulation:
         self._last_row = row
         b, n = self.cur, self.n
         # 1. push own particles
+        rng = nvtx("push")
+        rng.__enter__()
         _lib.call("spic_push", _lib.ptr(b.x), _lib.ptr(b.vp), b.cap, n, dv, _lib.ptr(f.E1),
                   _lib.ptr(f.E2), _lib.ptr(f.B3), g.M, float(g.eta), self.dt, _lib.ptr(self.flags), st)
+        rng.__exit__(None, None, None)
         # 2. bin them where they are (R0), deposit, one allreduce of [rho; J], field step
-        ci0 = self._bin(b, n, self.idx0)
+        with nvtx("bin"):
+            ci0 = self._bin(b, n, self.idx0)
+        rng = nvtx("deposit")
+        rng.__enter__()
         self._n0 = n
         gm = self.grid_moments
         deposit_from_index(ci0, b.view(n, self.uniform_w), g,
@@ -270,6 +277,7 @@ class DistSimulation:
         _lib.call("spic_field_step", _lib.ptr(f.E1), _lib.ptr(f.E2), _lib.ptr(f.B3), _lib.ptr(f.J),
                   g.M, float(g.eta), self.dt, fmode, _lib.ptr(d[0:3]), _lib.ptr(self.flags), st)
         self.steps_done += 1
+        rng.__exit__(None, None, None)
         if not (self.nu > 0 and self.est is not None):
             buf, nb = _lib.scratch("moments", _lib.query("spic_moments_scratch_bytes", n))
             _lib.call("spic_moments", _lib.ptr(b.vp), b.cap, _lib.ptr(b.w), n, dv,
@@ -278,6 +286,8 @@ class DistSimulation:
             comm.allreduce_(d[3:9])
             return
         # 3. boundary messages (fixed size) to the ring neighbours; counts staged for the host
+        rng = nvtx("exchange")
+        rng.__enter__()
         if R > 1:
             self._pack(0, ci0)
             self._pack(1, ci0)
@@ -288,7 +298,10 @@ class DistSimulation:
             self._stage[8:10].copy_(torch.index_select(ci0.cell_start, 0, self._cs_idx))
             self._stage_host.copy_(self._stage, non_blocking=True)
             self._ready.record()
+        rng.__exit__(None, None, None)
         # 4. score training on R0 (gradient rows allreduced before every finalize)
+        rng = nvtx("score")
+        rng.__enter__()
         if self.trainer is not None:
             gid_sorted = b.gid[:n][ci0.perm[:n].long()] if self.trainer.mode() == 2 else None
             self.trainer.run(n, ci=ci0, flags=self.flags,
@@ -322,7 +335,10 @@ class DistSimulation:
             blob_sorted(ci, p_all, g, self.est.bandwidth, self.flags, self.bad_pid, self.h_cell)
         else:
             raise TypeError("unsupported estimator for the device step engine")
+        rng.__exit__(None, None, None)
         # 7. pair kernel over the owned targets, epilogue into the next step's buffers
+        rng = nvtx("collide")
+        rng.__enter__()
         if self.U.shape[1] < n_u:
             self.U = torch.empty(dv, _round_up(int(n_u * 1.25) + 1024, 64), dtype=torch.float32,
                                  device=self.dev)
@@ -348,6 +364,7 @@ class DistSimulation:
                   _lib.ptr(nx.x), _lib.ptr(nx.vp), nx.cap, _lib.ptr(nx.w), _lib.ptr(nx.gid),
                   _lib.ptr(d[3:9]), _lib.ptr(self.flags), _lib.ptr(self._epi), self._epi_n, st)
         comm.allreduce_(d[3:9])
+        rng.__exit__(None, None, None)
         self.cur, self.nxt = nx, b
         self.n = n_next
 

@@ -19,6 +19,8 @@ error conditions in `flags`. The host reads both only when asked (`records`, `ch
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -30,6 +32,27 @@ from .score import BlobEstimator, SbtmEstimator, blob_sorted
 from .state import DiagnosticsRecord, FieldState, ParticleEnsemble, new_flags
 
 DIAG_W = 9
+
+
+class _Nvtx:
+    """Per-stage NVTX ranges (SURVEY §5 tracing; the reference's stage hook is run.py:83-105):
+    named ranges "push", "bin", "deposit", "score", "collide" around each stage's launches,
+    visible in nsys / ncu --nvtx timelines. Off unless SPIC_NVTX=1 (host-side markers only,
+    nothing is added to the device stream or to a captured graph)."""
+
+    def __call__(self, name: str):
+        return torch.cuda.nvtx.range(name) if os.environ.get("SPIC_NVTX") == "1" else _NullCtx()
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+nvtx = _Nvtx()
 
 
 class Simulation:
@@ -91,23 +114,30 @@ class Simulation:
         p, g, ci, f = self.p, self.grid, self.ci, self.f
         n, dv = p.n, p.dv
         st = _lib.stream_handle()
-        _lib.call("spic_push", _lib.ptr(p.x), _lib.ptr(p.vp), n, n, dv, _lib.ptr(f.E1),
-                  _lib.ptr(f.E2), _lib.ptr(f.B3), g.M, float(g.eta), self.dt, _lib.ptr(self.flags),
-                  st)
-        build_cell_index(p, g, self.S, out=ci)
+        with nvtx("push"):
+            _lib.call("spic_push", _lib.ptr(p.x), _lib.ptr(p.vp), n, n, dv, _lib.ptr(f.E1),
+                      _lib.ptr(f.E2), _lib.ptr(f.B3), g.M, float(g.eta), self.dt,
+                      _lib.ptr(self.flags), st)
+        with nvtx("bin"):
+            build_cell_index(p, g, self.S, out=ci)
         d = self.diag[row]
         d.zero_()
         fmode = FIELD_VML if self.mode == "VML" else FIELD_VPL
-        deposit_from_index(ci, p, g, fields=f, field_mode=fmode, dt=self.dt, diag_out=d[0:3],
-                           flags=self.flags)
+        with nvtx("deposit"):
+            deposit_from_index(ci, p, g, fields=f, field_mode=fmode, dt=self.dt, diag_out=d[0:3],
+                               flags=self.flags)
         if self.nu > 0 and self.est is not None:
-            if self.trainer is not None:
-                self.trainer.run(n, ci=ci, flags=self.flags, draw=draw)
-                self.est.estimate_sorted(ci, n)
-            elif isinstance(self.est, BlobEstimator):
-                blob_sorted(ci, p, g, self.est.bandwidth, self.flags, self.bad_pid, self.h_cell)
-            else:
-                raise TypeError("unsupported estimator for the device step engine")
+            with nvtx("score"):
+                if self.trainer is not None:
+                    self.trainer.run(n, ci=ci, flags=self.flags, draw=draw)
+                    self.est.estimate_sorted(ci, n)
+                elif isinstance(self.est, BlobEstimator):
+                    blob_sorted(ci, p, g, self.est.bandwidth, self.flags, self.bad_pid,
+                                self.h_cell)
+                else:
+                    raise TypeError("unsupported estimator for the device step engine")
+            collide = nvtx("collide")
+            collide.__enter__()
             ev = None
             if self.time_collision:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -120,6 +150,7 @@ class Simulation:
                       _lib.ptr(ci.perm), n, dv, float(self.nu * self.dt), _lib.ptr(p.vp), n, None,
                       n, _lib.ptr(d[3:8]), _lib.ptr(self.flags), _lib.ptr(self._epi), self._epi_n,
                       st)
+            collide.__exit__(None, None, None)
         else:
             buf, nb = _lib.scratch("moments", _lib.query("spic_moments_scratch_bytes", n))
             _lib.call("spic_moments", _lib.ptr(p.vp), n, _lib.ptr(p.w), n, dv, float(p.uniform_w),

@@ -1036,3 +1036,32 @@ def test_config4_size_binning_deposit_push(spic):
     d = np.abs(x2[idx] - xo)
     assert np.max(np.minimum(d, L - d)) <= 1e-5
     assert np.max(np.abs(p.vp.cpu().numpy()[:, idx].T - vo)) <= 1e-5
+
+
+def test_engine_step_with_nvtx_ranges(spic, monkeypatch):
+    """SPIC_NVTX=1 wraps every stage of the device step in a named NVTX range (push, bin,
+    deposit, score, collide); the step's results are unchanged (host-side markers only)."""
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
+    from paper_2603_25832_b200.score import BlobEstimator
+    from paper_2603_25832_b200.state import FieldState, ParticleEnsemble
+
+    rng = np.random.default_rng(2)
+    n, M, L = 4096, 16, 4 * math.pi
+    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SPIC_NVTX", flag)
+        p = ParticleEnsemble.from_arrays(x, v, np.full(n, L / n))
+        grid = Grid(M, L / M)
+        rho, _ = deposit(p, grid)
+        rho_ion = float(rho.sum()) * grid.eta / L
+        f = FieldState.zeros(M, 3, rho_ion)
+        f.E1.copy_(poisson_solve(rho, rho_ion, grid))
+        sim = Simulation(p, f, grid, dt=0.05, nu=0.1, mode="VPL", gamma=-3.0,
+                         estimator=BlobEstimator(grid, None), max_rows=4)
+        sim.step(1)
+        sim.check()
+        outs.append((p.v.cpu().numpy().copy(), sim.diag[1].cpu().numpy().copy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
