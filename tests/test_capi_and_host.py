@@ -92,3 +92,47 @@ def test_config_layering_and_errors():
         build_config(overrides=dict(k=0.3))
     with pytest.raises(ValueError, match="gamma must equal"):
         build_config(overrides=dict(gamma=-2.0))
+
+
+@pytest.mark.skipif(shutil.which("nvcc") is None and not os.path.exists("/usr/local/cuda/bin/nvcc"),
+                    reason="nvcc not available")
+def test_capi_rejects_invalid_arguments_before_any_launch():
+    """The boundary's error behaviour (include/scorepic_b200.h status codes): invalid sizes,
+    unsupported key ranges and short scratch buffers return SPIC_ERR_* before any device
+    work, so these calls are safe without a GPU."""
+    from paper_2603_25832_b200 import _lib
+
+    L = _lib.load()
+    ERR_ARG, ERR_SCRATCH, ERR_UNSUP = -1, -2, -3
+    null = None
+    # binning: dv, M, n out of range; M * S beyond the 15-bit key; scratch too small
+    assert L.spic_bin(null, null, 0, null, 10, 4, 0.1, 8, 1, null, null, null, null, null, null,
+                      0, null) == ERR_ARG
+    assert L.spic_bin(null, null, 0, null, 10, 3, 0.1, 0, 1, null, null, null, null, null, null,
+                      0, null) == ERR_ARG
+    assert L.spic_bin(null, null, 0, null, -1, 3, 0.1, 8, 1, null, null, null, null, null, null,
+                      0, null) == ERR_ARG
+    assert L.spic_bin(null, null, 0, null, 10, 3, 0.1, 1024, 64, null, null, null, null, null,
+                      null, 0, null) == ERR_UNSUP
+    need = L.spic_bin_scratch_bytes(1 << 20, 128, 32)
+    assert L.spic_bin(null, null, 0, null, 1 << 20, 3, 0.1, 128, 32, null, null, null, null,
+                      null, null, need - 1, null) == ERR_SCRATCH
+    # pair kernel: cell range out of order, dv, scratch
+    assert L.spic_landau_range(null, null, 100, 3, null, null, 8, 1, 0.1, -3.0, 0.1, 0, 5, 3,
+                               null, null, 1 << 30, null) == ERR_ARG
+    assert L.spic_landau_range(null, null, 100, 4, null, null, 8, 1, 0.1, -3.0, 0.1, 0, 0, 8,
+                               null, null, 1 << 30, null) == ERR_ARG
+    assert L.spic_landau(null, null, 1 << 20, 3, null, null, 128, 32, 0.1, -3.0, 0.1, 0, null,
+                         null, 0, null) == ERR_SCRATCH
+    # push: eta, M
+    assert L.spic_push(null, null, 0, 10, 3, null, null, null, 8, 0.0, 0.05, null, null) == ERR_ARG
+    assert L.spic_push(null, null, 0, 10, 3, null, null, null, 0, 0.1, 0.05, null, null) == ERR_ARG
+    # decomposition messages: cell bounds outside [0, M], negative row counts
+    import ctypes
+
+    int4 = ctypes.c_int32 * 4
+    bad, ok = int4(0, 9, 0, 0), int4(0, 2, 0, 0)
+    assert L.spic_dist_pack(null, null, 0, 3, null, 0.1, null, null, null, 8,
+                            ctypes.cast(bad, ctypes.c_void_p), ctypes.cast(ok, ctypes.c_void_p),
+                            16, null, null) == ERR_ARG
+    assert L.spic_dist_unpack(null, -1, 0, null, null, 0, 3, null, null, null) == ERR_ARG
