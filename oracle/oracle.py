@@ -456,3 +456,30 @@ def full_step(state: dict, *, eta: float, M: int, dt: float, nu: float, mode: st
         tick("collide", t0)
     state.update(x=x, v=v, E1=E1, E2=E2, B3=B3, rho=rho, J=J)
     return diagnostics(v, state["w"], E1, E2, B3, eta, nu=nu, U=U, s=s)
+
+
+# ------------------------------------------------------------------------------------------
+# Long-time equilibrium oracles (ref: equilibrium.py:24-55), used by the acceptance tests
+# ------------------------------------------------------------------------------------------
+
+def vpl_equilibrium(initial_energy: float, initial_momentum, rho_ion: float, volume: float):
+    """Electrostatic steady state (ref: equilibrium.py:40-55): drift u = P0 / (rho_ion |Omega|),
+    T_inf = 2 / (dv rho_ion |Omega|) (E0 - rho_ion |u|^2 |Omega| / 2). Returns (T_inf, u)."""
+    P0 = np.asarray(initial_momentum, dtype=np.float64)
+    dv = P0.shape[0]
+    u = P0 / (rho_ion * volume)
+    T = 2.0 / (dv * rho_ion * volume) * (initial_energy - 0.5 * rho_ion * float(u @ u) * volume)
+    if not T > 0:
+        raise ValueError("inconsistent energy accounting")
+    return T, u
+
+
+def vml_equilibrium(initial_energy: float, B_init_mean, rho_ion: float, volume: float,
+                    dv: int = 3):
+    """Electromagnetic steady state (ref: equilibrium.py:24-37): zero drift, B_inf = mean B(0),
+    T_inf = 2 / (dv rho_ion |Omega|) (E0 - |B_inf|^2 |Omega| / 2). Returns (T_inf, B_inf)."""
+    B = np.asarray(B_init_mean, dtype=np.float64).reshape(3)
+    T = 2.0 / (dv * rho_ion * volume) * (initial_energy - 0.5 * float(B @ B) * volume)
+    if not T > 0:
+        raise ValueError("inconsistent energy accounting")
+    return T, B

@@ -368,6 +368,28 @@ def gen_score_test():
          mse=np.array(rep["blob"]["mse"]))
 
 
+def gen_equilibrium():
+    """Long-time equilibrium oracles (ref: equilibrium.py:24-55) on a few inputs."""
+    from scorepic.equilibrium import vml_equilibrium, vpl_equilibrium
+
+    out = {}
+    cases = [(12.3, [0.1, -0.02], 1.0, 4 * math.pi), (7.5, [0.0, 0.0, 0.3], 1.0, 2 * math.pi),
+             (0.9, [0.01, 0.02, 0.0], 0.5, 5.0)]
+    for k, (E0, P0, rho, vol) in enumerate(cases):
+        eq = vpl_equilibrium(E0, np.array(P0), rho, vol)
+        out[f"vpl_in_{k}"] = np.array([E0, rho, vol])
+        out[f"vpl_P_{k}"] = np.array(P0)
+        out[f"vpl_T_{k}"] = np.array(eq.T_inf)
+        out[f"vpl_u_{k}"] = eq.u_inf
+    for k, (E0, B, vol) in enumerate([(3.0, [0.0, 0.0, 0.2], 2 * math.pi),
+                                      (1.5, [0.1, 0.0, 0.05], 5.0)]):
+        eq = vml_equilibrium(E0, np.array(B), 1.0, vol)
+        out[f"vml_in_{k}"] = np.array([E0, vol])
+        out[f"vml_B_{k}"] = np.array(B)
+        out[f"vml_T_{k}"] = np.array(eq.T_inf)
+    save("equilibrium.npz", **out)
+
+
 if __name__ == "__main__":
     gen_binning()
     gen_collision()
@@ -378,3 +400,4 @@ if __name__ == "__main__":
     gen_run()
     gen_faults()
     gen_score_test()
+    gen_equilibrium()

@@ -212,3 +212,17 @@ def test_score_test_fixture_matches_oracle_blob(golden):
     w = np.full(n, L / n)
     assert rel(O.blob_score(x, v, w, eta, M), s) <= 1e-11
     assert rel(O.collision_force(x, v, w, s, eta, M, -3.0), U) <= 1e-11
+
+
+def test_equilibrium_oracles_match_reference(golden):
+    """The long-time equilibrium oracles the acceptance tests use (ref: equilibrium.py:24-55)."""
+    g = golden("equilibrium.npz")
+    for k in range(3):
+        E0, rho, vol = g[f"vpl_in_{k}"]
+        T, u = O.vpl_equilibrium(E0, g[f"vpl_P_{k}"], rho, vol)
+        assert T == pytest.approx(float(g[f"vpl_T_{k}"]), rel=1e-14)
+        np.testing.assert_allclose(u, g[f"vpl_u_{k}"], rtol=1e-14)
+    for k in range(2):
+        E0, vol = g[f"vml_in_{k}"]
+        T, _ = O.vml_equilibrium(E0, g[f"vml_B_{k}"], 1.0, vol)
+        assert T == pytest.approx(float(g[f"vml_T_{k}"]), rel=1e-14)
