@@ -9,8 +9,9 @@ K = 10 exact-divergence ISM steps per time step with BASELINE's score MLP
 "(x, v) -> 2x128 SiLU -> R^3" (tcgen05 hidden GEMMs), Adam lr 1e-3 (AdamW, wd = 0).
 A step is one full Algorithm-1 step (push, bin, deposit + field, K ISM steps, score, Landau
 collision + push, diagnostics) over the synthetic ensemble (seeded sampler, random-init net).
-The same line carries config 3 (Weibel, full Maxwell VML, n = 2^22) as `config3_vml` and
-config 4 with the reference's own softsign network as `reference_net_variant`.
+The same line carries config 3 (Weibel, full Maxwell VML, n = 2^22) as `config3_vml`, config 4
+with the blob estimator (h = 0.025) as `config4_blob` and config 4 with the reference's own
+softsign network as `reference_net_variant`.
 
   value  = particle-steps/s, device-timed with CUDA events per step (L2 flushed between
            timed steps by a 256 MiB write outside the timed windows), max over ranks.
@@ -850,38 +851,40 @@ def main():
                "flags_checked_every_step": True}
         sim.check()
     elif not args.no_e2e:
-        # decomposed engine: each rank's particles through DistSimulation.step_host (pinned
-        # host buffers sized with headroom for migration), max over ranks
-        try:
-            dv = sim.dv
-            cap = int(1.5 * sim.n) + 1024
-            xh = torch.empty(cap, dtype=torch.float32).pin_memory()
-            vh = torch.empty(dv, cap, dtype=torch.float32).pin_memory()
-            dh = torch.empty(sim.diag.shape[1], dtype=torch.float64).pin_memory()
-            n0 = sim.n
-            xh[:n0].copy_(sim.buf.x[:n0])
-            vh[:, :n0].copy_(sim.buf.vp[:, :n0])
-            torch.cuda.synchronize()
-            sim.step_host(2, xh, vh, dh)  # warm
-            torch.cuda.synchronize()
-            dist.barrier()
-            counts = []
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(args.steps):
-                counts.append(sim.step_host(2, xh, vh, dh))
-            e1.record()
-            e1.synchronize()
-            te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
-            allreduce_max(dist, te, share_gpu)
-            nb = int(statistics.mean(counts)) * 4 * (1 + dv)
-            e2e = {"value": n * args.steps / (float(te[0]) * 1e-3),
-                   "unit": "particle-steps/s", "h2d_bytes_per_step": nb,
-                   "d2h_bytes_per_step": nb + dh.numel() * 8,
-                   "note": "per rank: its own particles in and out every step (rank 0's bytes)"}
-            sim.check()
-        except Exception as exc:  # noqa: BLE001
-            e2e = {"error": str(exc)}
+        # decomposed engine: each rank's particles through DistSimulation.step_host. The pinned
+        # host buffers are sized from the all-reduced largest rank count plus the most a rank
+        # can receive over the timed steps (two boundary messages per step), capped at the
+        # whole job — so no rank can fail inside the collective loop on capacity; any other
+        # error propagates (torchrun then stops every rank) instead of desynchronising them.
+        dv = sim.dv
+        nmax = torch.tensor([float(sim.n)], dtype=torch.float64, device=device)
+        allreduce_max(dist, nmax, share_gpu)
+        cap = int(min(n, int(nmax[0]) + (args.steps + 2) * 2 * (sim.mcap + 1))) + 64
+        xh = torch.empty(cap, dtype=torch.float32).pin_memory()
+        vh = torch.empty(dv, cap, dtype=torch.float32).pin_memory()
+        dh = torch.empty(sim.diag.shape[1], dtype=torch.float64).pin_memory()
+        n0 = sim.n
+        xh[:n0].copy_(sim.buf.x[:n0])
+        vh[:, :n0].copy_(sim.buf.vp[:, :n0])
+        torch.cuda.synchronize()
+        sim.step_host(2, xh, vh, dh)  # warm
+        torch.cuda.synchronize()
+        dist.barrier()
+        counts = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            counts.append(sim.step_host(2, xh, vh, dh))
+        e1.record()
+        e1.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        allreduce_max(dist, te, share_gpu)
+        nb = int(statistics.mean(counts)) * 4 * (1 + dv)
+        e2e = {"value": n * args.steps / (float(te[0]) * 1e-3),
+               "unit": "particle-steps/s", "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb + dh.numel() * 8,
+               "note": "per rank: its own particles in and out every step (rank 0's bytes)"}
+        sim.check()
 
     flop_launch = pair_flops(live, n)
     achieved = flop_launch / (coll_avg_ms * 1e-3) / 1e12
@@ -951,6 +954,13 @@ def main():
             out["config3_vml"]["config"] = bench_config(WORKLOADS["c3"], 1)
         except Exception as exc:  # noqa: BLE001
             out["config3_vml"] = {"error": str(exc)}
+    if world == 1 and args.workload == "c4":
+        # BASELINE config 4 is to be run "with both the SBTM and the blob estimator"
+        try:
+            out["config4_blob"] = variant_line(torch, device, WORKLOADS["c4blob"], args.seed)
+            out["config4_blob"]["config"] = bench_config(WORKLOADS["c4blob"], 1)
+        except Exception as exc:  # noqa: BLE001
+            out["config4_blob"] = {"error": str(exc)}
     if world == 1 and args.workload + "ss" in WORKLOADS:
         # the same config with the reference's own softsign network (like-for-like with the
         # reference arm, which has no SiLU network)
