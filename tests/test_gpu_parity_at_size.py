@@ -252,3 +252,72 @@ def test_config0_100_steps_traces_match_oracle(lib):
     assert ee <= 1e-3 and el <= 1e-3, (ee, el)
     assert pt <= 1e-4 and pyz <= 1e-6, (pt, pyz)
     assert hd <= 5e-2, hd
+
+
+def test_config3_weibel_200_steps_traces_match_oracle(lib):
+    """BASELINE config 3's physics (Weibel, full Maxwell VML: anisotropic Maxwellian
+    T = (0.01, 0.04, 0.04), seeded B_z noise 1e-4, M = 256, L = 2 pi / 1.25, nu = 0.01,
+    dt = 0.02) at n = 2^16 with the reference's softsign net (H = 128, K = 10 exact ISM
+    steps), 200 steps (t = 4, the linear growth of E_B) on the device engine and in
+    oracle.full_step from the same float32 initial state and network:
+      * energy: |E_tot(t) / E_tot(0) - 1| of the device run within 1e-6 of the oracle's at
+        every step (the VML scheme's own drift is shared, float32 adds the rest);
+      * E_B trace (the Weibel growth): max_t |E_B - E_B_ref| <= 1e-2 * max_t E_B_ref, and
+        the growth factor E_B(end) / E_B(0) within 5% of the oracle's;
+      * momentum: P_z (no force in this 1D3V geometry) constant to 1e-6 of sum w|v|.
+    Measured values are printed (DESIGN.md section 5 records them)."""
+    import bench
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.run import initial_fields
+    from paper_2603_25832_b200.score import MlpScoreNet, SbtmEstimator
+    from paper_2603_25832_b200.state import ParticleEnsemble
+
+    steps, K = 200, 10
+    wl = dict(bench.WORKLOADS["c3ss"], n=1 << 16)
+    cfg = bench.make_config(wl, 0)
+    rng = np.random.default_rng(0)
+    x, v, w, b3 = bench.sample_workload(wl, cfg, rng)
+    x, v = f32(x), f32(v)
+    n, M, L, dt, nu = wl["n"], wl["M"], wl["L"], wl["dt"], wl["nu"]
+    grid = Grid(M, L / M)
+    p = ParticleEnsemble.from_arrays(x, v, w)
+    w64 = p.w.double().cpu().numpy()
+    from paper_2603_25832_b200.pic import deposit
+
+    rho, J = deposit(p, grid)
+    f = initial_fields(cfg, grid, rho, J)
+    f.B3.copy_(torch.as_tensor(b3, dtype=torch.float64))
+    B3_0 = f.B3.cpu().numpy().copy()
+    net = MlpScoreNet.init_glorot(3, 128, rng)
+    onet = O.Net(*[a.cpu().numpy().astype(np.float64).copy() for a in net.params()])
+    est = SbtmEstimator(net, L, K, rng, lr=1e-3, weight_decay=0.0, divergence="exact")
+    sim = Simulation(p, f, grid, dt=dt, nu=nu, mode="VML", gamma=-3.0, estimator=est,
+                     max_rows=steps + 1)
+    for k in range(1, steps + 1):
+        sim.step(k)
+    sim.check()
+    got = sim.records(range(1, steps + 1), range(1, steps + 1), [dt * k for k in range(1, steps + 1)])
+
+    st = dict(x=x.copy(), v=v.copy(), w=w64, E1=np.zeros(M), E2=np.zeros(M), B3=B3_0.copy())
+    d0 = O.diagnostics(v, w64, np.zeros(M), np.zeros(M), B3_0, grid.eta)
+    opt = O.AdamW(lr=1e-3, weight_decay=0.0)
+    ref = [O.full_step(st, eta=grid.eta, M=M, dt=dt, nu=nu, mode="VML", gamma=-3.0, net=onet,
+                       opt=opt, K=K, divergence="exact") for _ in range(steps)]
+    E0 = d0["E_total"]
+    drift_g = np.array([r.E_total / E0 - 1.0 for r in got])
+    drift_r = np.array([r["E_total"] / E0 - 1.0 for r in ref])
+    EB_g, EB_r = np.array([r.E_B for r in got]), np.array([r["E_B"] for r in ref])
+    P_g = np.array([r.P for r in got])
+    pscale = float(np.sum(w64 * np.linalg.norm(v, axis=1)))
+    P0 = w64 @ v
+    eb = float(np.max(np.abs(EB_g - EB_r)) / np.max(EB_r))
+    growth_g, growth_r = EB_g[-1] / d0["E_B"], EB_r[-1] / d0["E_B"]
+    pz = float(np.max(np.abs(P_g[:, 2] - P0[2])) / pscale)
+    print(f"config3 (n = 2^16) 200 VML steps: max drift device {np.max(np.abs(drift_g)):.3e}, "
+          f"oracle {np.max(np.abs(drift_r)):.3e}, max |diff| {np.max(np.abs(drift_g - drift_r)):.3e}; "
+          f"E_B trace {eb:.3e}, growth {growth_g:.3f} vs {growth_r:.3f}; P_z drift {pz:.3e}")
+    assert np.max(np.abs(drift_g - drift_r)) <= 1e-6
+    assert eb <= 1e-2
+    assert abs(growth_g / growth_r - 1.0) <= 0.05
+    assert pz <= 1e-6
