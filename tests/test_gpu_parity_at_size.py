@@ -146,12 +146,13 @@ def _silu_oracle_chunked(params, x, v, w, L, chunk=1 << 17):
     return loss, grad
 
 
-@pytest.mark.parametrize("tag", ["c2", "c3"])
+@pytest.mark.parametrize("tag", ["c2", "c3", "c4"])
 def test_silu_ism_at_bench_size(lib, tag):
     """The SiLU ISM kernel at the bench's own sizes (config 2: n = 2^20 two-stream; config 3:
-    n = 2^22 Weibel velocities): one persistent CTA per SM accumulates ~150 (2^20) to ~600
-    (2^22) 48-particle chunks in float32 TMEM before its float64 partial row; loss and every
-    gradient tensor against the float64 oracle."""
+    n = 2^22 Weibel velocities; config 4, the headline: n = 2^24): one persistent CTA per SM
+    accumulates ~150 (2^20) to ~2400 (2^24) 48-particle chunks (float32 TMEM accumulators
+    flushed to a float32 buffer every 64 chunks) before its float64 partial row; loss and
+    every gradient tensor against the float64 oracle."""
     from oracle import silu_oracle as so
     from paper_2603_25832_b200.silu_net import SiluScoreNet, silu_ism_loss_and_grad
 
