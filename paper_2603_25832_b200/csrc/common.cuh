@@ -79,8 +79,13 @@ __device__ __forceinline__ CellKey cell_key(float xf, double eta, int M, int S) 
   double q = (double)xf / eta;
   double fl = floor(q);
   long long idx = (long long)fl;
-  long long r = idx % (long long)M;
-  if (r < 0) r += M;
+  // positions lie in [0, L): idx in [0, M] almost always; the 64-bit modulo (a software
+  // division) only for the rest. Same result as the floor-mod either way.
+  long long r = idx;
+  if (idx < 0 || idx >= (long long)M) {
+    r = idx % (long long)M;
+    if (r < 0) r += M;
+  }
   CellKey k;
   k.cell = (int)r;  // already <= M-1; the reference's min(., M-1) is a no-op after mod
   k.wrapped = idx >= M;
