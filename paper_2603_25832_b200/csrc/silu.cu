@@ -1042,6 +1042,8 @@ static int silu_reduce(int64_t n, void* scratch, cudaStream_t st) {
 extern "C" int spic_silu_forward(const float* params32, int32_t H, const float* xv,
                                  const float* sw, int64_t n, float x_scale, float* sw_out,
                                  void* stream) {
+  if (n < 0) return SPIC_ERR_ARG;
+  if (n == 0) return SPIC_OK;  // empty ensemble: nothing to score
   if (!sw_out || !xv) return SPIC_ERR_ARG;
   SiluInputs in{(const float4*)xv, (const float4*)sw, nullptr, nullptr, 0, nullptr, nullptr, 0,
                 nullptr, 0.f};

@@ -1065,3 +1065,27 @@ def test_engine_step_with_nvtx_ranges(spic, monkeypatch):
         sim.check()
         outs.append((p.v.cpu().numpy().copy(), sim.diag[1].cpu().numpy().copy()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_empty_ensemble_operators(spic):
+    """n = 0 through every operator of the path: empty outputs, zero grid moments, no error
+    (the reference's numpy forms return empty arrays / zero sums for an empty ensemble)."""
+    from paper_2603_25832_b200.collision import build_cell_index, collision_force
+    from paper_2603_25832_b200.pic import Grid, advance_positions, deposit, interpolate_fields
+    from paper_2603_25832_b200.score import MlpScoreNet, blob_score, mlp_forward
+    from paper_2603_25832_b200.silu_net import SiluScoreNet, silu_forward
+    from paper_2603_25832_b200.state import FieldState
+
+    g = Grid(8, 0.5)
+    p = ens(np.zeros(0), np.zeros((0, 3)), np.zeros(0))
+    ci = build_cell_index(p, g)
+    assert np.array_equal(ci.cell_start.cpu().numpy(), np.zeros(9, dtype=np.int32))
+    assert tuple(collision_force(p, np.zeros((0, 3)), ci, g, -3.0).shape) == (0, 3)
+    rho, J = deposit(p, g)
+    assert np.all(rho.cpu().numpy() == 0.0) and np.all(J.cpu().numpy() == 0.0)
+    assert tuple(blob_score(p, ci, g).shape) == (0, 3)
+    assert tuple(mlp_forward(MlpScoreNet(3, 8), np.zeros(0), np.zeros((0, 3))).shape) == (0, 3)
+    assert tuple(silu_forward(SiluScoreNet(), np.zeros(0), np.zeros((0, 3)), 4.0).shape) == (0, 3)
+    Ep, Bp = interpolate_fields(p, FieldState.zeros(8, 3), g)
+    assert Ep.shape[0] == 0 and Bp.shape[0] == 0
+    advance_positions(p, 0.1, 4.0)
