@@ -433,6 +433,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           }
           S.u[buf][pl] = u;
         }
+        if (tid == 0 && c + gridDim.x < nchunks) {  // next chunk's records into L2 (see ISM)
+          const int64_t p0n = (c + gridDim.x) * kCP;
+          const int64_t cntn = n - p0n < (int64_t)kCP ? n - p0n : (int64_t)kCP;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xv + p0n),
+                       "r"((uint32_t)(sizeof(float4) * (size_t)cntn))
+                       : "memory");
+        }
         wg_sync(wg);
 #pragma unroll
         for (int i = 0; i < kPPT; ++i) {
@@ -524,6 +531,20 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       S.u[ub][pl] = u;
       S.w[pl] = wt;
       if (MODE == 2) tgt[pl] = t;
+    }
+    if (xv && tid == 0) {
+      // the CTA's next chunk of records into L2 (one bulk prefetch per record array, no
+      // registers held): its loads at the top of the next chunk then miss only to L2
+      const int64_t cn = c + gridDim.x;
+      if (cn < nchunks) {
+        const int64_t p0n = cn * kCP;
+        const int64_t cntn = n - p0n < (int64_t)kCP ? n - p0n : (int64_t)kCP;
+        const uint32_t bytes = (uint32_t)(sizeof(float4) * (size_t)cntn);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xv + p0n), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sw + p0n), "r"(bytes)
+                     : "memory");
+      }
     }
     wg_sync(wg);
     SILU_TRACE(1);
