@@ -113,8 +113,11 @@ __global__ void __launch_bounds__(1024) k_sym_tiles(
         int b = 0;  // sub-cell of the tile's last record
         for (int k = 1; k < S; ++k)
           if (ss[k] <= t1 - 1) b = k;
-        const int hs = min(S - 1, b + 1);
-        len2 = sub_start[(size_t)cn * S + hs + 1] - cell_start[cn];
+        // next-cell records at sub-cell offsets > b lie farther than eta from every target of
+        // the tile (x_j - x_i > eta on the binning's own float64 cell coordinates; at a sub-cell
+        // boundary the float64 rounding of x / eta can only misplace a pair whose weight is
+        // ~1e-16 of psi(0)), so the prefix ends with sub-cell b
+        len2 = sub_start[(size_t)cn * S + b + 1] - cell_start[cn];
       } else {
         len2 = cell_start[cn + 1] - cell_start[cn];
       }

@@ -123,8 +123,10 @@ static __device__ Window build_window(const int32_t* __restrict__ cell_start,
       if (ss[k] <= t0) a = k;
       if (ss[k] <= t1 - 1) b = k;
     }
-    ulo = max(0, S + a - S - 1);
-    uhi = min(3 * S - 1, S + b + S + 1);
+    // cell c-1 from sub-cell a, cell c+1 through sub-cell b: beyond them every pair is
+    // farther than eta apart (see k_sym_tiles)
+    ulo = a;
+    uhi = 2 * S + b;
   }
   for (int d = -1; d <= 1; ++d) {
     int u0 = (d + 1) * S, u1 = u0 + S - 1;
