@@ -661,8 +661,8 @@ def allreduce_max(dist, t, host_staged: bool):
 def evaluated_pairs(cell_start, sub_start, M: int, S: int, TI: int = 512) -> float:
     """Unordered pairs the antisymmetric kernel evaluates in one launch ("count
     41 FLOP per evaluated unordered pair"): per target tile [t0, t1) of a cell, its forward
-    window (the rest of the cell, len1, plus the culled prefix of the next cell, len2 — the
-    k_sym_tiles rule, landau_sym.cu) and the tile's own unordered pairs (the diagonal block,
+    window (the rest of the cell, len1, plus the next cell's prefix through the sub-cell of
+    the tile's last record, len2 — the k_sym_tiles rule, landau_sym.cu) and the tile's own unordered pairs (the diagonal block,
     counted once although the kernel evaluates it one-sided in both orders). Host numpy on
     the cell / sub-cell starts; M >= 3."""
     cs = np.asarray(cell_start, dtype=np.int64)
@@ -677,8 +677,7 @@ def evaluated_pairs(cell_start, sub_start, M: int, S: int, TI: int = 512) -> flo
             if ss is not None:
                 sub = ss[c * S:(c + 1) * S]
                 b = int(np.searchsorted(sub, t1 - 1, side="right")) - 1
-                hs = min(S - 1, b + 1)
-                len2 = int(ss[cn * S + hs + 1] - cs[cn])
+                len2 = int(ss[cn * S + b + 1] - cs[cn])
             else:
                 len2 = int(cs[cn + 1] - cs[cn])
             total += tl * ((e - t1) + len2) + tl * (tl - 1) / 2.0
