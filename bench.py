@@ -662,9 +662,9 @@ def evaluated_pairs(cell_start, sub_start, M: int, S: int, TI: int = 512) -> flo
     """Unordered pairs the antisymmetric kernel evaluates in one launch ("count
     41 FLOP per evaluated unordered pair"): per target tile [t0, t1) of a cell, its forward
     window (the rest of the cell, len1, plus the next cell's prefix through the sub-cell of
-    the tile's last record, len2 — the k_sym_tiles rule, landau_sym.cu) and the tile's own unordered pairs (the diagonal block,
-    counted once although the kernel evaluates it one-sided in both orders). Host numpy on
-    the cell / sub-cell starts; M >= 3."""
+    the tile's last record, len2 — the k_sym_tiles rule, landau_sym.cu) and the tile's own
+    unordered pairs (the diagonal block, counted once although the kernel evaluates it
+    one-sided in both orders). Host numpy on the cell / sub-cell starts; M >= 3."""
     cs = np.asarray(cell_start, dtype=np.int64)
     ss = np.asarray(sub_start, dtype=np.int64) if S > 1 else None
     total = 0.0
