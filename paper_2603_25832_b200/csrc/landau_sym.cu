@@ -11,8 +11,8 @@
 // A target tile [t0, t1) of cell c owns the pairs it forms with its FORWARD window:
 //   seg0 = [t0, t1)            the diagonal block, evaluated one-sided (both orders),
 //   seg1 = [t1, ce)            the rest of cell c (every pair in a cell is within eta),
-//   seg2 = prefix of cell c+1  up to the sub-cell after the tile's last one (periodic shift
-//                              +L for c = M-1).
+//   seg2 = prefix of cell c+1  through the sub-cell of the tile's last record (periodic
+//                              shift +L for c = M-1); later sub-cells are beyond eta.
 // Every unordered pair of the 3-cell stencil is thus evaluated exactly once: pairs inside a
 // cell by the tile of the earlier record, pairs across the c|c+1 border by the tile in c.
 //
