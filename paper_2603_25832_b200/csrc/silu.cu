@@ -19,6 +19,7 @@
 
 #include "adamw.cuh"
 #include "common.cuh"
+#include "f32x2.cuh"
 #include "pairs.cuh"
 #include "umma.cuh"
 
@@ -102,7 +103,40 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p;
 }
 
-__device__ __forceinline__ float sigmoid(float a) { return fast_rcp(1.f + __expf(-a)); }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// logistic sigmoid: rcp.approx(1 + 2^(-a log2 e)) (MUFU.EX2 + MUFU.RCP)
+__device__ __forceinline__ float sigmoid(float a) {
+  return fast_rcp(1.f + ex2_approx(a * -1.4426950408889634f));
+}
+// the same for two values packed in f32x2 (FMUL2 / FADD2 around the per-lane MUFUs)
+__device__ __forceinline__ f2 sigmoid2(f2 a) {
+  float t0, t1;
+  un2(mul2(a, mk2(-1.4426950408889634f, -1.4426950408889634f)), t0, t1);
+  float s0, s1;
+  un2(add2(mk2(ex2_approx(t0), ex2_approx(t1)), mk2(1.f, 1.f)), s0, s1);
+  return mk2(fast_rcp(s0), fast_rcp(s1));
+}
+
+// The chunk's records sit in S.u in particle pairs, so the packed (f32x2) phases read two
+// particles' components as aligned register pairs: for particles 2j, 2j+1
+//   u[2j] = (x_a, x_b, v0_a, v0_b),  u[2j + 1] = (v1_a, v1_b, v2_a, v2_b).
+__device__ __forceinline__ void put_u(float4* ub, int p, float4 u) {
+  float* f = reinterpret_cast<float*>(ub + (p & ~1));
+  const int s = p & 1;
+  f[s] = u.x;
+  f[2 + s] = u.y;
+  f[4 + s] = u.z;
+  f[6 + s] = u.w;
+}
+__device__ __forceinline__ float4 get_u(const float4* ub, int p) {
+  const float* f = reinterpret_cast<const float*>(ub + (p & ~1));
+  const int s = p & 1;
+  return make_float4(f[s], f[2 + s], f[4 + s], f[6 + s]);
+}
 
 // lane l ends with the warp-wide sum of v[l] (31 shuffles for 32 values)
 __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
@@ -307,27 +341,42 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 #ifdef SPIC_SILU_NO_F3  // timing diagnostic only (wrong gradients): G1 without concurrent F3
     return;
 #endif
-    float aw1[4] = {0.f, 0.f, 0.f, 0.f}, ab1 = 0.f;
     float vd[16], vf[16];
     umma::tmem_ld12(tl + cD2 + p0, vd);
     if (DIV) umma::tmem_ld12(tl + cD2 + kCP + p0, vf);
+    const f2 one2 = mk2(1.f, 1.f);
+    f2 aw[4] = {mk2(0.f, 0.f), mk2(0.f, 0.f), mk2(0.f, 0.f), mk2(0.f, 0.f)}, ab = mk2(0.f, 0.f);
 #pragma unroll
-    for (int pp = 0; pp < kPPT; ++pp) {
-      const float4 u = S.u[ub][p0 + pp];
-      const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
-      const float sg = sigmoid(a);
-      const float d1 = sg * fmaf(a, 1.f - sg, 1.f);
-      float da1 = d1 * vd[pp];
-      if (DIV) da1 = fmaf(sg * (1.f - sg) * fmaf(a, 1.f - 2.f * sg, 2.f), vf[pp], da1);
-      ab1 += da1;
-      aw1[0] = fmaf(da1, u.x, aw1[0]);
-      aw1[1] = fmaf(da1, u.y, aw1[1]);
-      aw1[2] = fmaf(da1, u.z, aw1[2]);
-      aw1[3] = fmaf(da1, u.w, aw1[3]);
+    for (int pp = 0; pp < kPPT; pp += 2) {  // two particles per f32x2 lane pair
+      const float4 A = S.u[ub][p0 + pp], B = S.u[ub][p0 + pp + 1];
+      const f2 ux = mk2(A.x, A.y), uy = mk2(A.z, A.w), uz = mk2(B.x, B.y), uw = mk2(B.z, B.w);
+      const f2 a = fma2(mk2(w1[3], w1[3]), uw,
+                        fma2(mk2(w1[2], w1[2]), uz,
+                             fma2(mk2(w1[1], w1[1]), uy, fma2(mk2(w1[0], w1[0]), ux, mk2(bb1, bb1)))));
+      const f2 sg = sigmoid2(a);
+      const f2 omg = sub2(one2, sg);
+      const f2 d1 = mul2(sg, fma2(a, omg, one2));
+      f2 da1 = mul2(d1, mk2(vd[pp], vd[pp + 1]));
+      if (DIV)
+        da1 = fma2(mul2(mul2(sg, omg), fma2(a, fma2(mk2(-2.f, -2.f), sg, one2), mk2(2.f, 2.f))),
+                   mk2(vf[pp], vf[pp + 1]), da1);
+      ab = add2(ab, da1);
+      aw[0] = fma2(da1, ux, aw[0]);
+      aw[1] = fma2(da1, uy, aw[1]);
+      aw[2] = fma2(da1, uz, aw[2]);
+      aw[3] = fma2(da1, uw, aw[3]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) gw1[i] += aw1[i];
-    gb1 += ab1;
+    for (int i = 0; i < 4; ++i) {
+      float lo, hi;
+      un2(aw[i], lo, hi);
+      gw1[i] += lo + hi;
+    }
+    {
+      float lo, hi;
+      un2(ab, lo, hi);
+      gb1 += lo + hi;
+    }
   };
 
   // this thread's 32-column slice of D3 / D4 (row h, columns 32 wg ..) in the CTA's buffer
@@ -431,7 +480,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
             const float x = A.x < 0.f ? A.x + L : A.x;  // % M quirk records carry x - L
             u = make_float4(x * x_scale, A.y, A.z, A.w);
           }
-          S.u[buf][pl] = u;
+          put_u(S.u[buf], pl, u);
         }
         if (tid == 0 && c + gridDim.x < nchunks) {  // next chunk's records into L2 (see ISM)
           const int64_t p0n = (c + gridDim.x) * kCP;
@@ -443,7 +492,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         wg_sync(wg);
 #pragma unroll
         for (int i = 0; i < kPPT; ++i) {
-          const float4 u = S.u[buf][p0 + i];
+          const float4 u = get_u(S.u[buf], p0 + i);
           const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
           st_split(rb[i & 7] + (buf ? xdelta : 0u) + i * 128, a * sigmoid(a));
         }
@@ -528,7 +577,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           if (MODE == 2) t = make_float4(in.Z[r], in.Z[in.ldz + r], in.Z[2 * in.ldz + r], 0.f);
         }
       }
-      S.u[ub][pl] = u;
+      put_u(S.u[ub], pl, u);
       S.w[pl] = wt;
       if (MODE == 2) tgt[pl] = t;
     }
@@ -552,13 +601,17 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     // F1: layer 1 -> X rows p (h1) and 32 + p (d1 = silu'(a1)), column h
     if (MODE == 1) {
       float f1h[kPPT], f1d[kPPT];
+      const f2 one2 = mk2(1.f, 1.f);
 #pragma unroll
-      for (int i = 0; i < kPPT; ++i) {
-        const float4 u = S.u[ub][p0 + i];
-        const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
-        const float sg = sigmoid(a);
-        f1h[i] = a * sg;
-        f1d[i] = sg * fmaf(a, 1.f - sg, 1.f);
+      for (int i = 0; i < kPPT; i += 2) {  // two particles per f32x2 lane pair
+        const float4 A = S.u[ub][p0 + i], B = S.u[ub][p0 + i + 1];
+        const f2 a = fma2(mk2(w1[3], w1[3]), mk2(B.z, B.w),
+                          fma2(mk2(w1[2], w1[2]), mk2(B.x, B.y),
+                               fma2(mk2(w1[1], w1[1]), mk2(A.z, A.w),
+                                    fma2(mk2(w1[0], w1[0]), mk2(A.x, A.y), mk2(bb1, bb1)))));
+        const f2 sg = sigmoid2(a);
+        un2(mul2(a, sg), f1h[i], f1h[i + 1]);
+        un2(mul2(sg, fma2(a, sub2(one2, sg), one2)), f1d[i], f1d[i + 1]);
       }
       wait_g3();
 #pragma unroll
@@ -569,7 +622,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     } else {
 #pragma unroll
       for (int i = 0; i < kPPT; ++i) {
-        const float4 u = S.u[ub][p0 + i];
+        const float4 u = get_u(S.u[ub], p0 + i);
         const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
         const float sg = sigmoid(a);
         st_split(rb[i & 7] + i * 128, a * sg);
