@@ -138,35 +138,49 @@ __device__ __forceinline__ float4 get_u(const float4* ub, int p) {
   return make_float4(f[s], f[2 + s], f[4 + s], f[6 + s]);
 }
 
-// lane l ends with the warp-wide sum of v[l] (31 shuffles for 32 values)
-__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
+// one butterfly level over v[0 .. 2w): lanes with bit w set keep the upper half, the others
+// the lower, and add the partner's other half (adds paired into FADD2 for w >= 2)
+template <int W, int N>
+__device__ __forceinline__ void butterfly(float (&v)[N], int lane) {
+  const bool up = (lane & W) != 0;
+  if constexpr (W == 1) {
+    const float send = up ? v[0] : v[1];
+    const float keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  } else {
 #pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const bool up = (lane & w) != 0;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = up ? v[i] : v[i + w];
-      const float keep = up ? v[i + w] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    for (int i = 0; i < W; i += 2) {
+      const float s0 = up ? v[i] : v[i + W], s1 = up ? v[i + 1] : v[i + 1 + W];
+      const float k0 = up ? v[i + W] : v[i], k1 = up ? v[i + 1 + W] : v[i + 1];
+      const float r0 = __shfl_xor_sync(0xffffffffu, s0, W);
+      const float r1 = __shfl_xor_sync(0xffffffffu, s1, W);
+      un2(add2(mk2(k0, k1), mk2(r0, r1)), v[i], v[i + 1]);
     }
   }
+}
+
+// lane l ends with the warp-wide sum of v[l] (31 shuffles for 32 values)
+__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
+  butterfly<16>(v, lane);
+  butterfly<8>(v, lane);
+  butterfly<4>(v, lane);
+  butterfly<2>(v, lane);
+  butterfly<1>(v, lane);
   return v[0];
 }
 
 // lanes l and l ^ 16 end with the warp-wide sum of v[l & 15] (31 shuffles for 16 values)
 __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
-#pragma unroll
-  for (int w = 8; w >= 1; w >>= 1) {
-    const bool up = (lane & w) != 0;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = up ? v[i] : v[i + w];
-      const float keep = up ? v[i + w] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
-    }
+  for (int i = 0; i < 16; i += 2) {
+    const float r0 = __shfl_xor_sync(0xffffffffu, v[i], 16);
+    const float r1 = __shfl_xor_sync(0xffffffffu, v[i + 1], 16);
+    un2(add2(mk2(v[i], v[i + 1]), mk2(r0, r1)), v[i], v[i + 1]);
   }
+  butterfly<8>(v, lane);
+  butterfly<4>(v, lane);
+  butterfly<2>(v, lane);
+  butterfly<1>(v, lane);
   return v[0];
 }
 
@@ -654,16 +668,23 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       umma::tmem_ld12(tl + cD1 + p0, va);
       if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
       float v32[32], v16[16];
+      const f2 one2 = mk2(1.f, 1.f);
 #pragma unroll
-      for (int pp = 0; pp < kPPT; ++pp) {
-        const float a2 = va[pp] + bb2;
-        const float sg = sigmoid(a2);
-        const float h2 = a2 * sg;
-        float* dst = pp < 8 ? &v32[4 * pp] : &v16[4 * (pp - 8)];
-        dst[0] = w3[0] * h2;
-        dst[1] = w3[1] * h2;
-        dst[2] = w3[2] * h2;
-        dst[3] = DIV ? sg * fmaf(a2, 1.f - sg, 1.f) * ve[pp] : 0.f;
+      for (int pp = 0; pp < kPPT; pp += 2) {  // two particles per f32x2 lane pair
+        const f2 a2 = add2(mk2(va[pp], va[pp + 1]), mk2(bb2, bb2));
+        const f2 sg = sigmoid2(a2);
+        const f2 h2 = mul2(a2, sg);
+        float* d0 = pp < 8 ? &v32[4 * pp] : &v16[4 * (pp - 8)];
+        float* d1 = d0 + 4;
+        un2(mul2(mk2(w3[0], w3[0]), h2), d0[0], d1[0]);
+        un2(mul2(mk2(w3[1], w3[1]), h2), d0[1], d1[1]);
+        un2(mul2(mk2(w3[2], w3[2]), h2), d0[2], d1[2]);
+        if (DIV) {
+          un2(mul2(mul2(sg, fma2(a2, sub2(one2, sg), one2)), mk2(ve[pp], ve[pp + 1])), d0[3], d1[3]);
+        } else {
+          d0[3] = 0.f;
+          d1[3] = 0.f;
+        }
       }
       const float r32 = transpose_reduce32(v32, lane);
       const float r16 = transpose_reduce16(v16, lane);
@@ -710,33 +731,56 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 
     // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
     {
-      float aw3[3] = {0.f, 0.f, 0.f}, ab2 = 0.f;
+      const f2 z2 = mk2(0.f, 0.f), one2 = mk2(1.f, 1.f);
+      f2 aw3[3] = {z2, z2, z2}, ab2 = z2;
       float va[16], ve[16];
       umma::tmem_ld12(tl + cD1 + p0, va);
       if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
 #pragma unroll
-      for (int pp = 0; pp < kPPT; ++pp) {
-        const float4 G = S.gs[p0 + pp];
-        const float a2 = va[pp] + bb2;
-        const float sg = sigmoid(a2);
-        const float h2 = a2 * sg;
-        const float d2 = sg * fmaf(a2, 1.f - sg, 1.f);
-        const float dh2 = fmaf(w3[2], G.z, fmaf(w3[1], G.y, w3[0] * G.x));
-        float da2 = d2 * dh2;
+      for (int pp = 0; pp < kPPT; pp += 2) {  // two particles per f32x2 lane pair
+        const float4 Ga = S.gs[p0 + pp], Gb = S.gs[p0 + pp + 1];
+        const f2 gx = mk2(Ga.x, Gb.x), gy = mk2(Ga.y, Gb.y), gz = mk2(Ga.z, Gb.z);
+        const f2 a2 = add2(mk2(va[pp], va[pp + 1]), mk2(bb2, bb2));
+        const f2 sg = sigmoid2(a2);
+        const f2 omg = sub2(one2, sg);
+        const f2 h2 = mul2(a2, sg);
+        const f2 d2 = mul2(sg, fma2(a2, omg, one2));
+        const f2 dh2 = fma2(mk2(w3[2], w3[2]), gz,
+                            fma2(mk2(w3[1], w3[1]), gy, mul2(mk2(w3[0], w3[0]), gx)));
+        f2 da2 = mul2(d2, dh2);
+        f2 gwd2 = z2;
         if (DIV) {
-          const float e2 = sg * (1.f - sg) * fmaf(a2, 1.f - 2.f * sg, 2.f);
-          da2 = fmaf(e2, G.w * ve[pp], da2);
+          const f2 gw = mk2(Ga.w, Gb.w);
+          const f2 e2 = mul2(mul2(sg, omg), fma2(a2, fma2(mk2(-2.f, -2.f), sg, one2), mk2(2.f, 2.f)));
+          da2 = fma2(e2, mul2(gw, mk2(ve[pp], ve[pp + 1])), da2);
+          gwd2 = mul2(gw, d2);
         }
-        aw3[0] = fmaf(G.x, h2, aw3[0]);
-        aw3[1] = fmaf(G.y, h2, aw3[1]);
-        aw3[2] = fmaf(G.z, h2, aw3[2]);
-        ab2 += da2;
-        st_split(rb[pp & 7] + kY + pp * 128, da2);
-        if (DIV) st_split(rb[pp & 7] + kY + kDivRows + pp * 128, G.w * d2);
+        aw3[0] = fma2(gx, h2, aw3[0]);
+        aw3[1] = fma2(gy, h2, aw3[1]);
+        aw3[2] = fma2(gz, h2, aw3[2]);
+        ab2 = add2(ab2, da2);
+        float da_a, da_b;
+        un2(da2, da_a, da_b);
+        st_split(rb[pp & 7] + kY + pp * 128, da_a);
+        st_split(rb[(pp + 1) & 7] + kY + (pp + 1) * 128, da_b);
+        if (DIV) {
+          float y_a, y_b;
+          un2(gwd2, y_a, y_b);
+          st_split(rb[pp & 7] + kY + kDivRows + pp * 128, y_a);
+          st_split(rb[(pp + 1) & 7] + kY + kDivRows + (pp + 1) * 128, y_b);
+        }
       }
 #pragma unroll
-      for (int k = 0; k < 3; ++k) gw3[k] += aw3[k];
-      gb2 += ab2;
+      for (int k = 0; k < 3; ++k) {
+        float lo, hi;
+        un2(aw3[k], lo, hi);
+        gw3[k] += lo + hi;
+      }
+      {
+        float lo, hi;
+        un2(ab2, lo, hi);
+        gb2 += lo + hi;
+      }
     }
     fence_proxy_async();
     umma::fence_before();
