@@ -77,7 +77,8 @@ struct SiluShared {
   float4 u[2][kCP];  // chunk records, double-buffered (the layer-1 reverse sweep runs late)
   float w[kCP];
   float4 gs[kCP];              // ISM: (2w s, 2w); MSE: (2w' (s - t), 0)
-  uint64_t bar[3];  // [0] G1 done, [1] G3 done (X, Y free again), [2] G2 done
+  uint64_t bar[4];  // [0] G1 done, [1] G3 done (X, Y free again), [2] G2 done,
+                    // [3] G1's primal half done (ISM: F2a starts on it while B d1 runs)
   uint32_t tmem;
 };
 // W2 and B = W2 (.) C as 128-row operand tiles (hi, lo); X and Y as 96-row tiles (hi, lo):
@@ -308,6 +309,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
     mbar_init(&S.bar[2], 1);
+    mbar_init(&S.bar[3], 1);
     fence_barrier_init();
   }
   fence_proxy_async();
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   // cross-CTA combines are float64
   float gw1[4] = {0, 0, 0, 0}, gb1 = 0, gb2 = 0, gw3[3] = {0, 0, 0};
   float loss = 0, gb3[3] = {0, 0, 0};
-  uint32_t phase = 0, phase2 = 0, phase3 = 0;
+  uint32_t phase = 0, phase2 = 0, phase3 = 0, phase_p = 0;
   bool first = true;
   const int64_t nchunks = (n + kCP - 1) / kCP;
   const int p0 = kPPT * wg;  // this warpgroup's particles inside the chunk (= GEMM columns)
@@ -435,9 +437,11 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(tm + cD1, sW2h, sW2l, sXh, sXl,
                                                                 false);  // W2 h1
         }
-        if (DIV)
+        if (DIV) {
+          umma::commit_elect(&S.bar[3]);  // primal half: F2a's s partials start on it
           umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(
               tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);  // B d1
+        }
         umma::commit_elect(&S.bar[0]);
       }
       __syncwarp();
@@ -656,8 +660,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     }
     if (MODE == 1 && pending) layer1_reverse(ub ^ 1);  // overlaps this chunk's G1
     SILU_TRACE(3);
-    umma::wait_mma(&S.bar[0], phase);
-    phase ^= 1;
+    if (DIV) {  // the primal half of G1 (the div half is awaited inside F2a)
+      umma::wait_mma(&S.bar[3], phase_p);
+      phase_p ^= 1;
+    } else {
+      umma::wait_mma(&S.bar[0], phase);
+      phase ^= 1;
+    }
     umma::fence_after();
     SILU_TRACE(4);
 
@@ -666,7 +675,6 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     {
       float va[16], ve[16];
       umma::tmem_ld12(tl + cD1 + p0, va);
-      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
       float v32[32], v16[16];
       const f2 one2 = mk2(1.f, 1.f);
 #pragma unroll
@@ -679,11 +687,19 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         un2(mul2(mk2(w3[0], w3[0]), h2), d0[0], d1[0]);
         un2(mul2(mk2(w3[1], w3[1]), h2), d0[1], d1[1]);
         un2(mul2(mk2(w3[2], w3[2]), h2), d0[2], d1[2]);
-        if (DIV) {
-          un2(mul2(mul2(sg, fma2(a2, sub2(one2, sg), one2)), mk2(ve[pp], ve[pp + 1])), d0[3], d1[3]);
-        } else {
-          d0[3] = 0.f;
-          d1[3] = 0.f;
+        // d2 = silu'(a2) for now; times e (the div half of G1) below
+        un2(DIV ? mul2(sg, fma2(a2, sub2(one2, sg), one2)) : mk2(0.f, 0.f), d0[3], d1[3]);
+      }
+      if (DIV) {
+        umma::wait_mma(&S.bar[0], phase);
+        phase ^= 1;
+        umma::fence_after();
+        umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
+#pragma unroll
+        for (int pp = 0; pp < kPPT; pp += 2) {
+          float* d0 = pp < 8 ? &v32[4 * pp] : &v16[4 * (pp - 8)];
+          float* d1 = d0 + 4;
+          un2(mul2(mk2(d0[3], d1[3]), mk2(ve[pp], ve[pp + 1])), d0[3], d1[3]);
         }
       }
       const float r32 = transpose_reduce32(v32, lane);
