@@ -447,18 +447,27 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       __syncwarp();
       SILU_TRACE_I(11);
       if (ISM) {
-        handoff_wait(7);  // Y written (F2b of chunk c)
+        const bool acc3 = !fst && (iit % kFlushChunks) != 0;  // fresh after a flush
+        if (DIV) {
+          // The divergence columns of Y (y2 = 2w d2) do not depend on the scores: F2a stores
+          // them as soon as G1's primal half is in, and their halves of G3 and G2 run on the
+          // tensor pipe while the FP32 side does the s / div reductions and F2b.
+          handoff_wait(9);  // Y divergence rows written (F2a of chunk c)
+          umma::fence_after();
+          umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(
+              tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
+              acc3);  // y2 d1^T
+          umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(
+              tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
+          __syncwarp();
+        }
+        handoff_wait(7);  // Y primal rows written (F2b of chunk c)
         umma::fence_after();
         SILU_TRACE_I(12);
         {
           // G3 first: the next chunk's layer-1 sweep waits for it (X, Y reuse)
-          const bool acc3 = !fst && (iit % kFlushChunks) != 0;  // fresh after a flush
           umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(tm + cD3, sYh, sYl, sXh,
                                                                       sXl, acc3);  // da2 h1^T
-          if (DIV)
-            umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(
-                tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
-                acc3);  // y2 d1^T
           umma::commit_elect(&S.bar[1]);
 #ifdef SPIC_SILU_TRACE_G3  // timing diagnostic: stamp G3's completion before issuing G2
           {
@@ -469,9 +478,6 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 #endif
           umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(tm + cD2, sW2h, sW2l, sYh, sYl,
                                                                false);  // W2^T da2
-          if (DIV)
-            umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(
-                tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
           umma::commit_elect(&S.bar[2]);
         }
         __syncwarp();
@@ -689,8 +695,16 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         un2(mul2(mk2(w3[2], w3[2]), h2), d0[2], d1[2]);
         // d2 = silu'(a2) for now; times e (the div half of G1) below
         un2(DIV ? mul2(sg, fma2(a2, sub2(one2, sg), one2)) : mk2(0.f, 0.f), d0[3], d1[3]);
+        if (DIV) {  // Y divergence rows y2 = 2w d2 (no score dependence): G3 / G2 div halves
+          const float wa = S.w[p0 + pp], wb = S.w[p0 + pp + 1];
+          st_split(rb[pp & 7] + kY + kDivRows + pp * 128, (wa + wa) * d0[3]);
+          st_split(rb[(pp + 1) & 7] + kY + kDivRows + (pp + 1) * 128, (wb + wb) * d1[3]);
+        }
       }
       if (DIV) {
+        fence_proxy_async();
+        umma::fence_before();
+        handoff_arrive(9);
         umma::wait_mma(&S.bar[0], phase);
         phase ^= 1;
         umma::fence_after();
@@ -764,12 +778,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         const f2 dh2 = fma2(mk2(w3[2], w3[2]), gz,
                             fma2(mk2(w3[1], w3[1]), gy, mul2(mk2(w3[0], w3[0]), gx)));
         f2 da2 = mul2(d2, dh2);
-        f2 gwd2 = z2;
         if (DIV) {
           const f2 gw = mk2(Ga.w, Gb.w);
           const f2 e2 = mul2(mul2(sg, omg), fma2(a2, fma2(mk2(-2.f, -2.f), sg, one2), mk2(2.f, 2.f)));
           da2 = fma2(e2, mul2(gw, mk2(ve[pp], ve[pp + 1])), da2);
-          gwd2 = mul2(gw, d2);
         }
         aw3[0] = fma2(gx, h2, aw3[0]);
         aw3[1] = fma2(gy, h2, aw3[1]);
@@ -779,12 +791,6 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         un2(da2, da_a, da_b);
         st_split(rb[pp & 7] + kY + pp * 128, da_a);
         st_split(rb[(pp + 1) & 7] + kY + (pp + 1) * 128, da_b);
-        if (DIV) {
-          float y_a, y_b;
-          un2(gwd2, y_a, y_b);
-          st_split(rb[pp & 7] + kY + kDivRows + pp * 128, y_a);
-          st_split(rb[(pp + 1) & 7] + kY + kDivRows + (pp + 1) * 128, y_b);
-        }
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
