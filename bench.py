@@ -805,7 +805,8 @@ def main():
     if not dist_mode and not os.environ.get("SPIC_LANDAU_VARIANT") and sim.grid.M >= 3:
         try:
             evald = evaluated_pairs(sim.ci.cell_start.cpu().numpy(), sim.ci.sub_start.cpu().numpy(),
-                                    sim.grid.M, sim.S)
+                                    sim.grid.M, sim.S,
+                                    TI=int(_lib.query("spic_landau_tile_targets", sim.grid.M)))
         except Exception:  # noqa: BLE001
             evald = None
     t = torch.tensor([total_ms, statistics.mean(coll_ms) if coll_ms else float("nan")],

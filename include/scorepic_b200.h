@@ -83,6 +83,11 @@ int spic_gather_scores(const float* s, int64_t lds, const int32_t* perm, int64_t
 /* ---- Landau collision (replaces _collision_cell collision.py:49-89, collision_force
  *      collision.py:92-110, collision_push collision.py:113-116) --------------------------- */
 size_t spic_landau_scratch_bytes(int64_t n, int32_t M, int32_t dv, int32_t nsplit);
+/* Targets per tile of the antisymmetric pair kernel for an M-cell grid (threads x targets per
+ * thread of the configuration in use). A tile owns the pairs with its forward window, so the
+ * number of pairs one launch evaluates depends on it (bench.py's evaluated-pair count; no
+ * reference counterpart: _collision_cell, collision.py:49-89, loops over whole cells). */
+int spic_landau_tile_targets(int32_t M);
 /* U (sorted order, float[dv][n]) for all targets against their 3-cell stencil.
  * gamma must be -3 (dv=3) or -2 (dv=2) or any value (generic pow path).
  * uniform_w > 0: all weights equal uniform_w (sw.w ignored). nsplit: j-window split

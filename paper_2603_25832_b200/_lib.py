@@ -47,6 +47,7 @@ SIGNATURES = {
                                 _P, _SZ, _P]),
     "spic_gather_scores": (ctypes.c_int, [_P, _I64, _P, _I64, _I32, _P, _P, _P]),
     "spic_landau_scratch_bytes": (_SZ, [_I64, _I32, _I32, _I32]),
+    "spic_landau_tile_targets": (ctypes.c_int, [_I32]),
     "spic_landau_range_scratch_bytes": (_SZ, [_I64, _I32, _I32, _I32, _I32, _I32]),
     "spic_landau": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P, _I32, _I32, _D, _D, _F, _I32, _P,
                                    _P, _SZ, _P]),

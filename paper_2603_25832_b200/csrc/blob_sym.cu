@@ -284,22 +284,38 @@ using namespace spic;
 
 namespace {
 
-constexpr int kBlobSymNT = 128, kBlobSymRP = 2, kBlobSymMinB = 4;
-constexpr int kBlobSymTI = kBlobSymNT * 2 * kBlobSymRP;
+// kernel shape (threads, packed target pairs per thread, resident CTAs per SM), A/B by
+// SPIC_BLOB_SYM_CFG: 0 = 128 x 2 x 4, 1 = 64 x 4 x 6, 2 = 64 x 5 x 5 (see landau_sym.cu)
+struct BlobSymCfg {
+  int nt, rp, minb;
+  int ti() const { return nt * 2 * rp; }
+};
+constexpr BlobSymCfg kBlobSymCfgs[] = {{128, 2, 4}, {64, 4, 6}, {64, 5, 5}};
+// default: 64-thread CTAs as in landau_sym.cu — 10 targets per thread from n = 2^22 (config 4:
+// blob step 493.8 -> 475.3 ms), 8 below (config 2: 16.79 -> 16.48 ms; 10 targets there lose to
+// the wave quantisation of the fewer, larger tiles)
+BlobSymCfg blob_sym_cfg(int M, int64_t n) {
+  if (M <= 2) return kBlobSymCfgs[0];
+  const char* e = getenv("SPIC_BLOB_SYM_CFG");
+  const int def = n >= ((int64_t)1 << 22) ? 2 : 1;
+  const int k = e ? atoi(e) : def;
+  return kBlobSymCfgs[(k >= 0 && k < 3) ? k : def];
+}
 
-constexpr size_t blob_sym_smem_bytes() {
+constexpr size_t blob_sym_smem_bytes(int nt) {
   return 128 + sizeof(float4) * kSymStages * kSymTJ +
-         sizeof(float) * 2 * (kBlobSymNT / 32) * kSymTJ * kBlobNC + sizeof(uint64_t) * kSymStages;
+         sizeof(float) * 2 * (nt / 32) * kSymTJ * kBlobNC + sizeof(uint64_t) * kSymStages;
 }
 
 }  // namespace
 
 int spic_blob_sym_nsplit(int64_t n, int32_t M) {
-  return pair_nsplit_slots(n, M, kBlobSymTI, kBlobSymMinB * kNumSMs);
+  const BlobSymCfg c = blob_sym_cfg(M, n);
+  return pair_nsplit_slots(n, M, c.ti(), c.minb * kNumSMs);
 }
 
 size_t spic_blob_sym_scratch_bytes(int64_t n, int32_t M) {
-  return sym_layout(nullptr, n, M, spic_blob_sym_nsplit(n, M), kBlobSymTI, kBlobNC).bytes + 256;
+  return sym_layout(nullptr, n, M, spic_blob_sym_nsplit(n, M), blob_sym_cfg(M, n).ti(), kBlobNC).bytes + 256;
 }
 
 // dv = 3, uniform weights; h_cell (nullable: fixed h_fixed) already computed
@@ -309,44 +325,50 @@ int spic_blob_sym_run(const float4* xv, float4* sw, const int32_t* perm, int64_t
                       long long* bad_pid, int32_t* flags, void* scratch, size_t scratch_bytes,
                       cudaStream_t st) {
   const int nsplit = spic_blob_sym_nsplit(n, M);
+  const BlobSymCfg cfg = blob_sym_cfg(M, n);
+  const int TI = cfg.ti();
   uintptr_t b = ((uintptr_t)scratch + 255) & ~(uintptr_t)255;
-  SymScratch s = sym_layout((void*)b, n, M, nsplit, kBlobSymTI, kBlobNC);
+  SymScratch s = sym_layout((void*)b, n, M, nsplit, TI, kBlobNC);
   if (s.bytes + (b - (uintptr_t)scratch) > scratch_bytes) return SPIC_ERR_SCRATCH;
   const double L = (double)M * eta;
   const float wie = (float)((double)uniform_w / eta), wie2 = (float)((double)uniform_w / (eta * eta));
   const int32_t* ssp = (S > 1 && M >= 3) ? sub_start : nullptr;
-  k_sym_tiles<<<1, 1024, 0, st>>>(cell_start, ssp, M, S, kBlobSymTI, 0, M, s.cap, s.tile_start,
+  k_sym_tiles<<<1, 1024, 0, st>>>(cell_start, ssp, M, S, TI, 0, M, s.cap, s.tile_start,
                                   s.meta, s.off, s.flag);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
-  const int64_t ntile_grid = n / kBlobSymTI + M + 1;
+  const int64_t ntile_grid = n / TI + M + 1;
   const char* sf = getenv("SPIC_SYM_ORDER");  // "t": tile-fastest grid (A/B)
   const int split_fast = (ntile_grid <= 65535 && !(sf && sf[0] == 't')) ? 1 : 0;
   dim3 grid = split_fast ? dim3((unsigned)nsplit, (unsigned)ntile_grid)
                          : dim3((unsigned)ntile_grid, (unsigned)nsplit);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_blob_sym<kBlobSymNT, kBlobSymRP, kBlobSymMinB, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)blob_sym_smem_bytes());
-    cudaFuncSetAttribute(k_blob_sym<kBlobSymNT, kBlobSymRP, kBlobSymMinB, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)blob_sym_smem_bytes());
-    attr = true;
-  }
-#define SPIC_BLOBSYM(MI_)                                                                        \
-  k_blob_sym<kBlobSymNT, kBlobSymRP, kBlobSymMinB, MI_><<<grid, kBlobSymNT, blob_sym_smem_bytes(), \
-                                                          st>>>(                                 \
-      xv, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag, M, S, (float)L, wie, wie2, h_cell, \
-      h_fixed, nsplit, split_fast, s.Upart, s.Jslot, n)
+#define SPIC_BLOBSYM(NT_, RP_, MB_, MI_)                                                         \
+  do {                                                                                           \
+    static bool attr = false;                                                                    \
+    if (!attr) {                                                                                 \
+      cudaFuncSetAttribute(k_blob_sym<NT_, RP_, MB_, MI_>,                                       \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,                          \
+                           (int)blob_sym_smem_bytes(NT_));                                       \
+      attr = true;                                                                               \
+    }                                                                                            \
+    k_blob_sym<NT_, RP_, MB_, MI_><<<grid, NT_, blob_sym_smem_bytes(NT_), st>>>(                 \
+        xv, cell_start, ssp, s.tile_start, s.meta, s.off, s.flag, M, S, (float)L, wie, wie2,     \
+        h_cell, h_fixed, nsplit, split_fast, s.Upart, s.Jslot, n);                               \
+  } while (0)
   if (M <= 2)
-    SPIC_BLOBSYM(true);
+    SPIC_BLOBSYM(128, 2, 4, true);
+  else if (cfg.nt == 64 && cfg.rp == 4)
+    SPIC_BLOBSYM(64, 4, 6, false);
+  else if (cfg.nt == 64)
+    SPIC_BLOBSYM(64, 5, 5, false);
   else
-    SPIC_BLOBSYM(false);
+    SPIC_BLOBSYM(128, 2, 4, false);
 #undef SPIC_BLOBSYM
   spic::count_launch();
   SPIC_CHECK_LAUNCH();
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
   k_blob_sym_fold<<<blocks, 256, 0, st>>>(s.Upart, nsplit, n, cell_start, s.tile_start, s.meta,
-                                          s.off, s.flag, M, kBlobSymTI, s.Jslot, xv, sw, perm,
+                                          s.off, s.flag, M, TI, s.Jslot, xv, sw, perm,
                                           h_cell, h_fixed, bad_pid, flags);
   spic::count_launch();
   SPIC_CHECK_LAUNCH();

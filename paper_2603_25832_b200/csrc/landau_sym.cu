@@ -421,17 +421,26 @@ struct SymCfg {
 };
 constexpr SymCfg kSymCfgs[] = {{128, 2, 4, 8}, {128, 2, 3, 8}, {128, 3, 3, 8}, {256, 2, 2, 8},
                                {128, 3, 2, 8}, {128, 2, 5, 8}, {128, 2, 4, 4}, {128, 2, 5, 4},
-                               {128, 2, 6, 4}};
+                               {128, 2, 6, 4}, {128, 4, 3, 8}, {64, 4, 6, 8}, {64, 5, 5, 8},
+                               {64, 5, 6, 8}, {64, 6, 5, 8}, {64, 5, 5, 4}, {128, 5, 3, 8}};
+// default: 64 threads x 10 targets (5 packed pairs) per thread. ptxas settles at 168 registers
+// under __launch_bounds__(64, 5), so six CTAs (12 warps) are resident per SM; the j-side
+// reduce-scatter and the even + odd adds are amortised over 10 targets instead of 4, and a
+// two-warp CTA loses less at its per-stage barriers (config 4: 298.3 -> 282.9 ms, config 2:
+// 9.82 -> 9.38 ms; sweep in profiles/r2_pair_kernel_experiments.json)
+constexpr int kSymDefault = 11;
 constexpr int kNumSymCfgs = sizeof(kSymCfgs) / sizeof(kSymCfgs[0]);
 
 SymCfg sym_cfg(int M) {
   if (M <= 2) return kSymCfgs[0];
   const char* e = getenv("SPIC_SYM_CFG");
-  const int k = e ? atoi(e) : 0;
-  return kSymCfgs[(k >= 0 && k < kNumSymCfgs) ? k : 0];
+  const int k = e ? atoi(e) : kSymDefault;
+  return kSymCfgs[(k >= 0 && k < kNumSymCfgs) ? k : kSymDefault];
 }
 
 }  // namespace
+
+extern "C" int spic_landau_tile_targets(int32_t M) { return sym_cfg(M).ti(); }
 
 // nsplit for the symmetric kernel: whole waves of (CTAs per SM) x SMs
 int spic_landau_sym_nsplit(int64_t n, int32_t M, int32_t m_occ) {
@@ -489,6 +498,19 @@ int spic_landau_sym_run(const float* xv, const float* sw, int64_t n, const int32
   const float Lf = (float)L;
   if (M <= 2)
     launch_sym<128, 2, 4, true>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
+#define SPIC_SYM_CASE(NT_, RP_, MB_, G_)                                                        \
+  else if (cfg.nt == NT_ && cfg.rp == RP_ && cfg.minb == MB_ && cfg.g == G_)                    \
+    launch_sym<NT_, RP_, MB_, false, G_>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie,   \
+                                         wie2, nsplit, split_fast, n);
+  SPIC_SYM_CASE(64, 5, 5, 8)
+  SPIC_SYM_CASE(64, 4, 6, 8)
+  SPIC_SYM_CASE(64, 5, 6, 8)
+  SPIC_SYM_CASE(64, 6, 5, 8)
+  SPIC_SYM_CASE(64, 5, 5, 4)
+  SPIC_SYM_CASE(128, 5, 3, 8)
+#undef SPIC_SYM_CASE
+  else if (cfg.rp == 4 && cfg.nt == 128)
+    launch_sym<128, 4, 3, false>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.g == 4 && cfg.minb == 4)
     launch_sym<128, 2, 4, false, 4>(grid, st, xv, sw, cell_start, ssp, s, M, S, Lf, wie, wie2, nsplit, split_fast, n);
   else if (cfg.g == 4 && cfg.minb == 5)
