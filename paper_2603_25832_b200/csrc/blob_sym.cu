@@ -291,15 +291,15 @@ struct BlobSymCfg {
   int ti() const { return nt * 2 * rp; }
 };
 constexpr BlobSymCfg kBlobSymCfgs[] = {{128, 2, 4}, {64, 4, 6}, {64, 5, 5}};
-// default: 64-thread CTAs as in landau_sym.cu — 10 targets per thread from n = 2^22 (config 4:
-// blob step 493.8 -> 475.3 ms), 8 below (config 2: 16.79 -> 16.48 ms; 10 targets there lose to
-// the wave quantisation of the fewer, larger tiles)
-BlobSymCfg blob_sym_cfg(int M, int64_t n) {
+// default: 64-thread CTAs with 8 targets per thread as in landau_sym.cu (config 4: blob step
+// 493.8 -> 480.4 ms, config 2: 16.79 -> 16.48 ms). 10 targets per thread gain another 1% at
+// config 4 (475.3 ms) but lose at config 2 (17.3 ms: wave quantisation of the fewer, larger
+// tiles); the shape does not depend on n, so scratch sized for a capacity fits any smaller run
+BlobSymCfg blob_sym_cfg(int M, int64_t) {
   if (M <= 2) return kBlobSymCfgs[0];
   const char* e = getenv("SPIC_BLOB_SYM_CFG");
-  const int def = n >= ((int64_t)1 << 22) ? 2 : 1;
-  const int k = e ? atoi(e) : def;
-  return kBlobSymCfgs[(k >= 0 && k < 3) ? k : def];
+  const int k = e ? atoi(e) : 1;
+  return kBlobSymCfgs[(k >= 0 && k < 3) ? k : 1];
 }
 
 constexpr size_t blob_sym_smem_bytes(int nt) {
