@@ -81,10 +81,10 @@ struct SiluShared {
                     // [3] G1's primal half done (ISM: F2a starts on it while B d1 runs)
   uint32_t tmem;
 };
-// W2 and B = W2 (.) C as 128-row operand tiles (hi, lo); X and Y as 96-row tiles (hi, lo):
-// rows 0..47 = the chunk's primal columns, rows 48..95 = its divergence columns
-constexpr uint32_t kXHalf = 2 * kCP * 128;        // 96-row tile half (12 KB)
-constexpr uint32_t kXTile = 2 * kXHalf;           // 24 KB
+// W2 and B = W2 (.) C as 128-row SWIZZLE_128B operand tiles (hi, lo); X and Y as activation
+// tiles (hi, lo) of 96 particle columns in the interleaved core-matrix layout (umma.cuh):
+// columns 0..47 = the chunk's primal columns, 48..95 = its divergence columns
+constexpr uint32_t kXTile = 2 * (kCP / 8) * umma::kActGroup;  // 96 particle columns: 24 KB
 // per-warp-quarter partials (s0, s1, s2, div) per particle and the MSE targets live in the Y
 // tile while it is free (after the previous chunk's G2 / G3, before this chunk's F2b)
 constexpr uint32_t kRedBytes = 4 * 4 * kCP * sizeof(float);
@@ -199,21 +199,41 @@ __device__ __forceinline__ void handoff_wait(int id) {
   asm volatile("bar.sync %0, 544;" ::"r"(id) : "memory");
 }
 
-// Split-BF16 store of one value into a 64-row X / Y tile: hi at addr, lo at addr + kXTile.
-// addr = the thread's column base for the row's (r & 7) swizzle phase + r * 128; with the
-// particle loops unrolled the row part is a constant that folds into the STS immediate.
-__device__ __forceinline__ void st_split(uint32_t addr, float x) {
-  asm volatile(
-      "{\n.reg .b16 h16, l16, z16;\n.reg .b32 hf;\n.reg .f32 r;\n"
-      "mov.b16 z16, 0;\n"
-      "cvt.rn.bf16.f32 h16, %1;\n"
-      "mov.b32 hf, {z16, h16};\n"
-      "sub.rn.f32 r, %1, hf;\n"
-      "cvt.rn.bf16.f32 l16, r;\n"
-      "st.shared.b16 [%0], h16;\n"
-      "st.shared.b16 [%0+%2], l16;\n}\n" ::"r"(addr),
-      "f"(x), "n"(kXTile)
-      : "memory");
+// Split-BF16 of two values into packed bf16x2 words (lower half = a, upper half = b): hi and
+// the rounded remainder lo (x ~= hi + lo to ~2^-17 relative).
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+  const float ra = a - __uint_as_float(hi << 16), rb = b - __uint_as_float(hi & 0xffff0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(rb), "f"(ra));
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+// This thread's 12 particles (columns kPPT wg .. kPPT wg + 11 of a 48-column block) of hidden
+// unit h into an activation tile, hi at the given addresses, lo at + kXTile: one 16-byte
+// store for the 8-particle group it covers completely and one 8-byte store for the half
+// group it shares with the neighbouring warpgroup. a8 / a4: the thread's byte addresses of
+// those two (fixed per thread); odd warpgroups hold the half group first.
+__device__ __forceinline__ void store_act12(uint32_t a8, uint32_t a4, bool half_first,
+                                            const float (&v)[kPPT]) {
+  uint32_t hi[6], lo[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) split2(v[2 * j], v[2 * j + 1], hi[j], lo[j]);
+  if (half_first) {
+    sts64(a4, hi[0], hi[1]);
+    sts64(a4 + kXTile, lo[0], lo[1]);
+    sts128(a8, hi[2], hi[3], hi[4], hi[5]);
+    sts128(a8 + kXTile, lo[2], lo[3], lo[4], lo[5]);
+  } else {
+    sts128(a8, hi[0], hi[1], hi[2], hi[3]);
+    sts128(a8 + kXTile, lo[0], lo[1], lo[2], lo[3]);
+    sts64(a4, hi[4], hi[5]);
+    sts64(a4 + kXTile, lo[4], lo[5]);
+  }
 }
 
 // One CTA per SM, four warpgroups. Thread (h, warpgroup g) owns hidden unit h (its TMEM lane)
@@ -268,7 +288,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   uint8_t* Xh = base + 4 * umma::kTileBytes;  // lo at + kXTile, Y hi at + 2 kXTile
   SiluShared& S = *reinterpret_cast<SiluShared*>(base + kSiluTiles);
   constexpr uint32_t kY = 2 * kXTile;
-  constexpr uint32_t kDivRows = kCP * 128;  // byte offset of the divergence rows
+  constexpr uint32_t kDivRows = (kCP / 8) * umma::kActGroup;  // byte offset of the divergence columns
 
   SILU_TRACE_K(0);
   const int tid = threadIdx.x, h = tid & (kH - 1), wg = tid >> 7, lane = tid & 31;
@@ -324,15 +344,13 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
                  sYh = sXh + kY, sYl = sYh + kXTile;
   // TMEM columns: D1 = [a2 - b2 | e], D2 = [dh1 | f] (kCP each), D3 = dW2, D4 = M
   constexpr uint32_t cD1 = 0, cD2 = 128, cD3 = 256, cD4 = 384;
-  // store bases for this thread's column h and its rows kPPT g + i: rb[i & 7] + i * 128
-  uint32_t rb[8];
-  {
-    const int r0 = kPPT * wg;
-    const uint32_t col = sXh + (uint32_t)((h >> 6) * kXHalf + (h & 7) * 2 + 128 * r0);
-    const int hc = (h >> 3) & 7;
-#pragma unroll
-    for (int m = 0; m < 8; ++m) rb[m] = col + (uint32_t)((hc ^ ((r0 + m) & 7)) << 4);
-  }
+  // store addresses of this thread's hidden unit h in the X hi tile (primal columns): the
+  // 8-particle group its warpgroup covers completely and the half group it shares
+  // (warpgroup particles 12 wg .. 12 wg + 11: groups {0, 1lo}, {1hi, 2}, {3, 4lo}, {4hi, 5})
+  const bool half_first = (wg & 1) != 0;
+  const uint32_t hofs = (uint32_t)((h >> 3) * 128 + (h & 7) * 16);
+  const uint32_t xa8 = sXh + hofs + (uint32_t)((wg & 1 ? 3 * (wg >> 1) + 2 : 3 * (wg >> 1)) * umma::kActGroup);
+  const uint32_t xa4 = sXh + hofs + (uint32_t)((3 * (wg >> 1) + 1) * umma::kActGroup) + (half_first ? 8u : 0u);
   float (*red)[4 * kCP] = reinterpret_cast<float (*)[4 * kCP]>(Xh + kY);
   float4* tgt = reinterpret_cast<float4*>(Xh + kY + kRedBytes);
 
@@ -431,15 +449,15 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           // in the D2 columns)
           const bool odd = iit & 1;
           const uint32_t xb = odd ? sBh : sXh;
-          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(tm + (odd ? cD2 : cD1), sW2h,
-                                                                sW2l, xb, xb + kXTile, false);
+          umma::gemm_split_v<umma::kWK, umma::kActMN, kCP, 8>(tm + (odd ? cD2 : cD1), sW2h, sW2l, xb,
+                                                              xb + kXTile, false);
         } else {
-          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(tm + cD1, sW2h, sW2l, sXh, sXl,
-                                                                false);  // W2 h1
+          umma::gemm_split_v<umma::kWK, umma::kActMN, kCP, 8>(tm + cD1, sW2h, sW2l, sXh, sXl,
+                                                              false);  // W2 h1
         }
         if (DIV) {
           umma::commit_elect(&S.bar[3]);  // primal half: F2a's s partials start on it
-          umma::gemm_split<false, false, kCP, 8, 16384, kXHalf, true>(
+          umma::gemm_split_v<umma::kWK, umma::kActMN, kCP, 8>(
               tm + cD1 + kCP, sBh, sBl, sXh + kDivRows, sXl + kDivRows, false);  // B d1
         }
         umma::commit_elect(&S.bar[0]);
@@ -454,10 +472,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           // tensor pipe while the FP32 side does the s / div reductions and F2b.
           handoff_wait(9);  // Y divergence rows written (F2a of chunk c)
           umma::fence_after();
-          umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(
+          umma::gemm_split_v<umma::kActK, umma::kActK, 128, kCP / 16>(
               tm + cD4, sYh + kDivRows, sYl + kDivRows, sXh + kDivRows, sXl + kDivRows,
               acc3);  // y2 d1^T
-          umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(
+          umma::gemm_split_v<umma::kWMN, umma::kActMN, kCP, 8>(
               tm + cD2 + kCP, sBh, sBl, sYh + kDivRows, sYl + kDivRows, false);  // B^T y2
           __syncwarp();
         }
@@ -466,8 +484,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         SILU_TRACE_I(12);
         {
           // G3 first: the next chunk's layer-1 sweep waits for it (X, Y reuse)
-          umma::gemm_split<true, true, 128, kCP / 16, kXHalf, kXHalf, true>(tm + cD3, sYh, sYl, sXh,
-                                                                      sXl, acc3);  // da2 h1^T
+          umma::gemm_split_v<umma::kActK, umma::kActK, 128, kCP / 16>(tm + cD3, sYh, sYl, sXh, sXl,
+                                                                      acc3);  // da2 h1^T
           umma::commit_elect(&S.bar[1]);
 #ifdef SPIC_SILU_TRACE_G3  // timing diagnostic: stamp G3's completion before issuing G2
           {
@@ -476,7 +494,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
             SILU_TRACE_I(14);
           }
 #endif
-          umma::gemm_split<true, false, kCP, 8, 16384, kXHalf, true>(tm + cD2, sW2h, sW2l, sYh, sYl,
+          umma::gemm_split_v<umma::kWMN, umma::kActMN, kCP, 8>(tm + cD2, sW2h, sW2l, sYh, sYl,
                                                                false);  // W2^T da2
           umma::commit_elect(&S.bar[2]);
         }
@@ -514,11 +532,16 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
                        : "memory");
         }
         wg_sync(wg);
+        {
+          float f1h[kPPT];
 #pragma unroll
-        for (int i = 0; i < kPPT; ++i) {
-          const float4 u = get_u(S.u[buf], p0 + i);
-          const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
-          st_split(rb[i & 7] + (buf ? xdelta : 0u) + i * 128, a * sigmoid(a));
+          for (int i = 0; i < kPPT; ++i) {
+            const float4 u = get_u(S.u[buf], p0 + i);
+            const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
+            f1h[i] = a * sigmoid(a);
+          }
+          const uint32_t xo = buf ? xdelta : 0u;
+          store_act12(xa8 + xo, xa4 + xo, half_first, f1h);
         }
         fence_proxy_async();
         umma::fence_before();
@@ -638,20 +661,17 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         un2(mul2(sg, fma2(a, sub2(one2, sg), one2)), f1d[i], f1d[i + 1]);
       }
       wait_g3();
-#pragma unroll
-      for (int i = 0; i < kPPT; ++i) {
-        st_split(rb[i & 7] + i * 128, f1h[i]);
-        st_split(rb[i & 7] + kDivRows + i * 128, f1d[i]);
-      }
+      store_act12(xa8, xa4, half_first, f1h);
+      store_act12(xa8 + kDivRows, xa4 + kDivRows, half_first, f1d);
     } else {
+      float f1h[kPPT];
 #pragma unroll
       for (int i = 0; i < kPPT; ++i) {
         const float4 u = get_u(S.u[ub], p0 + i);
         const float a = fmaf(w1[3], u.w, fmaf(w1[2], u.z, fmaf(w1[1], u.y, fmaf(w1[0], u.x, bb1))));
-        const float sg = sigmoid(a);
-        st_split(rb[i & 7] + i * 128, a * sg);
-        if (DIV) st_split(rb[i & 7] + kDivRows + i * 128, sg * fmaf(a, 1.f - sg, 1.f));
+        f1h[i] = a * sigmoid(a);
       }
+      store_act12(xa8, xa4, half_first, f1h);
     }
     fence_proxy_async();
     umma::fence_before();
@@ -682,6 +702,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       float va[16], ve[16];
       umma::tmem_ld12(tl + cD1 + p0, va);
       float v32[32], v16[16];
+      float y2v[kPPT];
       const f2 one2 = mk2(1.f, 1.f);
 #pragma unroll
       for (int pp = 0; pp < kPPT; pp += 2) {  // two particles per f32x2 lane pair
@@ -697,11 +718,12 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         un2(DIV ? mul2(sg, fma2(a2, sub2(one2, sg), one2)) : mk2(0.f, 0.f), d0[3], d1[3]);
         if (DIV) {  // Y divergence rows y2 = 2w d2 (no score dependence): G3 / G2 div halves
           const float wa = S.w[p0 + pp], wb = S.w[p0 + pp + 1];
-          st_split(rb[pp & 7] + kY + kDivRows + pp * 128, (wa + wa) * d0[3]);
-          st_split(rb[(pp + 1) & 7] + kY + kDivRows + (pp + 1) * 128, (wb + wb) * d1[3]);
+          y2v[pp] = (wa + wa) * d0[3];
+          y2v[pp + 1] = (wb + wb) * d1[3];
         }
       }
       if (DIV) {
+        store_act12(xa8 + kY + kDivRows, xa4 + kY + kDivRows, half_first, y2v);
         fence_proxy_async();
         umma::fence_before();
         handoff_arrive(9);
@@ -763,7 +785,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     {
       const f2 z2 = mk2(0.f, 0.f), one2 = mk2(1.f, 1.f);
       f2 aw3[3] = {z2, z2, z2}, ab2 = z2;
-      float va[16], ve[16];
+      float va[16], ve[16], da2v[kPPT];
       umma::tmem_ld12(tl + cD1 + p0, va);
       if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
 #pragma unroll
@@ -787,11 +809,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         aw3[1] = fma2(gy, h2, aw3[1]);
         aw3[2] = fma2(gz, h2, aw3[2]);
         ab2 = add2(ab2, da2);
-        float da_a, da_b;
-        un2(da2, da_a, da_b);
-        st_split(rb[pp & 7] + kY + pp * 128, da_a);
-        st_split(rb[(pp + 1) & 7] + kY + (pp + 1) * 128, da_b);
+        un2(da2, da2v[pp], da2v[pp + 1]);
       }
+      store_act12(xa8 + kY, xa4 + kY, half_first, da2v);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         float lo, hi;

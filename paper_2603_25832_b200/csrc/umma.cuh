@@ -44,6 +44,46 @@ __device__ __forceinline__ uint32_t tile_off_h(int r, int c, uint32_t half) {
          (uint32_t)(r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4) + (c & 7) * 2);
 }
 
+// ---- activation tiles: no-swizzle ("interleaved") core-matrix layout --------------------
+// The X / Y tiles hold P particle columns x 128 hidden units as 8 x 8 core matrices of
+// 128 contiguous bytes: element (p, h) at
+//     (p / 8) * kActGroup + (h / 8) * 128 + (h % 8) * 16 + (p % 8) * 2.
+// A thread that owns hidden unit h writes 8 consecutive particles with ONE 16-byte store (and
+// a warp's 32 stores cover 512 contiguous bytes, conflict free), instead of 8 two-byte stores
+// into a particle-major swizzled tile. The same bytes are an MN-major operand over
+// (N = particles, K = h): LBO = 128 between the 8-wide K groups, SBO = kActGroup between the
+// 8-particle groups; and a K-major operand over (M or N = h, K = particles): LBO = kActGroup,
+// SBO = 128 (canonical INTERLEAVE layouts of the sm_100 shared-memory descriptor).
+constexpr uint32_t kActGroup = 2048;  // bytes per group of 8 particles (16 K-groups x 128 B)
+
+__device__ __forceinline__ uint64_t sdesc_i(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // layout type 0: no swizzle
+}
+
+// operand views of the split-BF16 GEMMs
+enum View {
+  kWK = 0,    // 128-row SWIZZLE_128B tile read K-major (rows = M, cols = K)
+  kWMN = 1,   // the same tile read MN-major (rows = K, cols = M)
+  kActMN = 2, // activation tile as (N = particles, K = h), MN-major; K-step = 16 hidden units
+  kActK = 3   // activation tile as (M / N = h, K = particles), K-major; K-step = 16 particles
+};
+template <int V>
+__device__ __forceinline__ uint64_t view_desc(uint32_t tile) {
+  if constexpr (V == kWK) return desc_k(tile, 0, 16384);
+  else if constexpr (V == kWMN) return desc_mn(tile, 0, 16384);
+  else if constexpr (V == kActMN) return sdesc_i(tile, 128, kActGroup);
+  else return sdesc_i(tile, kActGroup, 128);
+}
+template <int V>
+__host__ __device__ constexpr uint64_t view_step(int ks) {  // start-address increment, 16-B units
+  if constexpr (V == kWK) return (uint64_t)(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4);
+  else if constexpr (V == kWMN) return (uint64_t)(ks * 2048 >> 4);
+  else if constexpr (V == kActMN) return (uint64_t)(ks * 256 >> 4);
+  else return (uint64_t)(ks * 2 * kActGroup >> 4);
+}
+__host__ __device__ constexpr uint32_t view_mn(int V) { return (V == kWMN || V == kActMN) ? 1u : 0u; }
+
 // instruction descriptor: kind::f16, A/B bf16, D f32, M = 128, N, operand majors
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t a_mn, uint32_t b_mn, uint32_t N = 128) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) |
@@ -100,6 +140,22 @@ __device__ __forceinline__ void gemm_split(uint32_t d_tmem, uint32_t a_hi, uint3
       mma(d_tmem, ah0 + ao, bl0 + bo, id, 1u);
       mma(d_tmem, al0 + ao, bh0 + bo, id, 1u);
     }
+  }
+}
+
+// The same over operand views (see View): warp-wide issue, descriptors built once per GEMM.
+template <int AV, int BV, int N, int KSTEPS>
+__device__ __forceinline__ void gemm_split_v(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
+                                             uint32_t b_hi, uint32_t b_lo, bool accumulate) {
+  constexpr uint32_t id = idesc_bf16(view_mn(AV), view_mn(BV), (uint32_t)N);
+  const uint64_t ah0 = view_desc<AV>(a_hi), al0 = view_desc<AV>(a_lo);
+  const uint64_t bh0 = view_desc<BV>(b_hi), bl0 = view_desc<BV>(b_lo);
+#pragma unroll
+  for (int ks = 0; ks < KSTEPS; ++ks) {
+    const uint64_t ao = view_step<AV>(ks), bo = view_step<BV>(ks);
+    mma_elect(d_tmem, ah0 + ao, bh0 + bo, id, (accumulate || ks > 0) ? 1u : 0u);
+    mma_elect(d_tmem, ah0 + ao, bl0 + bo, id, 1u);
+    mma_elect(d_tmem, al0 + ao, bh0 + bo, id, 1u);
   }
 }
 
