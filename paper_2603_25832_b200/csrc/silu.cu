@@ -87,8 +87,9 @@ struct SiluShared {
 constexpr uint32_t kXTile = 2 * (kCP / 8) * umma::kActGroup;  // 96 particle columns: 24 KB
 // per-warp-quarter partials (s0, s1, s2, div) per particle and the MSE targets live in the Y
 // tile while it is free (after the previous chunk's G2 / G3, before this chunk's F2b)
-constexpr uint32_t kRedBytes = 4 * 4 * kCP * sizeof(float);
-static_assert(kRedBytes + kCP * sizeof(float4) <= kXTile, "scratch fits the Y tile");
+constexpr uint32_t kRedBytes = 4 * 4 * kPPT * sizeof(float);  // per warpgroup
+static_assert(kRedBytes <= umma::kActGroup && kCP * sizeof(float4) <= umma::kActGroup,
+              "scratch fits one 8-particle group of the Y tile");
 constexpr size_t kSiluTiles = 4 * umma::kTileBytes + 4 * kXTile;
 // The dynamic shared window starts 1024-B aligned on sm_100 (checked in-kernel: a
 // misaligned start traps), so no alignment slack is requested.
@@ -351,8 +352,14 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
   const uint32_t hofs = (uint32_t)((h >> 3) * 128 + (h & 7) * 16);
   const uint32_t xa8 = sXh + hofs + (uint32_t)((wg & 1 ? 3 * (wg >> 1) + 2 : 3 * (wg >> 1)) * umma::kActGroup);
   const uint32_t xa4 = sXh + hofs + (uint32_t)((3 * (wg >> 1) + 1) * umma::kActGroup) + (half_first ? 8u : 0u);
-  float (*red)[4 * kCP] = reinterpret_cast<float (*)[4 * kCP]>(Xh + kY);
-  float4* tgt = reinterpret_cast<float4*>(Xh + kY + kRedBytes);
+  // per-warp-quarter partials of this warpgroup's 12 particles: in the Y tile while it is
+  // free, inside the 8-particle group the warpgroup alone writes in F2b — so F2b of a faster
+  // warpgroup never touches another warpgroup's partials and the hand-over to F2b needs only a
+  // warpgroup barrier. The MSE targets sit in group 1 (shared by warpgroups 0 and 1: the MSE
+  // mode keeps the CTA-wide barrier).
+  float (*red)[4 * kPPT] = reinterpret_cast<float (*)[4 * kPPT]>(
+      Xh + kY + (size_t)(wg & 1 ? 3 * (wg >> 1) + 2 : 3 * (wg >> 1)) * umma::kActGroup);
+  float4* tgt = reinterpret_cast<float4*>(Xh + kY + umma::kActGroup);
 
   // per-thread sums over the CTA's chunks in float32 (<= ~150 chunk terms each); the CTA and
   // cross-CTA combines are float64
@@ -571,8 +578,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           }
           const float r32 = transpose_reduce32(v32, lane);
           const float r16 = transpose_reduce16(v16, lane);
-          red[quarter][4 * p0 + lane] = r32;
-          if (lane < 16) red[quarter][4 * (p0 + 8) + lane] = r16;
+          red[quarter][lane] = r32;
+          if (lane < 16) red[quarter][32 + lane] = r16;
         }
         wg_sync(wg);
         if (wtid < kPPT) {
@@ -580,8 +587,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           float sc[3];
 #pragma unroll
           for (int k = 0; k < 3; ++k)
-            sc[k] = b3[k] + ((red[0][4 * p + k] + red[1][4 * p + k]) +
-                             (red[2][4 * p + k] + red[3][4 * p + k]));
+            sc[k] = b3[k] + ((red[0][4 * wtid + k] + red[1][4 * wtid + k]) +
+                             (red[2][4 * wtid + k] + red[3][4 * wtid + k]));
           const int64_t q = cprev * kCP + p;
           if (q < n) sw_out[q] = make_float4(sc[0], sc[1], sc[2], sw[q].w);
         }
@@ -740,8 +747,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       }
       const float r32 = transpose_reduce32(v32, lane);
       const float r16 = transpose_reduce16(v16, lane);
-      red[quarter][4 * p0 + lane] = r32;
-      if (lane < 16) red[quarter][4 * (p0 + 8) + lane] = r16;
+      red[quarter][lane] = r32;
+      if (lane < 16) red[quarter][32 + lane] = r16;
     }
     wg_sync(wg);
     SILU_TRACE(5);
@@ -750,9 +757,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       float s[3], dv = 0.f;
 #pragma unroll
       for (int k = 0; k < 3; ++k)
-        s[k] = b3[k] + ((red[0][4 * p + k] + red[1][4 * p + k]) +
-                        (red[2][4 * p + k] + red[3][4 * p + k]));
-      dv = (red[0][4 * p + 3] + red[1][4 * p + 3]) + (red[2][4 * p + 3] + red[3][4 * p + 3]);
+        s[k] = b3[k] + ((red[0][4 * wtid + k] + red[1][4 * wtid + k]) +
+                        (red[2][4 * wtid + k] + red[3][4 * wtid + k]));
+      dv = (red[0][4 * wtid + 3] + red[1][4 * wtid + 3]) + (red[2][4 * wtid + 3] + red[3][4 * wtid + 3]);
       const int64_t q = c * kCP + p;
       if (MODE == 0) {
         if (q < n) sw_out[q] = make_float4(s[0], s[1], s[2], sw[q].w);
@@ -778,7 +785,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       wg_sync(wg);
       continue;
     }
-    compute_sync();  // F2b overwrites the Y tile that holds every warpgroup's partials
+    // F2b overwrites the Y tile that holds the partials: this warpgroup's own (ISM), or, with
+    // the MSE targets in a shared group, anybody's
+    if (MODE == 1) wg_sync(wg); else compute_sync();
     SILU_TRACE(6);
 
     // F2b: reverse through layer 2 -> Y rows p (da2) and 32 + p (y2 = 2w d2); dW3, db2
