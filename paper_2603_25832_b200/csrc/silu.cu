@@ -724,9 +724,9 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         // d2 = silu'(a2) for now; times e (the div half of G1) below
         un2(DIV ? mul2(sg, fma2(a2, sub2(one2, sg), one2)) : mk2(0.f, 0.f), d0[3], d1[3]);
         if (DIV) {  // Y divergence rows y2 = 2w d2 (no score dependence): G3 / G2 div halves
-          const float wa = S.w[p0 + pp], wb = S.w[p0 + pp + 1];
-          y2v[pp] = (wa + wa) * d0[3];
-          y2v[pp + 1] = (wb + wb) * d1[3];
+          const float2 wab = *reinterpret_cast<const float2*>(&S.w[p0 + pp]);  // one 8-B load
+          y2v[pp] = (wab.x + wab.x) * d0[3];
+          y2v[pp + 1] = (wab.y + wab.y) * d1[3];
         }
       }
       if (DIV) {
