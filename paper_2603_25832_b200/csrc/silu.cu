@@ -383,8 +383,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     return;
 #endif
     float vd[16], vf[16];
-    umma::tmem_ld12(tl + cD2 + p0, vd);
-    if (DIV) umma::tmem_ld12(tl + cD2 + kCP + p0, vf);
+    if (DIV) umma::tmem_ld12x2(tl + cD2 + p0, tl + cD2 + kCP + p0, vd, vf);
+    else umma::tmem_ld12(tl + cD2 + p0, vd);
     const f2 one2 = mk2(1.f, 1.f);
     f2 aw[4] = {mk2(0.f, 0.f), mk2(0.f, 0.f), mk2(0.f, 0.f), mk2(0.f, 0.f)}, ab = mk2(0.f, 0.f);
 #pragma unroll
@@ -795,8 +795,8 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       const f2 z2 = mk2(0.f, 0.f), one2 = mk2(1.f, 1.f);
       f2 aw3[3] = {z2, z2, z2}, ab2 = z2;
       float va[16], ve[16], da2v[kPPT];
-      umma::tmem_ld12(tl + cD1 + p0, va);
-      if (DIV) umma::tmem_ld12(tl + cD1 + kCP + p0, ve);
+      if (DIV) umma::tmem_ld12x2(tl + cD1 + p0, tl + cD1 + kCP + p0, va, ve);
+      else umma::tmem_ld12(tl + cD1 + p0, va);
 #pragma unroll
       for (int pp = 0; pp < kPPT; pp += 2) {  // two particles per f32x2 lane pair
         const float4 Ga = S.gs[p0 + pp], Gb = S.gs[p0 + pp + 1];
@@ -844,7 +844,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       layer1_reverse(ub);
     }
     umma::fence_before();
-    wg_sync(wg);
+    // The ISM needs no barrier here: everything the next chunk's loaders overwrite (S.u of two
+    // chunks ago, S.w, the targets) was last read before this chunk's warpgroup barriers, and
+    // the shared partials / gs are rewritten only behind the next chunk's own barriers.
+    if (MODE != 1) wg_sync(wg);
     SILU_TRACE(8);
     ub ^= 1;
   }

@@ -275,6 +275,33 @@ __device__ __forceinline__ void tmem_ld12(uint32_t taddr, float (&f)[16]) {
   for (int i = 12; i < 16; ++i) f[i] = 0.f;
 }
 
+// two 12-column slices of this thread's lane with one wait (the second load's latency hides
+// behind the first's)
+__device__ __forceinline__ void tmem_ld12x2(uint32_t ta, uint32_t tb, float (&f)[16], float (&g)[16]) {
+  uint32_t r[24];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%24];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [%25];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8,%9,%10,%11}, [%26];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%12,%13,%14,%15}, [%27];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%16,%17,%18,%19}, [%28];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%20,%21,%22,%23}, [%29];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23])
+      : "r"(ta), "r"(ta + 4), "r"(ta + 8), "r"(tb), "r"(tb + 4), "r"(tb + 8)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    f[i] = __uint_as_float(r[i]);
+    g[i] = __uint_as_float(r[12 + i]);
+  }
+#pragma unroll
+  for (int i = 12; i < 16; ++i) f[i] = g[i] = 0.f;
+}
+
 // split x into bf16 hi + lo (x ~= hi + lo to ~2^-17 relative) and store both tiles
 __device__ __forceinline__ void store_split(uint8_t* hi_tile, uint8_t* lo_tile, int r, int c,
                                             float x) {
