@@ -683,6 +683,38 @@ def test_antisymmetric_pair_path_matches_ordered_and_oracle(spic, case):
     assert mom < 1e-6, mom
 
 
+@pytest.mark.parametrize("cfg", [0, 2, 9, 10, 11, 12, 13, 14, 15])
+def test_antisymmetric_pair_kernel_shapes_match_oracle(spic, cfg):
+    """Every selectable shape of the unordered-pair kernel (SPIC_SYM_CFG: threads x targets per
+    thread x resident CTAs; 11 = the default 64 x 10, 0 = the 128 x 4 of round 1) gives the
+    same field as the float64 oracle on an ensemble whose cell populations are not multiples of
+    any tile size (empty cells, one dense cell, a z = 0 pair, periodic wrap pairs). Bound: 1e-4
+    relative L2 and 1e-4 max|U| per particle (check_field)."""
+    from paper_2603_25832_b200.collision import build_cell_index, gather_scores_sorted
+    from paper_2603_25832_b200.pic import Grid
+
+    rng = np.random.default_rng(40 + cfg)
+    n, M, L, S = 30011, 16, 8.0, 8
+    x = np.concatenate([rng.uniform(2.0, 2.5, 14000), rng.uniform(0, L, n - 14000 - 10),
+                        np.full(10, 4.0 - 1e-6)])
+    x = x.astype(np.float32).astype(np.float64)
+    x[x >= L] = 0.0
+    v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
+    v[5] = v[6]
+    s = (rng.normal(size=(n, 3)) * 2).astype(np.float32).astype(np.float64)
+    p = ens(x, v, np.full(n, L / n))
+    grid = Grid(M, L / M)
+    ci = build_cell_index(p, grid, S=S)
+    gather_scores_sorted(ci, s)
+    perm = ci.perm.cpu().numpy()
+    ref = O.collision_force(x, v, p.w.double().cpu().numpy(), s, grid.eta, M, -3.0)[perm].T
+    U = _landau_sorted_env(p, grid, ci, {"SPIC_SYM_CFG": str(cfg)})
+    check_field(U, ref)
+    assert np.array_equal(U, _landau_sorted_env(p, grid, ci, {"SPIC_SYM_CFG": str(cfg)}))
+    mom = np.abs(U.sum(1)).max() / np.abs(U).sum()
+    assert mom < 1e-6, mom
+
+
 def test_antisymmetric_pair_path_partial_cell_range(spic):
     """spic_landau_range over owned cells [c_lo, c_hi) (a domain rank's targets, halo cell
     c_lo - 1 contributing through its forward window) equals the full-ring result there."""
@@ -770,6 +802,34 @@ def test_symmetric_blob_path_matches_ordered_and_oracle(spic, case):
     check_field(s_ord, ref, tol=2e-4)
     check_field(s_fb, ref, tol=2e-4)
     check_field(s_sym, s_ord, tol=1e-4)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+@pytest.mark.parametrize("bw", [None, 0.3])
+def test_symmetric_blob_kernel_shapes_match_oracle(spic, cfg, bw, monkeypatch):
+    """Every selectable shape of the unordered-pair blob kernel (SPIC_BLOB_SYM_CFG: 128 x 4,
+    64 x 8 (default), 64 x 10 targets) against the float64 oracle, Silverman and fixed
+    bandwidth, on cell populations that are not multiples of any tile size. Bound 2e-4
+    (check_field; the blob sums use ex2.approx)."""
+    from paper_2603_25832_b200.collision import build_cell_index
+    from paper_2603_25832_b200.pic import Grid
+    from paper_2603_25832_b200.score import blob_score
+
+    monkeypatch.setenv("SPIC_BLOB_SYM_CFG", str(cfg))
+    rng = np.random.default_rng(70 + cfg)
+    n, M, L, S = 30011, 16, 8.0, 8
+    x = np.concatenate([rng.uniform(2.0, 2.5, 14000), rng.uniform(0, L, n - 14000)])
+    v = rng.normal(size=(n, 3)) * (1.0 + 0.5 * np.sin(x)[:, None])
+    x = x.astype(np.float32).astype(np.float64)
+    x[x >= L] = 0.0
+    v = v.astype(np.float32).astype(np.float64)
+    p = ens(x, v, np.full(n, L / n))
+    grid = Grid(M, L / M)
+    ci = build_cell_index(p, grid, S=S)
+    ref = O.blob_score(x, v, p.w.double().cpu().numpy(), grid.eta, M, bw)
+    got = blob_score(p, ci, grid, bw).double().cpu().numpy()
+    check_field(got, ref, tol=2e-4)
+    assert np.array_equal(got, blob_score(p, ci, grid, bw).double().cpu().numpy())
 
 
 @pytest.mark.parametrize("n,M,S", [(3000, 16, 8), (100000, 64, 16), (1 << 20, 128, 64),
