@@ -107,6 +107,27 @@ def test_silu_ism_loss_and_grad_matches_oracle(lib, n):
         assert relL2(g[a:b], ref_g[a:b]) <= 1e-4, (name, relL2(g[a:b], ref_g[a:b]))
 
 
+def test_silu_ism_is_bit_reproducible_over_many_launches(lib):
+    """The ISM kernel synchronises its phases with warpgroup barriers, mbarriers and hand-off
+    barriers only (no CTA-wide barrier inside a chunk). 40 launches on the same 2^19 + 77
+    particles (~74 chunks per CTA, flushes of the TMEM accumulators included) must give the
+    same loss and gradient bits every time — any race between a warpgroup's partials, the
+    chunk records or the operand tiles would show up as a difference."""
+    from paper_2603_25832_b200.silu_net import silu_ism_loss_and_grad
+
+    L = 4 * math.pi
+    n = (1 << 19) + 77
+    params = _params(seed=11)
+    x, v, w = _ensemble(n, L, seed=12)
+    net = _net(params)
+    loss0, g0 = silu_ism_loss_and_grad(net, x, v, w, L)
+    g0 = g0.clone()
+    for _ in range(39):
+        loss, g = silu_ism_loss_and_grad(net, x, v, w, L)
+        assert loss == loss0
+        assert torch.equal(g, g0)
+
+
 def test_silu_sorted_records_quirk_and_weights(lib):
     """Record inputs: x' = x - L (the %M quirk record) maps back to x; per-particle weights."""
     from paper_2603_25832_b200 import _lib
