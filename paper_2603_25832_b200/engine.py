@@ -110,7 +110,7 @@ class Simulation:
             self.diag[row].copy_(self.diag[self._graph_row])
 
     # ---- one step ---------------------------------------------------------------------------
-    def step(self, row: int, draw: bool = True) -> None:
+    def step(self, row: int, draw: bool = True, after_push=None) -> None:
         p, g, ci, f = self.p, self.grid, self.ci, self.f
         n, dv = p.n, p.dv
         st = _lib.stream_handle()
@@ -118,6 +118,8 @@ class Simulation:
             _lib.call("spic_push", _lib.ptr(p.x), _lib.ptr(p.vp), n, n, dv, _lib.ptr(f.E1),
                       _lib.ptr(f.E2), _lib.ptr(f.B3), g.M, float(g.eta), self.dt,
                       _lib.ptr(self.flags), st)
+        if after_push is not None:  # the positions are final from here on (step_host)
+            after_push()
         with nvtx("bin"):
             build_cell_index(p, g, self.S, out=ci)
         d = self.diag[row]
@@ -161,12 +163,26 @@ class Simulation:
         """Public end-to-end step on HOST buffers (pinned float32 x (n,), v planes (dv, n),
         float64 diag (DIAG_W,)): H2D of the state, one device step, D2H of the updated state,
         of the step's diagnostics row and (if given, pinned int32 (8,)) of the error flags —
-        all enqueued on the current stream; check_host(flags_host) after a sync raises the
+        all enqueued on (or joined into) the current stream; check_host(flags_host) after a sync raises the
         reference's exception for the step, as run() does once per step."""
         self.p.x.copy_(x_host, non_blocking=True)
         self.p.vp.copy_(v_host, non_blocking=True)
-        self.step(row)
-        x_host.copy_(self.p.x, non_blocking=True)
+        # the push leaves the step's final positions: their D2H copy runs on a second stream
+        # under the rest of the step (binning, deposit, score, collision only read x)
+        main = torch.cuda.current_stream()
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream()
+            self._ev_push, self._ev_xcopy = torch.cuda.Event(), torch.cuda.Event()
+
+        def copy_x():
+            self._ev_push.record(main)
+            self._copy_stream.wait_event(self._ev_push)
+            with torch.cuda.stream(self._copy_stream):
+                x_host.copy_(self.p.x, non_blocking=True)
+                self._ev_xcopy.record(self._copy_stream)
+
+        self.step(row, after_push=copy_x)
+        main.wait_event(self._ev_xcopy)  # a sync on the current stream covers the x copy
         v_host.copy_(self.p.vp, non_blocking=True)
         diag_host.copy_(self.diag[row], non_blocking=True)
         if flags_host is not None:

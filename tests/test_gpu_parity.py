@@ -1127,6 +1127,47 @@ def test_engine_step_with_nvtx_ranges(spic, monkeypatch):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
+def test_engine_step_host_equals_device_step(spic):
+    """Simulation.step_host (the bench's e2e path: pinned host buffers, H2D of the state, one
+    device step, D2H of the state, the diagnostics row and the flags, with the positions'
+    D2H overlapped on a second stream) returns exactly what step() leaves on the device, over
+    three consecutive steps fed from the returned host buffers."""
+    from paper_2603_25832_b200.engine import Simulation
+    from paper_2603_25832_b200.pic import Grid, deposit, poisson_solve
+    from paper_2603_25832_b200.score import BlobEstimator
+    from paper_2603_25832_b200.state import FieldState, ParticleEnsemble
+
+    rng = np.random.default_rng(3)
+    n, M, L = 8192, 16, 4 * math.pi
+    x = rng.uniform(0, L, n).astype(np.float32).astype(np.float64)
+    v = rng.normal(size=(n, 3)).astype(np.float32).astype(np.float64)
+
+    def make():
+        p = ParticleEnsemble.from_arrays(x, v, np.full(n, L / n))
+        grid = Grid(M, L / M)
+        rho, _ = deposit(p, grid)
+        rho_ion = float(rho.sum()) * grid.eta / L
+        f = FieldState.zeros(M, 3, rho_ion)
+        f.E1.copy_(poisson_solve(rho, rho_ion, grid))
+        return p, Simulation(p, f, grid, dt=0.05, nu=0.1, mode="VPL", gamma=-3.0,
+                             estimator=BlobEstimator(grid, None), max_rows=4)
+
+    p_dev, sim_dev = make()
+    p_host, sim_host = make()
+    xh = p_host.x.cpu().pin_memory()
+    vh = p_host.vp.cpu().pin_memory()
+    dh = torch.zeros_like(sim_host.diag[0], device="cpu").pin_memory()
+    fh = torch.zeros(8, dtype=torch.int32).pin_memory()
+    for row in (1, 2, 3):
+        sim_dev.step(row)
+        sim_host.step_host(row, xh, vh, dh, fh)
+        torch.cuda.synchronize()
+        sim_host.check_host(fh)
+        assert torch.equal(xh, p_dev.x.cpu())
+        assert torch.equal(vh, p_dev.vp.cpu())
+        assert torch.equal(dh, sim_dev.diag[row].cpu())
+
+
 def test_empty_ensemble_operators(spic):
     """n = 0 through every operator of the path: empty outputs, zero grid moments, no error
     (the reference's numpy forms return empty arrays / zero sums for an empty ensemble)."""
