@@ -875,56 +875,57 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     float* WM = reinterpret_cast<float*>(Xh);  // the X and Y tiles are free now
     float tw3[3] = {0.f, 0.f, 0.f};
     {
-      float v[32], m[32];
-      umma::tmem_ld32(tl + cD3 + (uint32_t)(32 * wg), v);
-      if (DIV) umma::tmem_ld32(tl + cD4 + (uint32_t)(32 * wg), m);
-      if (nflush) {  // the earlier windows' sums (fixed order: earlier windows first)
-        const float4* g3 = reinterpret_cast<const float4*>(acc_row);
-        const float4* g4 = reinterpret_cast<const float4*>(acc_row + kH * kH);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 a = g3[k];
-          v[4 * k] = a.x + v[4 * k]; v[4 * k + 1] = a.y + v[4 * k + 1];
-          v[4 * k + 2] = a.z + v[4 * k + 2]; v[4 * k + 3] = a.w + v[4 * k + 3];
-          if (DIV) {
-            const float4 b = g4[k];
-            m[4 * k] = b.x + m[4 * k]; m[4 * k + 1] = b.y + m[4 * k + 1];
-            m[4 * k + 2] = b.z + m[4 * k + 2]; m[4 * k + 3] = b.w + m[4 * k + 3];
-          }
-        }
-      }
       // the dW2 row block (rows 32q.. of this warp, columns 32g..32g+31) goes out through a
       // per-warp shared-memory transpose in two 16-column halves, so each store instruction
       // writes two 128-B row segments instead of 32 scattered doubles (free space after the
-      // per-h combine area: base + 56 KB .. + 124 KB, 4352 B per warp)
-      // this thread's W2 row segment W2[h][32g .. 32g+31] (128 B) by eight 16-B loads
-      float w2r[32];
-      if (DIV && !first) {
-        const float4* w2v = reinterpret_cast<const float4*>(W2 + h * kH + 32 * wg);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 t4 = __ldg(w2v + k);
-          w2r[4 * k] = t4.x; w2r[4 * k + 1] = t4.y; w2r[4 * k + 2] = t4.z; w2r[4 * k + 3] = t4.w;
-        }
-      }
+      // per-h combine area: base + 56 KB .. + 124 KB, 4352 B per warp). Each half loads its own
+      // 16 columns of D3 / D4, of the flushed sums and of the W2 row (48 live registers; with
+      // all 32 columns at once the block spilled most of them at the kernel's 96 registers)
       constexpr int kStg = 17;  // padded row stride (floats)
       float* stg = reinterpret_cast<float*>(base + 56 * 1024) + (size_t)(tid >> 5) * 32 * kStg;
       const int q32 = h & ~31;  // first row of this warp
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
+        const int c0 = 32 * wg + 16 * half;  // first column of this half
+        float v[16], m[16], w2r[16];
+        umma::tmem_ld16(tl + cD3 + (uint32_t)c0, v);
+        if (DIV) umma::tmem_ld16(tl + cD4 + (uint32_t)c0, m);
+        if (nflush) {  // the earlier windows' sums (fixed order: earlier windows first)
+          const float4* g3 = reinterpret_cast<const float4*>(acc_row + 16 * half);
+          const float4* g4 = reinterpret_cast<const float4*>(acc_row + kH * kH + 16 * half);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 a = g3[k];
+            v[4 * k] = a.x + v[4 * k]; v[4 * k + 1] = a.y + v[4 * k + 1];
+            v[4 * k + 2] = a.z + v[4 * k + 2]; v[4 * k + 3] = a.w + v[4 * k + 3];
+            if (DIV) {
+              const float4 b = g4[k];
+              m[4 * k] = b.x + m[4 * k]; m[4 * k + 1] = b.y + m[4 * k + 1];
+              m[4 * k + 2] = b.z + m[4 * k + 2]; m[4 * k + 3] = b.w + m[4 * k + 3];
+            }
+          }
+        }
+        if (DIV && !first) {  // this thread's W2 row segment W2[h][c0 .. c0 + 15]
+          const float4* w2v = reinterpret_cast<const float4*>(W2 + h * kH + c0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 t4 = __ldg(w2v + k);
+            w2r[4 * k] = t4.x; w2r[4 * k + 1] = t4.y; w2r[4 * k + 2] = t4.z; w2r[4 * k + 3] = t4.w;
+          }
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int i = 16 * half + j;
-          const int hp = 32 * wg + i;
-          float g = first ? 0.f : v[i];
+          const int hp = c0 + j;
+          float g = first ? 0.f : v[j];
           if (DIV && !first) {
-            const float Chh = fmaf(w3[2], W1[hp * 4 + 3], fmaf(w3[1], W1[hp * 4 + 2], w3[0] * W1[hp * 4 + 1]));
-            const float wm = w2r[i] * m[i];
-            g = fmaf(Chh, m[i], g);
+            const float4 w1c = __ldg(reinterpret_cast<const float4*>(W1) + hp);  // W1[hp][0..3]
+            const float Chh = fmaf(w3[2], w1c.w, fmaf(w3[1], w1c.z, w3[0] * w1c.y));
+            const float wm = w2r[j] * m[j];
+            g = fmaf(Chh, m[j], g);
             WM[h * kWMs + hp] = wm;
-            tw3[0] = fmaf(W1[hp * 4 + 1], wm, tw3[0]);
-            tw3[1] = fmaf(W1[hp * 4 + 2], wm, tw3[1]);
-            tw3[2] = fmaf(W1[hp * 4 + 3], wm, tw3[2]);
+            tw3[0] = fmaf(w1c.y, wm, tw3[0]);
+            tw3[1] = fmaf(w1c.z, wm, tw3[1]);
+            tw3[2] = fmaf(w1c.w, wm, tw3[2]);
           } else if (DIV) {
             WM[h * kWMs + hp] = 0.f;
           }
@@ -934,7 +935,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
 #pragma unroll
         for (int rr = 0; rr < 32; rr += 2) {
           const int r = rr + (lane >> 4), cc = lane & 15;
-          prow[(size_t)(q32 + r) * kH + 32 * wg + 16 * half + cc] = stg[r * kStg + cc];
+          prow[(size_t)(q32 + r) * kH + c0 + cc] = stg[r * kStg + cc];
         }
         __syncwarp();
       }
