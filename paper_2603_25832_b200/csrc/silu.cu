@@ -888,8 +888,10 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       for (int half = 0; half < 2; ++half) {
         const int c0 = 32 * wg + 16 * half;  // first column of this half
         float v[16], m[16], w2r[16];
+        if (half == 0) SILU_TRACE_K(8);
         umma::tmem_ld16(tl + cD3 + (uint32_t)c0, v);
         if (DIV) umma::tmem_ld16(tl + cD4 + (uint32_t)c0, m);
+        if (half == 0) SILU_TRACE_K(9);
         if (nflush) {  // the earlier windows' sums (fixed order: earlier windows first)
           const float4* g3 = reinterpret_cast<const float4*>(acc_row + 16 * half);
           const float4* g4 = reinterpret_cast<const float4*>(acc_row + kH * kH + 16 * half);
@@ -913,6 +915,7 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
             w2r[4 * k] = t4.x; w2r[4 * k + 1] = t4.y; w2r[4 * k + 2] = t4.z; w2r[4 * k + 3] = t4.w;
           }
         }
+        if (half == 0) SILU_TRACE_K(10);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int hp = c0 + j;
@@ -932,12 +935,14 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
           stg[lane * kStg + j] = g;
         }
         __syncwarp();
+        if (half == 0) SILU_TRACE_K(11);
 #pragma unroll
         for (int rr = 0; rr < 32; rr += 2) {
           const int r = rr + (lane >> 4), cc = lane & 15;
           prow[(size_t)(q32 + r) * kH + c0 + cc] = stg[r * kStg + cc];
         }
         __syncwarp();
+        if (half == 0) SILU_TRACE_K(12);
       }
     }
     SILU_TRACE_K(5);

@@ -80,6 +80,10 @@ int main(int argc, char** argv) {
          "final rows %lld\n", h[63 * 16 + 4] - h[63 * 16 + 2], h[63 * 16 + 5] - h[63 * 16 + 4],
          h[63 * 16 + 6] - h[63 * 16 + 5], h[63 * 16 + 7] - h[63 * 16 + 6],
          h[63 * 16 + 3] - h[63 * 16 + 7]);
+  if (h[63 * 16 + 12])
+    printf("epilogue dW2 block, first half: TMEM loads %lld, flushed sums + W2 row %lld, 16 columns %lld, "
+           "row stores %lld\n", h[63 * 16 + 9] - h[63 * 16 + 8], h[63 * 16 + 10] - h[63 * 16 + 9],
+           h[63 * 16 + 11] - h[63 * 16 + 10], h[63 * 16 + 12] - h[63 * 16 + 11]);
   printf("from F1 hand-off: issuer X-ready %+.0f, G1 issued %+.0f, G1 done %+.0f, F2b done %+.0f,\n"
          "  issuer Y-ready %+.0f, G3+G2 issued %+.0f; next chunk's F3 got G2 %+.0f after its F1 hand-off\n",
          a10 / cnt, a11 / cnt, a4 / cnt, a7 / cnt, a12 / cnt, a13 / cnt, a9 / cnt);
