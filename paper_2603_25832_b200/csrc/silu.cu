@@ -420,22 +420,28 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
     }
   };
 
-  // this thread's 32-column slice of D3 / D4 (row h, columns 32 wg ..) in the CTA's buffer
+  // this thread's 32-column slice of D3 / D4 (row h, columns 32 wg ..) in the CTA's buffer.
+  // Only this thread ever touches its slice, so the buffer is laid out for the access, not as
+  // a matrix: float4 number k (columns 32 wg + 4k ..) of row h sits at
+  // ((which * 4 + wg) * 8 + k) * 128 + h — a warp's 32 rows are 512 contiguous bytes per load
+  // instead of 32 half-used sectors.
   int nflush = 0;
-  float* acc_row = part_acc ? part_acc + (size_t)blockIdx.x * 2 * kH * kH + (size_t)h * kH + 32 * wg
-                            : nullptr;
+  float4* acc_row = part_acc ? reinterpret_cast<float4*>(part_acc + (size_t)blockIdx.x * 2 * kH * kH) +
+                                   (size_t)wg * 8 * kH + h
+                             : nullptr;
+  constexpr size_t kAccWhich = (size_t)kNWG * 8 * kH;  // float4 stride between D3 and D4 sums
   auto flush_acc = [&](uint32_t col, int which) {
     float t[32];
     umma::tmem_ld32(tl + col + (uint32_t)(32 * wg), t);
-    float4* g = reinterpret_cast<float4*>(acc_row + (size_t)which * kH * kH);
+    float4* g = acc_row + (size_t)which * kAccWhich;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       float4 a = make_float4(t[4 * k], t[4 * k + 1], t[4 * k + 2], t[4 * k + 3]);
       if (nflush) {
-        const float4 b = g[k];
+        const float4 b = g[k * kH];
         a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
       }
-      g[k] = a;
+      g[k * kH] = a;
     }
   };
   bool pending = false;  // the previous chunk's layer-1 reverse sweep is still to run (ISM)
@@ -893,15 +899,15 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
         if (DIV) umma::tmem_ld16(tl + cD4 + (uint32_t)c0, m);
         if (half == 0) SILU_TRACE_K(9);
         if (nflush) {  // the earlier windows' sums (fixed order: earlier windows first)
-          const float4* g3 = reinterpret_cast<const float4*>(acc_row + 16 * half);
-          const float4* g4 = reinterpret_cast<const float4*>(acc_row + kH * kH + 16 * half);
+          const float4* g3 = acc_row + (size_t)(4 * half) * kH;
+          const float4* g4 = g3 + kAccWhich;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float4 a = g3[k];
+            const float4 a = g3[k * kH];
             v[4 * k] = a.x + v[4 * k]; v[4 * k + 1] = a.y + v[4 * k + 1];
             v[4 * k + 2] = a.z + v[4 * k + 2]; v[4 * k + 3] = a.w + v[4 * k + 3];
             if (DIV) {
-              const float4 b = g4[k];
+              const float4 b = g4[k * kH];
               m[4 * k] = b.x + m[4 * k]; m[4 * k + 1] = b.y + m[4 * k + 1];
               m[4 * k + 2] = b.z + m[4 * k + 2]; m[4 * k + 3] = b.w + m[4 * k + 3];
             }
