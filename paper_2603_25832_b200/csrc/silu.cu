@@ -16,6 +16,7 @@
 // finalized by the shared AdamW kernel (adamw.cuh).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "adamw.cuh"
 #include "common.cuh"
@@ -715,28 +716,43 @@ __global__ void __launch_bounds__(kNT, 1) k_silu(const float* __restrict__ param
       float va[16], ve[16];
       umma::tmem_ld12(tl + cD1 + p0, va);
       float v32[32], v16[16];
-      float y2v[kPPT];
       const f2 one2 = mk2(1.f, 1.f);
+      // (instantiated for both warpgroup parities so the Y divergence rows leave as soon as a
+      // group's values exist: at most four packed words are pending instead of twelve floats)
+      auto f2a_loop = [&](auto hf_tag) {
+        constexpr bool HF = decltype(hf_tag)::value;  // half group (4 particles) first
+        uint32_t yh[4], yl[4];
 #pragma unroll
-      for (int pp = 0; pp < kPPT; pp += 2) {  // two particles per f32x2 lane pair
-        const f2 a2 = add2(mk2(va[pp], va[pp + 1]), mk2(bb2, bb2));
-        const f2 sg = sigmoid2(a2);
-        const f2 h2 = mul2(a2, sg);
-        float* d0 = pp < 8 ? &v32[4 * pp] : &v16[4 * (pp - 8)];
-        float* d1 = d0 + 4;
-        un2(mul2(mk2(w3[0], w3[0]), h2), d0[0], d1[0]);
-        un2(mul2(mk2(w3[1], w3[1]), h2), d0[1], d1[1]);
-        un2(mul2(mk2(w3[2], w3[2]), h2), d0[2], d1[2]);
-        // d2 = silu'(a2) for now; times e (the div half of G1) below
-        un2(DIV ? mul2(sg, fma2(a2, sub2(one2, sg), one2)) : mk2(0.f, 0.f), d0[3], d1[3]);
-        if (DIV) {  // Y divergence rows y2 = 2w d2 (no score dependence): G3 / G2 div halves
-          const float2 wab = *reinterpret_cast<const float2*>(&S.w[p0 + pp]);  // one 8-B load
-          y2v[pp] = (wab.x + wab.x) * d0[3];
-          y2v[pp + 1] = (wab.y + wab.y) * d1[3];
+        for (int pp = 0; pp < kPPT; pp += 2) {  // two particles per f32x2 lane pair
+          const f2 a2 = add2(mk2(va[pp], va[pp + 1]), mk2(bb2, bb2));
+          const f2 sg = sigmoid2(a2);
+          const f2 h2 = mul2(a2, sg);
+          float* d0 = pp < 8 ? &v32[4 * pp] : &v16[4 * (pp - 8)];
+          float* d1 = d0 + 4;
+          un2(mul2(mk2(w3[0], w3[0]), h2), d0[0], d1[0]);
+          un2(mul2(mk2(w3[1], w3[1]), h2), d0[1], d1[1]);
+          un2(mul2(mk2(w3[2], w3[2]), h2), d0[2], d1[2]);
+          // d2 = silu'(a2) for now; times e (the div half of G1) below
+          un2(DIV ? mul2(sg, fma2(a2, sub2(one2, sg), one2)) : mk2(0.f, 0.f), d0[3], d1[3]);
+          if (DIV) {  // Y divergence rows y2 = 2w d2 (no score dependence): G3 / G2 div halves
+            const float2 wab = *reinterpret_cast<const float2*>(&S.w[p0 + pp]);  // one 8-B load
+            const int j = pp >> 1;
+            const int slot = HF ? (j < 2 ? j : j - 2) : (j < 4 ? j : j - 4);
+            split2((wab.x + wab.x) * d0[3], (wab.y + wab.y) * d1[3], yh[slot], yl[slot]);
+            const uint32_t a8y = xa8 + kY + kDivRows, a4y = xa4 + kY + kDivRows;
+            if (HF ? j == 1 : j == 5) {
+              sts64(a4y, yh[0], yh[1]);
+              sts64(a4y + kXTile, yl[0], yl[1]);
+            }
+            if (HF ? j == 5 : j == 3) {
+              sts128(a8y, yh[0], yh[1], yh[2], yh[3]);
+              sts128(a8y + kXTile, yl[0], yl[1], yl[2], yl[3]);
+            }
+          }
         }
-      }
+      };
+      if (half_first) f2a_loop(std::true_type{}); else f2a_loop(std::false_type{});
       if (DIV) {
-        store_act12(xa8 + kY + kDivRows, xa4 + kY + kDivRows, half_first, y2v);
         fence_proxy_async();
         umma::fence_before();
         handoff_arrive(9);
