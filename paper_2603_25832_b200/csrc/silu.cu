@@ -172,19 +172,15 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
   return v[0];
 }
 
-// lanes l and l ^ 16 end with the warp-wide sum of v[l & 15] (31 shuffles for 16 values)
+// lanes l and l ^ 16 end with the warp-wide sum of v[l & 15]: the four butterfly levels leave
+// each lane the half-warp sum of one value, one xor-16 exchange finishes it (16 shuffles for 16
+// values; exchanging all 16 values across the half-warps first took 31)
 __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
-#pragma unroll
-  for (int i = 0; i < 16; i += 2) {
-    const float r0 = __shfl_xor_sync(0xffffffffu, v[i], 16);
-    const float r1 = __shfl_xor_sync(0xffffffffu, v[i + 1], 16);
-    un2(add2(mk2(v[i], v[i + 1]), mk2(r0, r1)), v[i], v[i + 1]);
-  }
   butterfly<8>(v, lane);
   butterfly<4>(v, lane);
   butterfly<2>(v, lane);
   butterfly<1>(v, lane);
-  return v[0];
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
 
 __device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one warpgroup
